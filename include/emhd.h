@@ -1,0 +1,174 @@
+/*
+ * emhd.h — C ABI of the B200-native EpiRK/Krylov hot path (libemhd.so).
+ *
+ * The reference (arxiv/paper_1604_02614, package `expmhd`) is pure Python:
+ * its "plugin boundary" for this path is the set of Python callables the
+ * EpiRK integrator hands to the Krylov layer.  Each entry point below
+ * replaces one of them; the reference file:line it stands in for is cited
+ * on the declaration.  A Python mirror with the reference's own names and
+ * signatures (paper_1604_02614_b200/) binds these through ctypes — see
+ * INTEGRATION.md for the binding a maintainer of `expmhd` would add.
+ *
+ * Conventions
+ *  - every vector pointer is a DEVICE pointer (fp64, caller-owned);
+ *  - calls are asynchronous and ordered on the context's CUDA stream
+ *    (emhd_set_stream); only emhd_status_read synchronises;
+ *  - state layout is the reference's (8, nx, ny) C order, y fastest
+ *    (mhd.py:99-103); a rank of a slab decomposition holds nx local rows;
+ *  - halos: optional [2 sides][8 fields][2 rows][ny] buffers holding the two
+ *    rows below row 0 and above row nx-1 (bc EMHD_BC_EXTERNAL sides only);
+ *  - return 0 on success, an EMHD_ERR_* code otherwise; numerical failures
+ *    (admissibility, non-finite Jv, dense overflow) are reported through the
+ *    device status word and mapped by the host to the reference's exception
+ *    types (AdmissibilityError, FloatingPointError).
+ *  - a context is not thread-safe; one host thread per GPU.
+ */
+#ifndef EMHD_H
+#define EMHD_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMHD_OK 0
+#define EMHD_ERR_DENSITY 1
+#define EMHD_ERR_PRESSURE 2
+#define EMHD_ERR_NONFINITE 3
+#define EMHD_ERR_CUDA 4
+#define EMHD_ERR_ARG 6
+#define EMHD_ERR_DENSE 7
+
+#define EMHD_BC_PERIODIC 0
+#define EMHD_BC_REFLECT 1
+#define EMHD_BC_ZEROGRAD 2
+#define EMHD_BC_EXTERNAL 3
+
+/* status flag bits */
+#define EMHD_ST_RHO 1
+#define EMHD_ST_PRESSURE 2
+#define EMHD_ST_NONFINITE 4
+#define EMHD_ST_BREAKDOWN 8
+#define EMHD_ST_DENSE 16
+
+typedef struct emhd_ctx emhd_ctx;
+
+/* Grid2D (mhd.py:31-64) + BoundaryPolicy (mhd.py:84-96) + slab placement */
+typedef struct emhd_geometry {
+  int nx, ny;              /* local rows (x), columns (y) */
+  int nx_global;           /* global rows */
+  int x_offset;            /* global index of local row 0 */
+  double hx, hy;           /* (x_hi - x_lo)/nx_global, (y_hi - y_lo)/ny */
+  int bc_x_lo, bc_x_hi;    /* EMHD_BC_*; EXTERNAL = rows come from a halo buffer */
+  int bc_y;                /* EMHD_BC_PERIODIC / REFLECT / ZEROGRAD */
+} emhd_geometry;
+
+/* MhdParams (mhd.py:67-81) + make_rhs(check=) (mhd.py:280) */
+typedef struct emhd_physics {
+  double mu, eta, kappa, gamma;
+  int b_half;
+  int check;
+} emhd_physics;
+
+typedef struct emhd_status {
+  int flags;                           /* EMHD_ST_* bits seen since the last reset */
+  int rhs_evals;                       /* stencil evaluations executed (device-counted) */
+  unsigned long long first_nonfinite;  /* flat index of the first non-finite F(a+sigma v) */
+  int breakdown;                       /* Arnoldi lucky breakdown seen */
+  int pad;
+} emhd_status;
+
+/* ---- context -------------------------------------------------------- */
+const char* emhd_version(void);
+const char* emhd_error_string(int code);
+int emhd_ctx_create(emhd_ctx** ctx, const emhd_geometry* g, const emhd_physics* p, int max_vectors);
+int emhd_ctx_destroy(emhd_ctx* ctx);
+int emhd_set_stream(emhd_ctx* ctx, void* cuda_stream);
+int emhd_num_sms(emhd_ctx* ctx);
+/* synchronous read of the device status word (stream-ordered) */
+int emhd_status_read(emhd_ctx* ctx, emhd_status* out);
+int emhd_status_reset(emhd_ctx* ctx);
+
+/* ---- (a) right-hand side ------------------------------------------- */
+/* F = rhs(u)   — replaces make_rhs(...)(y) / rhs(U, params, grid, bc)  mhd.py:269-285 */
+int emhd_rhs(emhd_ctx* ctx, const double* u, const double* u_halo, double* F);
+
+/* ---- (b) finite-difference Jacobian action ------------------------- */
+/* out = (F(a + sigma v) - F(a)) / sigma, sigma from *d_vnorm = ||v||_inf on device;
+ * ||v||_inf == 0 -> zeros, no RHS evaluation.
+ * Replaces FdJacobianOperator._apply  fdjac.py:38-49 */
+int emhd_jv(emhd_ctx* ctx, const double* a, const double* a_halo, const double* fa,
+            const double* v, const double* v_halo, const double* d_vnorm, double* out);
+
+/* Augmented apply of phi_comb (krylov.py:268-273): top = ch*J u + sum_k bcol[k]*q[bidx[k]],
+ * bottom = upshift(q); x = [u; q] with q = d_q (length p).  nb <= 5, p <= 5. */
+int emhd_jv_aug(emhd_ctx* ctx, const double* a, const double* a_halo, const double* fa,
+                const double* u, const double* u_halo, const double* d_vnorm, const double* d_q,
+                int p, double ch, int nb, const double* const* bcol, const int* bidx, double* out);
+
+/* Fused Arnoldi operator step: v_j = w/h (written to v_out, incl. the p-entry tail),
+ * out = J v_j (plain, or augmented when p > 0).  d_scal = {h_next, max|w_top|}.
+ * Replaces V[:, j+1] = w / hnext (krylov.py:167) followed by apply(V[:, j]) (:149). */
+int emhd_jv_normalized(emhd_ctx* ctx, const double* a, const double* a_halo, const double* fa,
+                       const double* w, const double* w_halo, const double* d_scal, double* v_out,
+                       int p, double ch, int nb, const double* const* bcol, const int* bidx,
+                       double* out);
+
+/* ---- (c) Arnoldi step pieces (krylov.py:144-168) ------------------- */
+/* out[i] = <w, V_i> for i < nvec over len_dot; self: out[nvec] = <w, w> */
+int emhd_multidot(emhd_ctx* ctx, const double* w, const double* V, long long ldv, int nvec,
+                  long long len_dot, int self, double* out);
+/* w[:len_upd] -= sum_i h[i] V_i; mode 0: out[i] = <w, V_i> (len_dot);
+ * mode 1: out = {sum w^2 over len_dot, max|w| over len_max} */
+int emhd_update(emhd_ctx* ctx, double* w, const double* V, long long ldv, int nvec, const double* h,
+                long long len_upd, long long len_dot, long long len_max, int mode, double* out);
+/* out = {sum x^2 over len_sum, max|x| over len_max} */
+int emhd_norms(emhd_ctx* ctx, const double* x, long long len_sum, long long len_max, double* out);
+/* H[:j+1, j] = h1 + h2; hnext = sqrt(nrm[0]); breakdown if hnext <= 1e-12 max(sqrt(selfdot), 1);
+ * scal = {hnext, nrm[1], breakdown} */
+int emhd_arnoldi_finish(emhd_ctx* ctx, const double* h1, const double* h2, const double* nrm,
+                        const double* selfdot, int j, double* H, long long ldh, double* scal);
+/* out = x / d (d = sqrt(*d) when take_sqrt); d_out receives d.  (krylov.py:137, :167) */
+int emhd_div_scalar(emhd_ctx* ctx, const double* x, const double* d, int take_sqrt, double* out,
+                    double* d_out, long long n);
+
+/* ---- small dense phi (phifuncs.py:65-107, krylov.py:209-238,378-383) */
+/* For s < S: y_s = beta * phi_order(scales[s] * H_m) e_1, res[s] = |h_next| |y_s[m-1]| / ||y_s||
+ * * res_scale[s]; scales/res_scale/scal/beta/Y/res are device pointers. */
+int emhd_phi_small(emhd_ctx* ctx, const double* H, long long ldh, int m, int order, int S,
+                   const double* scales, const double* res_scale, const double* scal,
+                   const double* beta, double* Y, double* res);
+
+/* E = expm(A), n x n row-major device matrices; work: device scratch of n + 4 doubles.
+ * Synchronous.  (scipy.linalg.expm as called by phi_dense, phifuncs.py:97,104) */
+int emhd_expm(emhd_ctx* ctx, const double* A, int n, double* E, double* work);
+
+/* ---- (d) combinations ---------------------------------------------- */
+/* outs[s] = base[s] + coef[s] * (V_m Y[s]) (base[s] may be NULL: outs[s] = V_m Y[s]); S <= 4.
+ * Replaces Vm @ y (krylov.py:316, 374) fused with the stage axpys (epirk.py:207, 251-252). */
+int emhd_combine(emhd_ctx* ctx, const double* V, long long ldv, int m, const double* Y, int S,
+                 const double* const* base, const double* coef, double* const* outs, long long len);
+/* out = post * (t_0 + t_1 + ...), t_k = c_k x_k (has_c[k]) or x_k, left to right, no FMA;
+ * max_out (optional): max|out| over the first len_max entries.  (epirk.py stage algebra) */
+int emhd_lincomb(emhd_ctx* ctx, int nterms, const double* const* x, const double* c, const int* has_c,
+                 double post, int has_post, double* out, long long n, long long len_max,
+                 double* max_out);
+/* out[0] = sum_e (err_e / (tol + tol |y_e|))^2  (StepController.error_norm, epirk.py:156-158) */
+int emhd_wrms(emhd_ctx* ctx, const double* err, const double* y, double tol, long long n, double* out);
+
+/* ---- diagnostics --------------------------------------------------- */
+/* Synchronous error-path report of the state a stencil call in `mode` (0 RHS, 1 Jv, 2 normalised
+ * Jv) evaluated: report = {int which (1 density, 2 pressure, 0 none), int i, int j, int pad,
+ * double value}, (i, j) the first minimising cell of the ghost-padded field, as the reference's
+ * AdmissibilityError names it (mhd.py:111-131). */
+int emhd_admissibility_report(emhd_ctx* ctx, int mode, const double* a, const double* a_halo,
+                              const double* v, const double* v_halo, const double* scal,
+                              void* report);
+
+/* ---- slab halos ------------------------------------------------------ */
+/* sendbuf[2][8][2][ny] = rows {0,1} and {nx-2, nx-1} of every field of x */
+int emhd_pack_edges(emhd_ctx* ctx, const double* x, double* sendbuf);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMHD_H */

@@ -1,0 +1,384 @@
+// C ABI of libemhd.so (declared in include/emhd.h).
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include "../../include/emhd.h"
+#include "emhd_common.cuh"
+#include "stencil.cuh"
+#include "krylov.cuh"
+#include "dense.cuh"
+#include "vecops.cuh"
+
+using namespace emhd;
+
+struct emhd_ctx {
+  emhd_geometry g;
+  emhd_physics p;
+  cudaStream_t stream = 0;
+  int device = 0;
+  int num_sms = 148;
+  int max_vectors = 0;
+  double* partials = nullptr;         // reduction scratch
+  size_t partials_len = 0;
+  unsigned int* ticket = nullptr;
+  DevStatus* st = nullptr;
+  DevStatus* st_host = nullptr;       // pinned mirror
+  double* dense = nullptr;            // dense workspace
+  size_t dense_len = 0;
+  StencilParams base{};
+};
+
+static int cerr(cudaError_t e) {
+  if (e == cudaSuccess) return EMHD_OK;
+  std::fprintf(stderr, "libemhd: CUDA error %s\n", cudaGetErrorString(e));
+  return EMHD_ERR_CUDA;
+}
+
+extern "C" const char* emhd_version(void) { return "emhd-b200 0.1 (sm_100a)"; }
+
+extern "C" const char* emhd_error_string(int code) {
+  switch (code) {
+    case EMHD_OK: return "ok";
+    case EMHD_ERR_DENSITY: return "non-positive density";
+    case EMHD_ERR_PRESSURE: return "non-positive pressure";
+    case EMHD_ERR_NONFINITE: return "non-finite rhs value during Jacobian apply";
+    case EMHD_ERR_CUDA: return "CUDA error";
+    case EMHD_ERR_ARG: return "bad argument";
+    case EMHD_ERR_DENSE: return "non-finite small dense exponential";
+    default: return "unknown";
+  }
+}
+
+static void fill_base(emhd_ctx* c) {
+  StencilParams& P = c->base;
+  std::memset(&P, 0, sizeof(P));
+  P.nx = c->g.nx; P.ny = c->g.ny; P.nxg = c->g.nx_global; P.x_off = c->g.x_offset;
+  P.bcx_lo = c->g.bc_x_lo; P.bcx_hi = c->g.bc_x_hi; P.bcy = c->g.bc_y;
+  P.rows_per_cta = 0;
+  P.check = c->p.check;
+  const double g = c->p.gamma;
+  P.gm1 = g - 1.0;
+  P.mu = c->p.mu; P.eta = c->p.eta;
+  P.heat = g * c->p.mu * c->p.kappa / (g - 1.0);          // mhd.py:259
+  P.bfac = c->p.b_half ? 0.5 : 1.0;                         // mhd.py:108
+  P.two_hx = 2.0 * c->g.hx; P.r_two_hx = 1.0 / P.two_hx;    // mhd.py:202
+  P.two_hy = 2.0 * c->g.hy; P.r_two_hy = 1.0 / P.two_hy;    // mhd.py:206
+  P.n_top = (long long)NF * c->g.nx * c->g.ny;
+  P.st = c->st;
+}
+
+extern "C" int emhd_ctx_create(emhd_ctx** out, const emhd_geometry* g, const emhd_physics* p,
+                               int max_vectors) {
+  if (!out || !g || !p) return EMHD_ERR_ARG;
+  if (g->nx < 2 || g->ny < 4 || g->nx_global < g->nx || g->hx <= 0 || g->hy <= 0) return EMHD_ERR_ARG;
+  if (g->bc_y < 0 || g->bc_y > 2 || g->bc_x_lo < 0 || g->bc_x_lo > 3 || g->bc_x_hi < 0 || g->bc_x_hi > 3)
+    return EMHD_ERR_ARG;
+  emhd_ctx* c = new (std::nothrow) emhd_ctx();
+  if (!c) return EMHD_ERR_ARG;
+  c->g = *g;
+  c->p = *p;
+  c->max_vectors = max_vectors < 8 ? 8 : max_vectors;
+  int rc = cerr(cudaGetDevice(&c->device));
+  if (!rc) rc = cerr(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  c->partials_len = (size_t)(c->max_vectors + 8) * 4 * c->num_sms + 64;
+  if (!rc) rc = cerr(cudaMalloc(&c->partials, c->partials_len * sizeof(double)));
+  if (!rc) rc = cerr(cudaMalloc(&c->ticket, 16 * sizeof(unsigned int)));
+  if (!rc) rc = cerr(cudaMemset(c->ticket, 0, 16 * sizeof(unsigned int)));
+  if (!rc) rc = cerr(cudaMalloc(&c->st, sizeof(DevStatus)));
+  if (!rc) rc = cerr(cudaMallocHost(&c->st_host, sizeof(DevStatus)));
+  if (rc) { emhd_ctx_destroy(c); return rc; }
+  fill_base(c);
+  emhd_status_reset(c);
+  rc = cerr(cudaStreamSynchronize(0));
+  *out = c;
+  return rc;
+}
+
+extern "C" int emhd_ctx_destroy(emhd_ctx* c) {
+  if (!c) return EMHD_OK;
+  cudaFree(c->partials);
+  cudaFree(c->ticket);
+  cudaFree(c->st);
+  cudaFree(c->dense);
+  if (c->st_host) cudaFreeHost(c->st_host);
+  delete c;
+  return EMHD_OK;
+}
+
+extern "C" int emhd_set_stream(emhd_ctx* c, void* s) {
+  if (!c) return EMHD_ERR_ARG;
+  c->stream = (cudaStream_t)s;
+  return EMHD_OK;
+}
+
+extern "C" int emhd_num_sms(emhd_ctx* c) { return c ? c->num_sms : 0; }
+
+extern "C" int emhd_status_reset(emhd_ctx* c) {
+  if (!c) return EMHD_ERR_ARG;
+  DevStatus h{};
+  h.first_nonfinite = ~0ull;
+  // small H2D copy from a stack value must complete before return: use the pinned mirror
+  *c->st_host = h;
+  int rc = cerr(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevStatus), cudaMemcpyHostToDevice, c->stream));
+  if (!rc) rc = cerr(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
+extern "C" int emhd_status_read(emhd_ctx* c, emhd_status* out) {
+  if (!c || !out) return EMHD_ERR_ARG;
+  int rc = cerr(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream));
+  if (!rc) rc = cerr(cudaStreamSynchronize(c->stream));
+  if (rc) return rc;
+  out->flags = c->st_host->flags;
+  out->rhs_evals = c->st_host->rhs_evals;
+  out->first_nonfinite = c->st_host->first_nonfinite;
+  out->breakdown = c->st_host->breakdown;
+  out->pad = 0;
+  return EMHD_OK;
+}
+
+static void set_epilogue(StencilParams& P, int p, double ch, int nb, const double* const* bcol,
+                         const int* bidx) {
+  P.p = p;
+  P.ch = ch;
+  P.nb = nb;
+  for (int k = 0; k < 5; ++k) { P.bcol[k] = nullptr; P.bidx[k] = 0; }
+  for (int k = 0; k < nb; ++k) { P.bcol[k] = bcol[k]; P.bidx[k] = bidx[k]; }
+}
+
+extern "C" int emhd_rhs(emhd_ctx* c, const double* u, const double* u_halo, double* F) {
+  if (!c || !u || !F) return EMHD_ERR_ARG;
+  StencilParams P = c->base;
+  P.a = u; P.a_halo = u_halo; P.out = F;
+  return cerr(launch_stencil(P, MODE_RHS, false, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_jv(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
+                       const double* v, const double* v_halo, const double* d_vnorm, double* out) {
+  if (!c || !a || !fa || !v || !d_vnorm || !out) return EMHD_ERR_ARG;
+  StencilParams P = c->base;
+  P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = v; P.v_halo = v_halo; P.scal = d_vnorm; P.out = out;
+  return cerr(launch_stencil(P, MODE_JV, false, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_jv_aug(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
+                           const double* u, const double* u_halo, const double* d_vnorm, const double* d_q,
+                           int p, double ch, int nb, const double* const* bcol, const int* bidx,
+                           double* out) {
+  if (!c || !a || !fa || !u || !d_vnorm || !out || p < 1 || p > 5 || nb < 0 || nb > 5 || !d_q)
+    return EMHD_ERR_ARG;
+  StencilParams P = c->base;
+  P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = u; P.v_halo = u_halo; P.scal = d_vnorm; P.out = out;
+  P.qsrc = d_q;
+  set_epilogue(P, p, ch, nb, bcol, bidx);
+  return cerr(launch_stencil(P, MODE_JV, true, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_jv_normalized(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
+                                  const double* w, const double* w_halo, const double* d_scal,
+                                  double* v_out, int p, double ch, int nb, const double* const* bcol,
+                                  const int* bidx, double* out) {
+  if (!c || !a || !fa || !w || !d_scal || !v_out || !out || p < 0 || p > 5 || nb < 0 || nb > 5)
+    return EMHD_ERR_ARG;
+  StencilParams P = c->base;
+  P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = w; P.v_halo = w_halo; P.scal = d_scal;
+  P.out = out; P.vout = v_out;
+  set_epilogue(P, p, ch, nb, bcol, bidx);
+  return cerr(launch_stencil(P, MODE_JVN, p > 0, c->num_sms, c->stream));
+}
+
+static KWork kwork(emhd_ctx* c) {
+  KWork w;
+  w.partials = c->partials;
+  w.ticket = c->ticket;
+  w.num_sms = c->num_sms;
+  return w;
+}
+
+extern "C" int emhd_multidot(emhd_ctx* c, const double* w, const double* V, long long ldv, int nvec,
+                             long long len_dot, int self, double* out) {
+  if (!c || !w || !out || nvec < 0 || nvec > c->max_vectors || (nvec > 0 && !V)) return EMHD_ERR_ARG;
+  KWork k = kwork(c);
+  return cerr(launch_multidot(w, V, ldv, nvec, len_dot, self ? 1 : 0, k, out, c->stream));
+}
+
+extern "C" int emhd_update(emhd_ctx* c, double* w, const double* V, long long ldv, int nvec, const double* h,
+                           long long len_upd, long long len_dot, long long len_max, int mode, double* out) {
+  if (!c || !w || !out || nvec < 0 || nvec > c->max_vectors || (nvec > 0 && (!V || !h))) return EMHD_ERR_ARG;
+  KWork k = kwork(c);
+  return cerr(launch_update(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode, k, out, c->stream));
+}
+
+extern "C" int emhd_norms(emhd_ctx* c, const double* x, long long len_sum, long long len_max, double* out) {
+  if (!c || !x || !out) return EMHD_ERR_ARG;
+  KWork k = kwork(c);
+  return cerr(launch_norms(x, len_sum, len_max, k, out, c->stream));
+}
+
+extern "C" int emhd_arnoldi_finish(emhd_ctx* c, const double* h1, const double* h2, const double* nrm,
+                                   const double* selfdot, int j, double* H, long long ldh, double* scal) {
+  if (!c || !h1 || !h2 || !nrm || !selfdot || !H || !scal || j < 0) return EMHD_ERR_ARG;
+  return cerr(launch_arnoldi_finish(h1, h2, nrm, selfdot, j, H, ldh, scal, c->st, 1e-12, c->stream));
+}
+
+extern "C" int emhd_div_scalar(emhd_ctx* c, const double* x, const double* d, int take_sqrt, double* out,
+                               double* d_out, long long n) {
+  if (!c || !x || !d || !out) return EMHD_ERR_ARG;
+  return cerr(launch_div_scalar(x, d, take_sqrt, out, d_out, n, c->num_sms, c->stream));
+}
+
+static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, int order, int S,
+                          const double* scales, const double* res_scale, const double* scal,
+                          const double* beta, double* Y, double* res, double* E_out) {
+  if (!c || !H || m < 1 || order < 0 || order > 4 || S < 1 || S > DENSE_MAX_SCALES || !scales ||
+      !res_scale || !beta || !Y || !res)
+    return EMHD_ERR_ARG;
+  const size_t n = (size_t)(order + 1) * m;
+  const size_t per = 11 * n * n + 3 * n + 64;
+  const size_t need = per * S;
+  if (need > c->dense_len) {
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return cerr(e);
+    cudaFree(c->dense);
+    c->dense = nullptr;
+    c->dense_len = 0;
+    size_t want = need < (size_t)4 * 11 * 256 * 256 ? (size_t)4 * 11 * 256 * 256 + 4096 : need;
+    e = cudaMalloc(&c->dense, want * sizeof(double));
+    if (e != cudaSuccess) return cerr(e);
+    c->dense_len = want;
+  }
+  PhiSmallArgs P;
+  std::memset(&P, 0, sizeof(P));
+  P.H = H; P.ldh = ldh; P.m = m; P.order = order; P.scales = scales; P.res_scale = res_scale;
+  P.scal = scal; P.beta = beta; P.Y = Y; P.res = res; P.st = c->st; P.E_out = E_out;
+  for (int s = 0; s < S; ++s) {
+    double* b = c->dense + per * s;
+    size_t nn = n * n;
+    P.work[s].a = b;
+    P.work[s].e = b + nn;
+    for (int k = 0; k < 7; ++k) P.work[s].m[k] = b + (2 + k) * nn;
+    P.work[s].m[7] = b + 9 * nn;     // n x 2n
+    P.work[s].vec = b + 11 * nn;
+  }
+  return cerr(launch_phi_small(P, S, c->stream));
+}
+
+extern "C" int emhd_phi_small(emhd_ctx* c, const double* H, long long ldh, int m, int order, int S,
+                              const double* scales, const double* res_scale, const double* scal,
+                              const double* beta, double* Y, double* res) {
+  return phi_small_impl(c, H, ldh, m, order, S, scales, res_scale, scal, beta, Y, res, nullptr);
+}
+
+// E = expm(A) for an n x n device matrix (scratch: 4 doubles + n doubles in `work`)
+extern "C" int emhd_expm(emhd_ctx* c, const double* A, int n, double* E, double* work) {
+  if (!c || !A || !E || !work || n < 1) return EMHD_ERR_ARG;
+  // work = {scale=1, res_scale=1, beta=1, res, Y[n]}
+  double ones[3] = {1.0, 1.0, 1.0};
+  int rc = cerr(cudaMemcpyAsync(work, ones, sizeof(ones), cudaMemcpyHostToDevice, c->stream));
+  if (rc) return rc;
+  rc = phi_small_impl(c, A, n, n, 0, 1, work, work + 1, nullptr, work + 2, work + 4, work + 3, E);
+  if (!rc) rc = cerr(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
+extern "C" int emhd_combine(emhd_ctx* c, const double* V, long long ldv, int m, const double* Y, int S,
+                            const double* const* base, const double* coef, double* const* outs,
+                            long long len) {
+  if (!c || !V || !Y || S < 1 || S > 4 || m < 1 || !outs) return EMHD_ERR_ARG;
+  CombineOut co;
+  for (int s = 0; s < 4; ++s) {
+    co.base[s] = (s < S && base) ? base[s] : nullptr;
+    co.coef[s] = (s < S && coef) ? coef[s] : 1.0;
+    co.out[s] = s < S ? outs[s] : nullptr;
+  }
+  return cerr(launch_combine(V, ldv, m, Y, S, co, len, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_lincomb(emhd_ctx* c, int nterms, const double* const* x, const double* cc,
+                            const int* has_c, double post, int has_post, double* out, long long n,
+                            long long len_max, double* max_out) {
+  if (!c || nterms < 1 || nterms > 6 || !x || !out) return EMHD_ERR_ARG;
+  LinComb L;
+  std::memset(&L, 0, sizeof(L));
+  for (int k = 0; k < nterms; ++k) {
+    if (!x[k]) return EMHD_ERR_ARG;
+    L.x[k] = x[k];
+    L.has_c[k] = has_c ? has_c[k] : 0;
+    L.c[k] = cc ? cc[k] : 1.0;
+  }
+  L.nterms = nterms;
+  L.post = post;
+  L.has_post = has_post;
+  L.out = out;
+  return cerr(launch_lincomb(L, n, len_max, c->partials, max_out, c->ticket, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_wrms(emhd_ctx* c, const double* err, const double* y, double tol, long long n,
+                         double* out) {
+  if (!c || !err || !y || !out) return EMHD_ERR_ARG;
+  return cerr(launch_wrms(err, y, tol, n, c->partials, out, c->ticket, c->num_sms, c->stream));
+}
+
+__global__ void pack_edges_kernel(const double* x, double* buf, int nx, int ny) {
+  // buf[side][f][r][j]: side 0 = rows {0,1}, side 1 = rows {nx-2, nx-1}
+  const long long total = 2LL * NF * 2 * ny;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e % ny);
+    long long q = e / ny;
+    const int r = (int)(q % 2); q /= 2;
+    const int f = (int)(q % NF);
+    const int side = (int)(q / NF);
+    const int row = side == 0 ? r : nx - 2 + r;
+    buf[e] = x[((long long)f * nx + row) * ny + j];
+  }
+}
+
+extern "C" int emhd_pack_edges(emhd_ctx* c, const double* x, double* sendbuf) {
+  if (!c || !x || !sendbuf) return EMHD_ERR_ARG;
+  const long long total = 2LL * NF * 2 * c->g.ny;
+  int G = (int)((total + 255) / 256);
+  pack_edges_kernel<<<G, 256, 0, c->stream>>>(x, sendbuf, c->g.nx, c->g.ny);
+  return cerr(cudaGetLastError());
+}
+
+struct emhd_report_s { int which, i, j, pad; double value; };
+
+// Admissibility diagnostics of the state a stencil call saw (error path only):
+// which = 1 (density) / 2 (pressure) / 0, with the reference's padded-field
+// argmin cell (mhd.py:111-131) and its value.
+extern "C" int emhd_admissibility_report(emhd_ctx* c, int mode, const double* a, const double* a_halo,
+                                         const double* v, const double* v_halo, const double* scal,
+                                         void* report) {
+  if (!c || !a || !report || mode < 0 || mode > 2) return EMHD_ERR_ARG;
+  StencilParams P = c->base;
+  P.a = a; P.a_halo = a_halo; P.v = v; P.v_halo = v_halo; P.scal = scal;
+  unsigned long long* keys = nullptr;
+  int rc = cerr(cudaMalloc(&keys, 4 * sizeof(unsigned long long)));
+  if (rc) return rc;
+  unsigned long long init[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+  unsigned long long host[4];
+  rc = cerr(cudaMemcpy(keys, init, sizeof(init), cudaMemcpyHostToDevice));
+  if (!rc) rc = cerr(launch_admissibility(P, mode, keys, c->stream));
+  if (!rc) rc = cerr(cudaStreamSynchronize(c->stream));
+  if (!rc) rc = cerr(cudaMemcpy(host, keys, sizeof(host), cudaMemcpyDeviceToHost));
+  cudaFree(keys);
+  if (rc) return rc;
+  auto val = [](unsigned long long k) {
+    unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    double d;
+    std::memcpy(&d, &b, sizeof(d));
+    return d;
+  };
+  emhd_report_s* R = (emhd_report_s*)report;
+  const int W = c->g.ny + 4;
+  R->which = 0; R->i = R->j = -1; R->pad = 0; R->value = 0.0;
+  const double rmin = val(host[0]), pmin = val(host[1]);
+  if (host[0] != ~0ull && rmin <= 0.0 && c->p.check) {
+    R->which = 1; R->i = (int)(host[2] / W); R->j = (int)(host[2] % W); R->value = rmin;
+  } else if (host[1] != ~0ull && pmin <= 0.0 && c->p.check) {
+    R->which = 2; R->i = (int)(host[3] / W); R->j = (int)(host[3] % W); R->value = pmin;
+  }
+  if (R->which && c->g.x_offset) R->i += c->g.x_offset;
+  return EMHD_OK;
+}

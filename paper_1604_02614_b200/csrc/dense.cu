@@ -1,0 +1,369 @@
+// Small dense phi-functions of the Krylov Hessenberg matrix, on the GPU.
+//
+// Replaces reference pkg/src/expmhd/phifuncs.py:65-107 (phi_dense: one
+// exponential of the block upper-bidiagonal augmented matrix) and
+// krylov.py:209-238, 378-383 (residual_estimate, _expm_seed, _phi_seed).
+// The exponential is the Al-Mohy & Higham (2009) Pade scaling-and-squaring
+// algorithm with exact 1-norms — the algorithm scipy.linalg.expm (the
+// reference's third-party dependency, scipy 1.18.1) implements — run by one
+// CTA per requested scale: degree selection, Pade numerator/denominator,
+// Gauss–Jordan solve with partial pivoting and the squarings all stay on the
+// device, so a residual check costs one launch and one 8-byte read.
+#include <math.h>
+#include "emhd_common.cuh"
+#include "dense.cuh"
+
+namespace emhd {
+
+constexpr int DT = 512;   // threads per CTA
+
+// C = alpha * A * B (+ beta * C0 when C0 given); n x n row-major, ld = n.
+__device__ void mm(double* C, const double* A, const double* B, int n, double* sA, double* sB) {
+  // 64x64 output tiles, 16-wide k steps; thread owns a 4 x 2 micro-tile
+  const int t = threadIdx.x;
+  const int tr = (t / 32) * 4;      // 16 row-groups of 4
+  const int tc = (t % 32) * 2;      // 32 col-groups of 2
+  for (int bi = 0; bi < n; bi += 64) {
+    for (int bj = 0; bj < n; bj += 64) {
+      double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+      for (int bk = 0; bk < n; bk += 16) {
+        // load A[bi:bi+64, bk:bk+16] and B[bk:bk+16, bj:bj+64]
+        for (int q = t; q < 64 * 16; q += DT) {
+          int r = q / 16, c = q % 16;
+          int gr = bi + r, gc = bk + c;
+          sA[r * 17 + c] = (gr < n && gc < n) ? A[gr * n + gc] : 0.0;
+          int r2 = q / 64, c2 = q % 64;
+          int gr2 = bk + r2, gc2 = bj + c2;
+          sB[r2 * 64 + c2] = (gr2 < n && gc2 < n) ? B[gr2 * n + gc2] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const double b0 = sB[k * 64 + tc], b1 = sB[k * 64 + tc + 1];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double a = sA[(tr + u) * 17 + k];
+            acc[u][0] = fma(a, b0, acc[u][0]);
+            acc[u][1] = fma(a, b1, acc[u][1]);
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int gr = bi + tr + u, gc = bj + tc + v;
+          if (gr < n && gc < n) C[gr * n + gc] = acc[u][v];
+        }
+    }
+  }
+  __syncthreads();
+}
+
+// 1-norm (max column sum) of an n x n matrix
+__device__ double norm1(const double* A, int n, double* red) {
+  double best = 0.0;
+  for (int c = threadIdx.x; c < n; c += DT) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += fabs(A[r * n + c]);
+    best = fmax(best, s);
+  }
+  best = warp_max(best);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < DT / 32; ++w) b = fmax(b, red[w]);
+    red[DT / 32] = b;
+  }
+  __syncthreads();
+  const double r = red[DT / 32];
+  __syncthreads();
+  return r;
+}
+
+// || |A|^p ||_1 via p row-vector products 1^T |A| ... |A|
+__device__ double norm1_abs_power(const double* A, int n, int p, double* x, double* y, double* red) {
+  for (int i = threadIdx.x; i < n; i += DT) x[i] = 1.0;
+  __syncthreads();
+  for (int k = 0; k < p; ++k) {
+    for (int c = threadIdx.x; c < n; c += DT) {
+      double s = 0.0;
+      for (int r = 0; r < n; ++r) s += x[r] * fabs(A[r * n + c]);
+      y[c] = s;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += DT) x[i] = y[i];
+    __syncthreads();
+  }
+  double best = 0.0;
+  for (int i = threadIdx.x; i < n; i += DT) best = fmax(best, x[i]);
+  best = warp_max(best);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < DT / 32; ++w) b = fmax(b, red[w]);
+    red[DT / 32] = b;
+  }
+  __syncthreads();
+  const double r = red[DT / 32];
+  __syncthreads();
+  return r;
+}
+
+// Al-Mohy & Higham backward-error estimate ell(A, m) (exact norms)
+__device__ int ell(const double* A, int n, int m, double a1, double* x, double* y, double* red) {
+  // |c_{2m+1}|^{-1} = C(4m+2, 2m+1) * (4m+3)!
+  const int p = 2 * m + 1;
+  double lg = lgamma(2.0 * p + 1.0) - 2.0 * lgamma((double)p + 1.0) + lgamma(2.0 * p + 2.0);
+  const double nap = norm1_abs_power(A, n, p, x, y, red);
+  if (nap == 0.0 || a1 == 0.0) return 0;
+  // alpha = nap / (a1 * abs_c_recip); value = ceil(log2(alpha / u) / (2m))
+  const double log2_alpha = log2(nap) - log2(a1) - lg / log(2.0);
+  const double v = ceil((log2_alpha + 53.0) / (2.0 * m));
+  return v > 0.0 ? (int)v : 0;
+}
+
+__device__ void axpby_mat(double* out, const double* const* terms, const double* coefs, int nterms,
+                          int n, double diag) {
+  for (int e = threadIdx.x; e < n * n; e += DT) {
+    double s = ((e / n) == (e % n)) ? diag : 0.0;
+    for (int k = 0; k < nterms; ++k) s = fma(coefs[k], terms[k][e], s);
+    out[e] = s;
+  }
+  __syncthreads();
+}
+
+// Gauss–Jordan with partial pivoting on M = [Q | R] (n x 2n): R <- Q^{-1} R
+__device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac) {
+  const int w2 = 2 * n;
+  for (int k = 0; k < n; ++k) {
+    // pivot: largest |M[i][k]| for i >= k, lowest index on ties
+    double best = -1.0; int bi = n;
+    for (int i = k + threadIdx.x; i < n; i += DT) {
+      const double a = fabs(M[i * w2 + k]);
+      if (a > best) { best = a; bi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = best; ired[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0; int ii = n;
+      for (int w = 0; w < DT / 32; ++w)
+        if (red[w] > b || (red[w] == b && ired[w] < ii)) { b = red[w]; ii = ired[w]; }
+      ired[DT / 32] = ii;
+      red[DT / 32] = b;
+    }
+    __syncthreads();
+    const int piv = ired[DT / 32];
+    if (!(red[DT / 32] > 0.0)) return false;
+    if (piv != k)
+      for (int c = threadIdx.x; c < w2; c += DT) {
+        const double a = M[k * w2 + c];
+        M[k * w2 + c] = M[piv * w2 + c];
+        M[piv * w2 + c] = a;
+      }
+    __syncthreads();
+    const double d = M[k * w2 + k];
+    __syncthreads();
+    for (int c = k + threadIdx.x; c < w2; c += DT) M[k * w2 + c] /= d;
+    for (int i = threadIdx.x; i < n; i += DT) fac[i] = (i == k) ? 0.0 : M[i * w2 + k];
+    __syncthreads();
+    const int width = w2 - k - 1;
+    for (int e = threadIdx.x; e < n * width; e += DT) {
+      const int i = e / width, c = k + 1 + e % width;
+      if (i != k) M[i * w2 + c] = fma(-fac[i], M[k * w2 + c], M[i * w2 + c]);
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// E = exp(A), A overwritten by scaling; returns false on failure.
+__device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA, double* sB, double* red,
+                          int* ired) {
+  double* A2 = W.m[0];
+  double* A4 = W.m[1];
+  double* A6 = W.m[2];
+  double* A8 = W.m[3];
+  double* U = W.m[4];
+  double* Vm = W.m[5];
+  double* T = W.m[6];
+  double* M = W.m[7];      // n x 2n
+  double* x = W.vec;
+  double* y = W.vec + n;
+  double* fac = W.vec + 2 * n;
+
+  mm(A2, A, A, n, sA, sB);
+  mm(A4, A2, A2, n, sA, sB);
+  mm(A6, A4, A2, n, sA, sB);
+  const double a1 = norm1(A, n, red);
+  const double d4 = pow(norm1(A4, n, red), 0.25);
+  const double d6 = pow(norm1(A6, n, red), 1.0 / 6.0);
+  const double eta1 = fmax(d4, d6);
+  int mdeg = 0, s = 0;
+  if (eta1 <= 1.495585217958292e-002 && ell(A, n, 3, a1, x, y, red) == 0) mdeg = 3;
+  else if (eta1 <= 2.539398330063230e-001 && ell(A, n, 5, a1, x, y, red) == 0) mdeg = 5;
+  double d8 = 0.0, eta3 = 0.0;
+  if (mdeg == 0) {
+    mm(A8, A4, A4, n, sA, sB);
+    d8 = pow(norm1(A8, n, red), 0.125);
+    eta3 = fmax(d6, d8);
+    if (eta3 <= 9.504178996162932e-001 && ell(A, n, 7, a1, x, y, red) == 0) mdeg = 7;
+    else if (eta3 <= 2.097847961257068e+000 && ell(A, n, 9, a1, x, y, red) == 0) mdeg = 9;
+  }
+  if (mdeg == 0) {
+    mm(T, A4, A6, n, sA, sB);           // A^10
+    const double d10 = pow(norm1(T, n, red), 0.1);
+    const double eta4 = fmax(d8, d10);
+    const double eta5 = fmin(eta3, eta4);
+    s = (eta5 == 0.0) ? 0 : (int)fmax(ceil(log2(eta5 / 4.25)), 0.0);
+    // scale A by 2^-s and the even powers accordingly
+    const double sc = ldexp(1.0, -s);
+    for (int e = threadIdx.x; e < n * n; e += DT) A[e] *= sc;
+    __syncthreads();
+    const double a1s = norm1(A, n, red);
+    s += ell(A, n, 13, a1s, x, y, red);
+    const double sc2 = ldexp(1.0, -s);
+    // rescale from the already-applied 2^-s0 to 2^-s (A), then rebuild powers
+    const double extra = sc2 / sc;
+    for (int e = threadIdx.x; e < n * n; e += DT) A[e] *= extra;
+    __syncthreads();
+    mm(A2, A, A, n, sA, sB);
+    mm(A4, A2, A2, n, sA, sB);
+    mm(A6, A4, A2, n, sA, sB);
+    mdeg = 13;
+  }
+  // Pade numerator (V + U) and denominator (V - U)
+  if (mdeg == 13) {
+    const double b[14] = {64764752532480000., 32382376266240000., 7771770303897600.,
+                          1187353796428800., 129060195264000., 10559470521600.,
+                          670442572800., 33522128640., 1323241920., 40840800., 960960.,
+                          16380., 182., 1.};
+    {
+      const double* tt[3] = {A6, A4, A2};
+      const double cc[3] = {b[13], b[11], b[9]};
+      axpby_mat(T, tt, cc, 3, n, 0.0);
+      mm(U, A6, T, n, sA, sB);
+      const double* t2[4] = {U, A6, A4, A2};
+      const double c2[4] = {1.0, b[7], b[5], b[3]};
+      axpby_mat(T, t2, c2, 4, n, b[1]);
+      mm(U, A, T, n, sA, sB);
+    }
+    {
+      const double* tt[3] = {A6, A4, A2};
+      const double cc[3] = {b[12], b[10], b[8]};
+      axpby_mat(T, tt, cc, 3, n, 0.0);
+      mm(Vm, A6, T, n, sA, sB);
+      const double* t2[4] = {Vm, A6, A4, A2};
+      const double c2[4] = {1.0, b[6], b[4], b[2]};
+      axpby_mat(T, t2, c2, 4, n, b[0]);
+      for (int e = threadIdx.x; e < n * n; e += DT) Vm[e] = T[e];
+      __syncthreads();
+    }
+  } else {
+    double b[10];
+    if (mdeg == 3) { const double c[] = {120., 60., 12., 1.}; for (int k = 0; k < 4; ++k) b[k] = c[k]; }
+    if (mdeg == 5) { const double c[] = {30240., 15120., 3360., 420., 30., 1.}; for (int k = 0; k < 6; ++k) b[k] = c[k]; }
+    if (mdeg == 7) { const double c[] = {17297280., 8648640., 1995840., 277200., 25200., 1512., 56., 1.}; for (int k = 0; k < 8; ++k) b[k] = c[k]; }
+    if (mdeg == 9) { const double c[] = {17643225600., 8821612800., 2075673600., 302702400., 30270240., 2162160., 110880., 3960., 90., 1.}; for (int k = 0; k < 10; ++k) b[k] = c[k]; }
+    const double* pw[4] = {A2, A4, A6, A8};
+    // odd part: A * (b1 I + b3 A2 + b5 A4 + ...); even part: b0 I + b2 A2 + ...
+    const int nt = mdeg / 2;          // number of non-identity even powers
+    double co[4], ce[4];
+    for (int k = 0; k < nt; ++k) { co[k] = b[2 * k + 3]; ce[k] = b[2 * k + 2]; }
+    axpby_mat(T, pw, co, nt, n, b[1]);
+    mm(U, A, T, n, sA, sB);
+    axpby_mat(Vm, pw, ce, nt, n, b[0]);
+  }
+  // M = [V - U | V + U]
+  for (int e = threadIdx.x; e < n * n; e += DT) {
+    const int r = e / n, c = e % n;
+    M[r * 2 * n + c] = Vm[e] - U[e];
+    M[r * 2 * n + n + c] = Vm[e] + U[e];
+  }
+  __syncthreads();
+  if (!gj_solve(M, n, red, ired, fac)) return false;
+  for (int e = threadIdx.x; e < n * n; e += DT) E[e] = M[(e / n) * 2 * n + n + e % n];
+  __syncthreads();
+  for (int k = 0; k < s; ++k) {
+    mm(T, E, E, n, sA, sB);
+    for (int e = threadIdx.x; e < n * n; e += DT) E[e] = T[e];
+    __syncthreads();
+  }
+  return true;
+}
+
+// One CTA per scale s: A = (scale_s * post) * augmented(H_m, order); E = expm(A);
+// y_s = beta * E[0:m, order*m]; res_s = |h_next| |y_m| / ||y|| * res_scale_s.
+__global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
+  __shared__ double sA[64 * 17];
+  __shared__ double sB[16 * 64];
+  __shared__ double red[DT / 32 + 1];
+  __shared__ int ired[DT / 32 + 1];
+  const int sidx = blockIdx.x;
+  const int m = P.m, n = (P.order + 1) * m;
+  DenseWork W = P.work[sidx];
+  double* A = W.a;
+  double* E = W.e;
+  const double sc = P.scales[sidx];
+  const double hn = P.scal ? P.scal[0] : 0.0;
+  const bool brk = P.scal ? (P.scal[2] != 0.0) : true;
+  const double beta = P.beta[0];
+  // build the block upper-bidiagonal matrix [[sc*H, I, 0..], [0, 0, I..], ...]
+  for (int e = threadIdx.x; e < n * n; e += DT) {
+    const int r = e / n, c = e % n;
+    double v = 0.0;
+    if (r < m && c < m) v = sc * P.H[(size_t)r * P.ldh + c];
+    else if (c == r + m) v = 1.0;
+    A[e] = v;
+  }
+  __syncthreads();
+  bool finite = true;
+  for (int e = threadIdx.x; e < m * m; e += DT) if (!isfinite(A[(e / m) * n + e % m])) finite = false;
+  finite = __syncthreads_and(finite);
+  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired);
+  if (ok) {
+    bool fin2 = true;
+    for (int e = threadIdx.x; e < n * n; e += DT) if (!isfinite(E[e])) fin2 = false;
+    ok = __syncthreads_and(fin2);
+  }
+  if (!ok) {
+    if (threadIdx.x == 0) { atomicOr(&P.st->flags, (int)ST_DENSE); P.res[sidx] = INFINITY; }
+    return;
+  }
+  if (P.E_out) {
+    for (int e = threadIdx.x; e < n * n; e += DT) P.E_out[e] = E[e];
+  }
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < m; i += DT) {
+    const double yv = E[(size_t)i * n + P.order * m] * beta;
+    P.Y[(size_t)sidx * m + i] = yv;
+    ss += yv * yv;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < DT / 32; ++w) t += red[w];
+    const double nrm = sqrt(t);
+    const double ylast = E[(size_t)(m - 1) * n + P.order * m] * beta;
+    const double hnext = brk ? 0.0 : hn;
+    double r = (nrm == 0.0) ? 0.0 : fabs(hnext) * fabs(ylast) / nrm;
+    P.res[sidx] = r * P.res_scale[sidx];
+  }
+}
+
+cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s) {
+  phi_small_kernel<<<nscales, DT, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace emhd

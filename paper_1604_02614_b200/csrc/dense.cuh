@@ -1,0 +1,33 @@
+// Small dense phi / exponential of the Krylov Hessenberg matrix (dense.cu).
+#pragma once
+#include "emhd_common.cuh"
+
+namespace emhd {
+
+constexpr int DENSE_MAX_SCALES = 4;
+
+struct DenseWork {
+  double* a;        // n x n input (scaled in place)
+  double* e;        // n x n exponential
+  double* m[8];     // 7 n x n work matrices + one n x 2n
+  double* vec;      // 3 n
+};
+
+struct PhiSmallArgs {
+  const double* H;          // Hessenberg (device), leading m x m block used
+  long long ldh;
+  int m, order;             // phi_order of the ((order+1) m)^2 block matrix
+  const double* scales;     // device [S]: scale applied to H (c*h or delta)
+  const double* res_scale;  // device [S]: factor applied to the residual
+  const double* scal;       // device {h_next, max|w|, breakdown} of the basis (null: breakdown)
+  const double* beta;       // device scalar: ||seed||
+  double* Y;                // [S][m] coefficient vectors y_s
+  double* res;              // [S] residual estimates
+  DenseWork work[DENSE_MAX_SCALES];
+  DevStatus* st;
+  double* E_out;            // optional: full n x n exponential of scale_0 * A (S = 1)
+};
+
+cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s);
+
+}  // namespace emhd

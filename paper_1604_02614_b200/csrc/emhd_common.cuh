@@ -1,0 +1,55 @@
+// Shared device helpers for the expmhd B200 hot path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace emhd {
+
+constexpr int NF = 8;                // conserved fields (rho, mx, my, mz, Bx, By, Bz, E)
+constexpr double SQRT_EPS = 1.4901161193847656e-08;   // 2^-26 == sqrt(DBL_EPSILON)
+
+enum Bc : int { BC_PERIODIC = 0, BC_REFLECT = 1, BC_ZEROGRAD = 2, BC_EXTERNAL = 3 };
+
+// status word bits (device-resident, read at host sync points)
+enum : int { ST_RHO = 1, ST_PRESSURE = 2, ST_NONFINITE = 4, ST_BREAKDOWN = 8, ST_DENSE = 16 };
+
+struct DevStatus {
+  int flags;
+  int rhs_evals;
+  unsigned long long first_nonfinite;   // flat index of first non-finite Jv entry
+  int breakdown;
+  int pad;
+};
+
+// Correctly rounded x / d for a constant divisor d with r = RN(1/d), using
+// FMA residual corrections (no MUFU, no slow path).  q0 = RN(x r) is within
+// 1.5 ulp of x/d; the first correction makes it faithful, the second is
+// Markstein's theorem (faithful q, r within half an ulp of 1/d  =>
+// RN(q + RN(x - q d) r) = RN(x/d)).  Bit-identical to IEEE x / d for all
+// finite x whose quotient neither overflows nor underflows.
+__device__ __forceinline__ double div_const(double x, double d, double r) {
+  double q = __dmul_rn(x, r);
+  double e = __fma_rn(-q, d, x);
+  q = __fma_rn(e, r, q);
+  e = __fma_rn(-q, d, x);
+  return __fma_rn(e, r, q);
+}
+
+// sigma rule of the forward-difference Jacobian (reference fdjac.py:43)
+__device__ __forceinline__ double fd_sigma(double vnorm) {
+  return vnorm > SQRT_EPS ? SQRT_EPS / vnorm : 1.0;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace emhd

@@ -1,0 +1,360 @@
+// Arnoldi building blocks: deterministic multi-dot, fused update + re-dot,
+// fused update + norm, basis combination (V y) and norms.
+//
+// Replaces reference pkg/src/expmhd/krylov.py:144-168 (_ArnoldiProcess.extend:
+// MGS pass + re-orthogonalisation pass + norm + normalisation) and the
+// V_m @ y products at krylov.py:316,374.  The orthogonalisation is classical
+// Gram–Schmidt applied twice (CGS2): the same projector as the reference's
+// MGS2 to round-off, but each pass is ONE sweep over the basis instead of j+1
+// dependent dot/axpy sweeps, so an iteration costs (3j+~12) vector reads and
+// three grid reductions.
+//
+// Reductions are deterministic: every CTA reduces its own elements in a fixed
+// order into a per-CTA partial, and the last CTA to finish (threadfence +
+// ticket) sums the partials in CTA order.  No floating-point atomics.
+#include "emhd_common.cuh"
+#include "krylov.cuh"
+
+namespace emhd {
+
+constexpr int KT = 256;          // threads per CTA
+constexpr int EPT = 2;           // elements per thread per tile (one double2)
+constexpr int TILE = KT * EPT;   // 512 elements per tile
+constexpr int NWARP = KT / 32;
+
+// Last-CTA deterministic reduction of partials[nval][G] -> out[nval].
+// kind[v]: 0 = sum, 1 = max.  Returns true in the CTA that did it.
+__device__ bool finish_partials(const double* partials, int nval, int G, const int* kinds,
+                                double* out, unsigned int* ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int prev = atomicAdd(ticket, 1u);
+    last = (prev == (unsigned)G - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int v = warp; v < nval; v += NWARP) {
+    const bool mx = kinds && kinds[v] == 1;
+    double acc = mx ? 0.0 : 0.0;
+    for (int c = lane; c < G; c += 32) {
+      const double x = __ldcg(partials + (size_t)v * G + c);
+      acc = mx ? fmax(acc, x) : acc + x;
+    }
+    acc = mx ? warp_max(acc) : warp_sum(acc);
+    if (lane == 0) out[v] = acc;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;     // re-arm for the next launch
+  return true;
+}
+
+// per-warp slot accumulation of one double per vector, then CTA partial
+__device__ __forceinline__ void cta_store_partials(double* s_acc, int nval, double* partials, int G) {
+  __syncthreads();
+  for (int v = threadIdx.x; v < nval; v += KT) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) acc += s_acc[v * NWARP + w];
+    partials[(size_t)v * G + blockIdx.x] = acc;
+  }
+}
+
+// out[i] = <w, V_i>, i < nvec (over len_dot); optional out[nvec] = <w, w>.
+__global__ void __launch_bounds__(KT) multidot_kernel(const double* __restrict__ w,
+    const double* __restrict__ V, long long ldv, int nvec, long long len_dot, int self,
+    double* partials, double* out, unsigned int* ticket) {
+  extern __shared__ double s_acc[];            // [(nvec+1)][NWARP]
+  const int nval = nvec + self;
+  for (int k = threadIdx.x; k < nval * NWARP; k += KT) s_acc[k] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double selfacc = 0.0;
+  const long long ntiles = (len_dot + TILE - 1) / TILE;
+  for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const long long e = tl * TILE + (long long)threadIdx.x * EPT;
+    double2 wv = make_double2(0.0, 0.0);
+    if (e + 1 < len_dot) wv = __ldcs(reinterpret_cast<const double2*>(w + e));
+    else if (e < len_dot) wv.x = w[e];
+    selfacc = fma(wv.x, wv.x, fma(wv.y, wv.y, selfacc));
+    int i = 0;
+    for (; i + 4 <= nvec; i += 4) {
+      double2 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* Vi = V + (size_t)(i + u) * ldv;
+        x[u] = make_double2(0.0, 0.0);
+        if (e + 1 < len_dot) x[u] = __ldcs(reinterpret_cast<const double2*>(Vi + e));
+        else if (e < len_dot) x[u].x = Vi[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double d = warp_sum(fma(wv.x, x[u].x, wv.y * x[u].y));
+        if (lane == 0) s_acc[(i + u) * NWARP + warp] += d;
+      }
+    }
+    for (; i < nvec; ++i) {
+      const double* Vi = V + (size_t)i * ldv;
+      double2 x = make_double2(0.0, 0.0);
+      if (e + 1 < len_dot) x = __ldcs(reinterpret_cast<const double2*>(Vi + e));
+      else if (e < len_dot) x.x = Vi[e];
+      double d = warp_sum(fma(wv.x, x.x, wv.y * x.y));
+      if (lane == 0) s_acc[i * NWARP + warp] += d;
+    }
+  }
+  if (self) {
+    selfacc = warp_sum(selfacc);
+    if (lane == 0) s_acc[nvec * NWARP + warp] = selfacc;
+  }
+  cta_store_partials(s_acc, nval, partials, gridDim.x);
+  finish_partials(partials, nval, gridDim.x, nullptr, out, ticket);
+}
+
+// w[0:len_upd] -= sum_i h[i] V_i ; then out[i] = <w_new, V_i> over len_dot.
+// mode 0: re-dot (CGS2 pass-2 projections); mode 1: out = {sum w^2 (len_dot), max|w| (len_max)}
+__global__ void __launch_bounds__(KT) update_kernel(double* __restrict__ w,
+    const double* __restrict__ V, long long ldv, int nvec, const double* __restrict__ h,
+    long long len_upd, long long len_dot, long long len_max, int mode,
+    double* partials, double* out, unsigned int* ticket) {
+  extern __shared__ double sm[];
+  double* s_h = sm;                              // [nvec]
+  double* s_acc = sm + ((nvec + 1) & ~1);        // [(nvec or 2)][NWARP]
+  const int nval = mode == 0 ? nvec : 2;
+  for (int k = threadIdx.x; k < nvec; k += KT) s_h[k] = h[k];
+  for (int k = threadIdx.x; k < nval * NWARP; k += KT) s_acc[k] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double ss = 0.0, mx = 0.0;
+  const long long ntiles = (len_upd + TILE - 1) / TILE;
+  for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const long long e = tl * TILE + (long long)threadIdx.x * EPT;
+    const bool full = e + 1 < len_upd;
+    double2 wv = make_double2(0.0, 0.0);
+    if (full) wv = *reinterpret_cast<const double2*>(w + e);
+    else if (e < len_upd) wv.x = w[e];
+    int i = 0;
+    for (; i + 4 <= nvec; i += 4) {
+      double2 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* Vi = V + (size_t)(i + u) * ldv;
+        x[u] = make_double2(0.0, 0.0);
+        if (full) x[u] = __ldg(reinterpret_cast<const double2*>(Vi + e));
+        else if (e < len_upd) x[u].x = Vi[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        wv.x = fma(-s_h[i + u], x[u].x, wv.x);
+        wv.y = fma(-s_h[i + u], x[u].y, wv.y);
+      }
+    }
+    for (; i < nvec; ++i) {
+      const double* Vi = V + (size_t)i * ldv;
+      double2 x = make_double2(0.0, 0.0);
+      if (full) x = __ldg(reinterpret_cast<const double2*>(Vi + e));
+      else if (e < len_upd) x.x = Vi[e];
+      wv.x = fma(-s_h[i], x.x, wv.x);
+      wv.y = fma(-s_h[i], x.y, wv.y);
+    }
+    if (full) *reinterpret_cast<double2*>(w + e) = wv;
+    else if (e < len_upd) w[e] = wv.x;
+    // mask entries beyond the dot / max ranges
+    const double dx = (e < len_dot) ? wv.x : 0.0, dy = (e + 1 < len_dot) ? wv.y : 0.0;
+    if (mode == 0) {
+      int k = 0;
+      for (; k + 4 <= nvec; k += 4) {
+        double2 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* Vi = V + (size_t)(k + u) * ldv;
+          x[u] = make_double2(0.0, 0.0);
+          if (full) x[u] = __ldg(reinterpret_cast<const double2*>(Vi + e));
+          else if (e < len_upd) x[u].x = Vi[e];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double d = warp_sum(fma(dx, x[u].x, dy * x[u].y));
+          if (lane == 0) s_acc[(k + u) * NWARP + warp] += d;
+        }
+      }
+      for (; k < nvec; ++k) {
+        const double* Vi = V + (size_t)k * ldv;
+        double2 x = make_double2(0.0, 0.0);
+        if (full) x = __ldg(reinterpret_cast<const double2*>(Vi + e));
+        else if (e < len_upd) x.x = Vi[e];
+        double d = warp_sum(fma(dx, x.x, dy * x.y));
+        if (lane == 0) s_acc[k * NWARP + warp] += d;
+      }
+    } else {
+      ss = fma(dx, dx, fma(dy, dy, ss));
+      const double mxx = (e < len_max) ? fabs(wv.x) : 0.0;
+      const double mxy = (e + 1 < len_max) ? fabs(wv.y) : 0.0;
+      mx = fmax(mx, fmax(mxx, mxy));
+    }
+  }
+  if (mode == 1) {
+    ss = warp_sum(ss);
+    mx = warp_max(mx);
+    if (lane == 0) { s_acc[0 * NWARP + warp] = ss; s_acc[1 * NWARP + warp] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int q = 0; q < NWARP; ++q) { a += s_acc[q]; b = fmax(b, s_acc[NWARP + q]); }
+      partials[blockIdx.x] = a;
+      partials[(size_t)gridDim.x + blockIdx.x] = b;
+    }
+    __shared__ int kinds_s[2];
+    if (threadIdx.x == 0) { kinds_s[0] = 0; kinds_s[1] = 1; }
+    __syncthreads();
+    finish_partials(partials, 2, gridDim.x, kinds_s, out, ticket);
+  } else {
+    cta_store_partials(s_acc, nval, partials, gridDim.x);
+    finish_partials(partials, nval, gridDim.x, nullptr, out, ticket);
+  }
+}
+
+// out = {sum x^2 over len_sum, max|x| over len_max}
+__global__ void __launch_bounds__(KT) norms_kernel(const double* __restrict__ x, long long len_sum,
+    long long len_max, double* partials, double* out, unsigned int* ticket) {
+  __shared__ double s[2 * NWARP];
+  __shared__ int kinds_s[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long len = len_sum > len_max ? len_sum : len_max;
+  double ss = 0.0, mx = 0.0;
+  for (long long e = (long long)blockIdx.x * KT + threadIdx.x; e < len; e += (long long)gridDim.x * KT) {
+    const double v = x[e];
+    if (e < len_sum) ss = fma(v, v, ss);
+    if (e < len_max) mx = fmax(mx, fabs(v));
+  }
+  ss = warp_sum(ss);
+  mx = warp_max(mx);
+  if (lane == 0) { s[warp] = ss; s[NWARP + warp] = mx; }
+  if (threadIdx.x == 0) { kinds_s[0] = 0; kinds_s[1] = 1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int q = 0; q < NWARP; ++q) { a += s[q]; b = fmax(b, s[NWARP + q]); }
+    partials[blockIdx.x] = a;
+    partials[(size_t)gridDim.x + blockIdx.x] = b;
+  }
+  finish_partials(partials, 2, gridDim.x, kinds_s, out, ticket);
+}
+
+// Arnoldi column bookkeeping after the (all-reduced) sums are known:
+// H[0:j+1, j] = h1 + h2 ; hnext = sqrt(ss) ; breakdown test (krylov.py:161-166);
+// scal = {hnext, max|w_top|} for the next fused normalise + Jv.
+__global__ void arnoldi_finish_kernel(const double* h1, const double* h2, const double* nrm,
+    const double* selfdot, int j, double* H, long long ldh, double* scal, DevStatus* st,
+    double rtol) {
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) H[(size_t)i * ldh + j] = h1[i] + h2[i];
+  if (threadIdx.x == 0) {
+    const double hnext = sqrt(nrm[0]);
+    const double scale = sqrt(selfdot[0]);
+    const bool brk = hnext <= rtol * fmax(scale, 1.0);
+    if (brk) {
+      st->breakdown = 1;
+    } else {
+      H[(size_t)(j + 1) * ldh + j] = hnext;
+    }
+    scal[0] = hnext;
+    scal[1] = nrm[1];
+    scal[2] = brk ? 1.0 : 0.0;
+  }
+}
+
+// out[s] = base[s] (+) coef[s] * sum_i Y[s*m + i] V_i   (S <= 4 outputs, one sweep over V)
+__global__ void __launch_bounds__(KT) combine_kernel(const double* __restrict__ V, long long ldv, int m,
+    const double* __restrict__ Y, int S, const CombineOut co, long long len) {
+  extern __shared__ double s_y[];               // [S][m]
+  for (int k = threadIdx.x; k < S * m; k += KT) s_y[k] = Y[k];
+  __syncthreads();
+  for (long long e = ((long long)blockIdx.x * KT + threadIdx.x) * EPT; e < len;
+       e += (long long)gridDim.x * KT * EPT) {
+    const bool full = e + 1 < len;
+    double2 acc[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) acc[s] = make_double2(0.0, 0.0);
+    for (int i = 0; i < m; ++i) {
+      const double* Vi = V + (size_t)i * ldv;
+      double2 x = make_double2(0.0, 0.0);
+      if (full) x = __ldcs(reinterpret_cast<const double2*>(Vi + e));
+      else x.x = Vi[e];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (s < S) {
+          const double y = s_y[s * m + i];
+          acc[s].x = fma(x.x, y, acc[s].x);
+          acc[s].y = fma(x.y, y, acc[s].y);
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (s < S) {
+        double2 r = acc[s];
+        if (co.base[s]) {
+          const double c = co.coef[s];
+          const double* b = co.base[s];
+          r.x = __dadd_rn(b[e], __dmul_rn(c, r.x));
+          if (full) r.y = __dadd_rn(b[e + 1], __dmul_rn(c, r.y));
+        }
+        if (full) *reinterpret_cast<double2*>(co.out[s] + e) = r;
+        else co.out[s][e] = r.x;
+      }
+    }
+  }
+}
+
+static int grid_for(long long len, int num_sms) {
+  long long tiles = (len + TILE - 1) / TILE;
+  long long g = 2LL * num_sms;
+  return (int)(tiles < g ? (tiles < 1 ? 1 : tiles) : g);
+}
+
+cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
+                            int self, KWork& wk, double* out, cudaStream_t s) {
+  const int G = grid_for(len_dot, wk.num_sms);
+  const size_t sm = sizeof(double) * (size_t)(nvec + 1) * NWARP;
+  multidot_kernel<<<G, KT, sm, s>>>(w, V, ldv, nvec, len_dot, self, wk.partials, out, wk.ticket);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
+                          long long len_upd, long long len_dot, long long len_max, int mode,
+                          KWork& wk, double* out, cudaStream_t s) {
+  const int G = grid_for(len_upd, wk.num_sms);
+  const int nval = mode == 0 ? nvec : 2;
+  const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)(nval > 0 ? nval : 1) * NWARP);
+  update_kernel<<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode,
+                                   wk.partials, out, wk.ticket);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, KWork& wk, double* out,
+                         cudaStream_t s) {
+  const long long len = len_sum > len_max ? len_sum : len_max;
+  long long g = (len + KT - 1) / KT;
+  const int G = (int)(g < 2LL * wk.num_sms ? (g < 1 ? 1 : g) : 2LL * wk.num_sms);
+  norms_kernel<<<G, KT, 0, s>>>(x, len_sum, len_max, wk.partials, out, wk.ticket);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,
+                                  const double* selfdot, int j, double* H, long long ldh, double* scal,
+                                  DevStatus* st, double rtol, cudaStream_t s) {
+  arnoldi_finish_kernel<<<1, 128, 0, s>>>(h1, h2, nrm, selfdot, j, H, ldh, scal, st, rtol);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const double* V, long long ldv, int m, const double* Y, int S,
+                           const CombineOut& co, long long len, int num_sms, cudaStream_t s) {
+  long long g = (len + TILE - 1) / TILE;
+  const int G = (int)(g < 4LL * num_sms ? (g < 1 ? 1 : g) : 4LL * num_sms);
+  const size_t sm = sizeof(double) * (size_t)S * m;
+  combine_kernel<<<G, KT, sm, s>>>(V, ldv, m, Y, S, co, len);
+  return cudaGetLastError();
+}
+
+}  // namespace emhd

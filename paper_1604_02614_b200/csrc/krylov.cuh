@@ -1,0 +1,32 @@
+// Launchers of the Arnoldi / combination kernels (krylov.cu).
+#pragma once
+#include "emhd_common.cuh"
+
+namespace emhd {
+
+struct KWork {
+  double* partials;          // >= (m_cap + 3) * 2 * num_sms doubles
+  unsigned int* ticket;      // zero-initialised, re-armed by each reduction
+  int num_sms;
+};
+
+struct CombineOut {
+  const double* base[4];     // optional base vector per output (null: plain V y)
+  double coef[4];            // out = base + coef * (V y)
+  double* out[4];
+};
+
+cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
+                            int self, KWork& wk, double* out, cudaStream_t s);
+cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
+                          long long len_upd, long long len_dot, long long len_max, int mode,
+                          KWork& wk, double* out, cudaStream_t s);
+cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, KWork& wk, double* out,
+                         cudaStream_t s);
+cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,
+                                  const double* selfdot, int j, double* H, long long ldh, double* scal,
+                                  DevStatus* st, double rtol, cudaStream_t s);
+cudaError_t launch_combine(const double* V, long long ldv, int m, const double* Y, int S,
+                           const CombineOut& co, long long len, int num_sms, cudaStream_t s);
+
+}  // namespace emhd

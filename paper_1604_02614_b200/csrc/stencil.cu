@@ -1,0 +1,485 @@
+// Fused 2.5D resistive-MHD right-hand side / finite-difference Jv stencil.
+//
+// Replaces reference pkg/src/expmhd/mhd.py:144-285 (apply_ghosts, pressure,
+// hyperbolic_flux, diffusive_flux, rhs) and fdjac.py:38-49 (FdJacobianOperator
+// ._apply), bit for bit: every floating-point operation is issued in the
+// reference NumPy evaluation order, this translation unit is compiled with
+// -fmad=false (no contraction), divisions by the per-cell density are IEEE
+// divisions and divisions by the constants 2h and sigma use the exact
+// FMA-corrected reciprocal (div_const, emhd_common.cuh).
+//
+// Layout: state (8, nx, ny) fp64, y fastest (mhd.py:99-103).  One CTA owns a
+// strip of TY columns (one thread per column) and marches down a chunk of
+// rows, keeping three rows of per-cell primitives, three rows of x-fluxes and
+// two rows of y-fluxes in shared memory.  Primitives are evaluated once per
+// cell (the reference evaluates them twice, mhd.py:177-179 and :218-221 —
+// identical bits), the derivatives of a flux cell are shared by its x- and
+// y-flux, and halo recomputation only happens at strip edges (4 columns) and
+// chunk edges (4 rows).
+#include "emhd_common.cuh"
+#include "stencil.cuh"
+
+namespace emhd {
+
+// primitive slots kept per cell in shared memory
+enum : int { Q_RHO = 0, Q_MX, Q_MY, Q_EN, Q_B0, Q_B1, Q_B2, Q_V0, Q_V1, Q_V2, Q_T, Q_PT, NQ };
+
+struct RowRef {
+  long long off;     // element offset of (field 0, row, col 0) in the chosen buffer
+  long long fs;      // field stride in that buffer
+  bool halo;         // read from the halo buffer instead of the interior
+  bool flip;         // mirrored ghost row: MX, BX change sign
+};
+
+__device__ __forceinline__ int map_ghost(int k, int n, int bc, bool& flip) {
+  flip = false;
+  if (k >= 0 && k < n) return k;
+  if (bc == BC_PERIODIC) return k < 0 ? k + n : k - n;
+  if (bc == BC_ZEROGRAD) return k < 0 ? 0 : n - 1;
+  flip = true;                                  // reflect ('symmetric' pad)
+  return k < 0 ? -k - 1 : 2 * n - 1 - k;
+}
+
+__device__ __forceinline__ RowRef row_ref(const StencilParams& P, int r) {
+  RowRef R;
+  const long long ny = P.ny;
+  R.halo = false;
+  R.fs = (long long)P.nx * ny;
+  if (r < 0 && P.bcx_lo == BC_EXTERNAL) {
+    R.halo = true; R.fs = 2 * ny; R.off = (long long)(r + 2) * ny; R.flip = false;
+    return R;
+  }
+  if (r >= P.nx && P.bcx_hi == BC_EXTERNAL) {
+    R.halo = true; R.fs = 2 * ny; R.off = (long long)NF * 2 * ny + (long long)(r - P.nx) * ny;
+    R.flip = false;
+    return R;
+  }
+  bool fl;
+  int src = map_ghost(r, P.nx, r < 0 ? P.bcx_lo : P.bcx_hi, fl);
+  R.off = (long long)src * ny;
+  R.flip = fl;
+  return R;
+}
+
+// perturbed / plain state of one cell, with ghost sign flips applied after the
+// arithmetic exactly as np.pad followed by "*= -1.0" would see it
+template <int MODE>
+__device__ __forceinline__ void load_cell(const StencilParams& P, const RowRef& R, int jsrc,
+                                          bool yflip, double sigma, double hnext, double rh,
+                                          double u[NF]) {
+  const double* A = R.halo ? P.a_halo : P.a;
+  const double* Vv = nullptr;
+  if (MODE != MODE_RHS) Vv = R.halo ? P.v_halo : P.v;
+  const long long o = R.off + jsrc;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    double x = __ldg(A + o + f * R.fs);
+    if (MODE == MODE_JV) {
+      double d = __ldg(Vv + o + f * R.fs);
+      x = __dadd_rn(x, __dmul_rn(sigma, d));          // a + sigma * v   (fdjac.py:44)
+    } else if (MODE == MODE_JVN) {
+      double d = div_const(__ldg(Vv + o + f * R.fs), hnext, rh);   // v_j = w / h (krylov.py:167)
+      x = __dadd_rn(x, __dmul_rn(sigma, d));
+    }
+    u[f] = x;
+  }
+  if (R.flip) { u[1] = -u[1]; u[4] = -u[4]; }
+  if (yflip) { u[2] = -u[2]; u[5] = -u[5]; }
+}
+
+// pressure / admissibility / primitives (mhd.py:106-131, 176-181, 217-221)
+__device__ __forceinline__ void cell_prims(const StencilParams& P, const double u[NF],
+                                           double* q, int qs, int& flag) {
+  const double rho = u[0], mx = u[1], my = u[2], mz = u[3];
+  const double b0 = u[4], b1 = u[5], b2 = u[6], en = u[7];
+  if (P.check && rho <= 0.0) flag |= ST_RHO;
+  const double m2 = __dadd_rn(__dadd_rn(__dmul_rn(mx, mx), __dmul_rn(my, my)), __dmul_rn(mz, mz));
+  const double bb = __dadd_rn(__dadd_rn(__dmul_rn(b0, b0), __dmul_rn(b1, b1)), __dmul_rn(b2, b2));
+  const double kin = __dmul_rn(0.5, m2) / rho;
+  const double mag = __dmul_rn(P.bfac, bb);
+  const double p = __dmul_rn(P.gm1, __dsub_rn(__dsub_rn(en, kin), mag));
+  if (P.check && p <= 0.0) flag |= ST_PRESSURE;
+  q[Q_RHO * qs] = rho;
+  q[Q_MX * qs] = mx;
+  q[Q_MY * qs] = my;
+  q[Q_EN * qs] = en;
+  q[Q_B0 * qs] = b0;
+  q[Q_B1 * qs] = b1;
+  q[Q_B2 * qs] = b2;
+  q[Q_V0 * qs] = mx / rho;
+  q[Q_V1 * qs] = my / rho;
+  q[Q_V2 * qs] = mz / rho;
+  q[Q_T * qs] = p / rho;
+  q[Q_PT * qs] = __dadd_rn(p, __dmul_rn(0.5, bb));
+}
+
+// x- and y-flux G = F_hyp - F_diff at one cell (mhd.py:174-197, 209-266, 275-276).
+// c: prim column slot of the cell; qm/q0/qp: prim rows i-1, i, i+1.
+__device__ __forceinline__ void flux_cell(const StencilParams& P, const double* qm,
+                                          const double* q0, const double* qp, int c, int qs,
+                                          bool need_x, bool need_y, double gx[NF], double gy[NF]) {
+#define QV(row, k, col) row[(k) * qs + (col)]
+  const double thx = P.two_hx, rhx = P.r_two_hx, thy = P.two_hy, rhy = P.r_two_hy;
+  // centred derivatives of v, B, T at the cell (mhd.py:224-227, 261, 264)
+  const double dvx0 = div_const(__dsub_rn(QV(qp, Q_V0, c), QV(qm, Q_V0, c)), thx, rhx);
+  const double dvx1 = div_const(__dsub_rn(QV(qp, Q_V1, c), QV(qm, Q_V1, c)), thx, rhx);
+  const double dvy0 = div_const(__dsub_rn(QV(q0, Q_V0, c + 1), QV(q0, Q_V0, c - 1)), thy, rhy);
+  const double dvy1 = div_const(__dsub_rn(QV(q0, Q_V1, c + 1), QV(q0, Q_V1, c - 1)), thy, rhy);
+  const double dBx1 = div_const(__dsub_rn(QV(qp, Q_B1, c), QV(qm, Q_B1, c)), thx, rhx);
+  const double dBy0 = div_const(__dsub_rn(QV(q0, Q_B0, c + 1), QV(q0, Q_B0, c - 1)), thy, rhy);
+
+  const double rho = QV(q0, Q_RHO, c), en = QV(q0, Q_EN, c), pt = QV(q0, Q_PT, c);
+  const double v0 = QV(q0, Q_V0, c), v1 = QV(q0, Q_V1, c), v2 = QV(q0, Q_V2, c);
+  const double b0 = QV(q0, Q_B0, c), b1 = QV(q0, Q_B1, c), b2 = QV(q0, Q_B2, c);
+  const double mu = P.mu, eta = P.eta, heat = P.heat;
+
+  const double divv = __dadd_rn(dvx0, dvy1);
+  const double c23d = __dmul_rn(2.0 / 3.0, divv);
+  const double tau_xy = __dadd_rn(dvy0, dvx1);
+  const double curl = __dsub_rn(dBx1, dBy0);               // dBx[1] - dBy[0]
+  const double bv = __dadd_rn(__dadd_rn(__dmul_rn(b0, v0), __dmul_rn(b1, v1)), __dmul_rn(b2, v2));
+  const double ept = __dadd_rn(en, pt);
+  const double r0 = __dmul_rn(rho, v0), r1 = __dmul_rn(rho, v1), r2 = __dmul_rn(rho, v2);
+
+  if (need_x) {
+    const double dvx2 = div_const(__dsub_rn(QV(qp, Q_V2, c), QV(qm, Q_V2, c)), thx, rhx);
+    const double dBx2 = div_const(__dsub_rn(QV(qp, Q_B2, c), QV(qm, Q_B2, c)), thx, rhx);
+    const double dTx = div_const(__dsub_rn(QV(qp, Q_T, c), QV(qm, Q_T, c)), thx, rhx);
+    const double tau_xx = __dsub_rn(__dmul_rn(2.0, dvx0), c23d);
+    // diffusive x-flux (mhd.py:244-262)
+    const double fmx = __dmul_rn(mu, tau_xx);
+    const double fmy = __dmul_rn(mu, tau_xy);
+    const double fmz = __dmul_rn(mu, dvx2);
+    const double fby = __dmul_rn(eta, curl);
+    const double fbz = __dmul_rn(eta, dBx2);
+    const double visc = __dmul_rn(mu, __dadd_rn(__dadd_rn(__dmul_rn(tau_xx, v0), __dmul_rn(tau_xy, v1)),
+                                                __dmul_rn(dvx2, v2)));
+    const double res = __dmul_rn(eta, __dadd_rn(__dmul_rn(b1, curl), __dmul_rn(b2, dBx2)));
+    const double fen = __dadd_rn(__dadd_rn(visc, __dmul_rn(heat, dTx)), res);
+    // hyperbolic x-flux (mhd.py:185-196) minus diffusive
+    gx[0] = QV(q0, Q_MX, c);
+    gx[1] = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(r0, v0), __dmul_rn(b0, b0)), pt), fmx);
+    gx[2] = __dsub_rn(__dsub_rn(__dmul_rn(r1, v0), __dmul_rn(b1, b0)), fmy);
+    gx[3] = __dsub_rn(__dsub_rn(__dmul_rn(r2, v0), __dmul_rn(b2, b0)), fmz);
+    gx[4] = __dsub_rn(__dmul_rn(v0, b0), __dmul_rn(b0, v0));
+    gx[5] = __dsub_rn(__dsub_rn(__dmul_rn(v0, b1), __dmul_rn(b0, v1)), fby);
+    gx[6] = __dsub_rn(__dsub_rn(__dmul_rn(v0, b2), __dmul_rn(b0, v2)), fbz);
+    gx[7] = __dsub_rn(__dsub_rn(__dmul_rn(ept, v0), __dmul_rn(b0, bv)), fen);
+  }
+  if (need_y) {
+    const double dvy2 = div_const(__dsub_rn(QV(q0, Q_V2, c + 1), QV(q0, Q_V2, c - 1)), thy, rhy);
+    const double dBy2 = div_const(__dsub_rn(QV(q0, Q_B2, c + 1), QV(q0, Q_B2, c - 1)), thy, rhy);
+    const double dTy = div_const(__dsub_rn(QV(q0, Q_T, c + 1), QV(q0, Q_T, c - 1)), thy, rhy);
+    const double tau_yy = __dsub_rn(__dmul_rn(2.0, dvy1), c23d);
+    // diffusive y-flux (mhd.py:245-265)
+    const double fmx = __dmul_rn(mu, tau_xy);
+    const double fmy = __dmul_rn(mu, tau_yy);
+    const double fmz = __dmul_rn(mu, dvy2);
+    const double fbx = -__dmul_rn(eta, curl);                 // fy[BX] = -fx[BY]
+    const double fbz = __dmul_rn(eta, dBy2);
+    const double visc = __dmul_rn(mu, __dadd_rn(__dadd_rn(__dmul_rn(tau_xy, v0), __dmul_rn(tau_yy, v1)),
+                                                __dmul_rn(dvy2, v2)));
+    const double res = __dmul_rn(eta, __dadd_rn(__dmul_rn(b0, __dsub_rn(dBy0, dBx1)), __dmul_rn(b2, dBy2)));
+    const double fen = __dadd_rn(__dadd_rn(visc, __dmul_rn(heat, dTy)), res);
+    gy[0] = QV(q0, Q_MY, c);
+    gy[1] = __dsub_rn(__dsub_rn(__dmul_rn(r0, v1), __dmul_rn(b0, b1)), fmx);
+    gy[2] = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(r1, v1), __dmul_rn(b1, b1)), pt), fmy);
+    gy[3] = __dsub_rn(__dsub_rn(__dmul_rn(r2, v1), __dmul_rn(b2, b1)), fmz);
+    gy[4] = __dsub_rn(__dsub_rn(__dmul_rn(v1, b0), __dmul_rn(b1, v0)), fbx);
+    gy[5] = __dsub_rn(__dmul_rn(v1, b1), __dmul_rn(b1, v1));
+    gy[6] = __dsub_rn(__dsub_rn(__dmul_rn(v1, b2), __dmul_rn(b1, v2)), fbz);
+    gy[7] = __dsub_rn(__dsub_rn(__dmul_rn(ept, v1), __dmul_rn(b1, bv)), fen);
+  }
+#undef QV
+}
+
+template <int TY, int MODE, bool AUG>
+__global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
+  constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
+  constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
+  extern __shared__ double smem[];
+  double* qring = smem;                             // [3][NQ][QW]
+  double* gxring = qring + 3 * NQ * QW;             // [3][NF][TY]
+  double* gyring = gxring + 3 * NF * TY;            // [2][NF][GYW]
+
+  const int t = threadIdx.x;
+  const int j0 = blockIdx.x * TY;
+  const int i0 = blockIdx.y * P.rows_per_cta;
+  if (i0 >= P.nx) return;
+  const int i1 = min(i0 + P.rows_per_cta, P.nx);   // exclusive end of output rows
+
+  // per-call scalars: sigma, 1/sigma, h_next, 1/h_next
+  double sigma = 1.0, rsig = 1.0, hnext = 1.0, rh = 1.0;
+  bool skip_stencil = false;
+  if (MODE == MODE_JV) {
+    const double vn = P.scal[0];
+    skip_stencil = (vn == 0.0);
+    sigma = fd_sigma(vn);
+    rsig = 1.0 / sigma;
+  } else if (MODE == MODE_JVN) {
+    hnext = P.scal[0];
+    rh = 1.0 / hnext;
+    const double vn = P.scal[1] / hnext;   // max|w/h| == fl(max|w| / h) (monotone rounding)
+    skip_stencil = (vn == 0.0);
+    sigma = fd_sigma(vn);
+    rsig = 1.0 / sigma;
+  }
+
+  // augmented tail q of the current basis vector (krylov.py:268-273)
+  double qv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (AUG) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (k < P.p) {
+        if (MODE == MODE_JVN) qv[k] = div_const(P.v[P.n_top + k], hnext, rh);
+        else qv[k] = P.qsrc[k];
+      }
+    }
+  }
+
+  const int ncols_out = min(TY, P.ny - j0);
+  int flag = 0;
+  unsigned long long bad = ~0ull;
+
+  if (skip_stencil) {
+    // zero direction: Jv = 0 without an RHS evaluation (fdjac.py:41-42)
+    for (int r = i0; r < i1; ++r) {
+      if (t < ncols_out) {
+        const long long o = (long long)r * P.ny + j0 + t;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const long long idx = o + (long long)f * P.nx * P.ny;
+          double val = 0.0;
+          if (AUG) {
+            val = __dmul_rn(P.ch, 0.0);
+            for (int k = 0; k < P.nb; ++k)
+              val = __dadd_rn(val, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
+          }
+          P.out[idx] = val;
+          if (MODE == MODE_JVN) P.vout[idx] = div_const(__ldg(P.v + idx), hnext, rh);
+        }
+      }
+    }
+  } else {
+    // column slots handled by this thread: main slot c = t + 2 (column j0 + t),
+    // extra halo slots 0,1 (threads 0,1) and TY+2, TY+3 (threads TY-2, TY-1)
+    const int cmain = t + 2;
+    const int cextra = (t < 2) ? t : ((t >= TY - 2) ? t + 4 : -1);
+    auto col_ok = [&](int c) { int j = j0 - 2 + c; return j >= -2 && j <= P.ny + 1; };
+    bool fm, fe;
+    const int jm = map_ghost(j0 - 2 + cmain, P.ny, P.bcy, fm);
+    const int je = cextra >= 0 ? map_ghost(j0 - 2 + cextra, P.ny, P.bcy, fe) : 0;
+    const bool okm = col_ok(cmain), oke = cextra >= 0 && col_ok(cextra);
+
+    const int nsteps = (i1 - i0) + 4;
+    for (int s = 0; s < nsteps; ++s) {
+      const int r = i0 - 2 + s;                // prim row
+      // ---- primitives of row r
+      {
+        const RowRef R = row_ref(P, r);
+        double* q = qring + ((r + 3) % 3) * NQ * QW;
+        double u[NF];
+        if (okm) {
+          load_cell<MODE>(P, R, jm, fm, sigma, hnext, rh, u);
+          cell_prims(P, u, q + cmain, QW, flag);
+        }
+        if (oke) {
+          load_cell<MODE>(P, R, je, fe, sigma, hnext, rh, u);
+          cell_prims(P, u, q + cextra, QW, flag);
+        }
+      }
+      __syncthreads();
+      // ---- fluxes of row rf = r - 1
+      const int rf = r - 1;
+      if (rf >= i0 - 1) {
+        const double* qm = qring + ((rf + 2) % 3) * NQ * QW;
+        const double* q0 = qring + ((rf + 3) % 3) * NQ * QW;
+        const double* qp = qring + ((rf + 4) % 3) * NQ * QW;
+        double* gxr = gxring + ((rf + 3) % 3) * NF * TY;
+        double* gyr = gyring + ((rf + 2) % 2) * NF * GYW;
+        const bool out_row = (rf >= i0 && rf < i1);
+        double gx[NF], gy[NF];
+        if (t < ncols_out) {
+          flux_cell(P, qm, q0, qp, cmain, QW, true, out_row, gx, gy);
+#pragma unroll
+          for (int f = 0; f < NF; ++f) gxr[f * TY + t] = gx[f];
+          if (out_row) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) gyr[f * GYW + t + 1] = gy[f];
+          }
+        }
+        if (out_row) {
+          // y-fluxes at the strip's halo columns j0-1 (thread 0) and j0+ncols (last thread)
+          int cs = -1, gslot = 0;
+          if (t == 0) { cs = 1; gslot = 0; }
+          if (t == TY - 1) { cs = ncols_out + 2; gslot = ncols_out + 1; }
+          if (cs >= 0) {
+            flux_cell(P, qm, q0, qp, cs, QW, false, true, gx, gy);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) gyr[f * GYW + gslot] = gy[f];
+          }
+        }
+      }
+      __syncthreads();
+      // ---- output row ro = r - 2
+      const int ro = r - 2;
+      if (ro >= i0 && t < ncols_out) {
+        const double* gxp = gxring + ((ro + 4) % 3) * NF * TY;
+        const double* gxm = gxring + ((ro + 2) % 3) * NF * TY;
+        const double* gyr = gyring + ((ro + 2) % 2) * NF * GYW;
+        const long long o = (long long)ro * P.ny + j0 + t;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const double ddx = div_const(__dsub_rn(gxp[f * TY + t], gxm[f * TY + t]), P.two_hx, P.r_two_hx);
+          const double ddy = div_const(__dsub_rn(gyr[f * GYW + t + 2], gyr[f * GYW + t]), P.two_hy, P.r_two_hy);
+          double F = __dsub_rn(-ddx, ddy);                    // -ddx(gx) - ddy(gy) (mhd.py:277)
+          const long long idx = o + (long long)f * P.nx * P.ny;
+          if (MODE == MODE_RHS) {
+            P.out[idx] = F;
+          } else {
+            if (!isfinite(F)) {
+              const unsigned long long gidx = (unsigned long long)f * P.nxg * P.ny +
+                  (unsigned long long)(P.x_off + ro) * P.ny + j0 + t;
+              bad = gidx < bad ? gidx : bad;
+            }
+            double jv = div_const(__dsub_rn(F, __ldg(P.fa + idx)), sigma, rsig);   // fdjac.py:49
+            if (AUG) {
+              jv = __dmul_rn(P.ch, jv);
+              for (int k = 0; k < P.nb; ++k)
+                jv = __dadd_rn(jv, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
+            }
+            P.out[idx] = jv;
+            if (MODE == MODE_JVN) P.vout[idx] = div_const(__ldg(P.v + idx), hnext, rh);
+          }
+        }
+      }
+    }
+  }
+
+  // tail of the augmented output: bottom = upshift(q) (krylov.py:271-272); v_j tail
+  if (AUG && blockIdx.x == 0 && blockIdx.y == 0 && t < P.p) {
+    double nxt = 0.0;
+#pragma unroll
+    for (int k = 1; k < 5; ++k) if (k == t + 1 && k < P.p) nxt = qv[k];
+    P.out[P.n_top + t] = nxt;
+    if (MODE == MODE_JVN) {
+      double cur = 0.0;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) if (k == t) cur = qv[k];
+      P.vout[P.n_top + t] = cur;
+    }
+  }
+
+  // status aggregation: one atomic per CTA
+  __shared__ int s_flag;
+  __shared__ unsigned long long s_bad;
+  if (t == 0) { s_flag = 0; s_bad = ~0ull; }
+  __syncthreads();
+  if (flag) atomicOr(&s_flag, flag);
+  if (bad != ~0ull) atomicMin(&s_bad, bad);
+  __syncthreads();
+  if (t == 0) {
+    if (s_flag) atomicOr(&P.st->flags, s_flag);
+    if (s_bad != ~0ull) {
+      atomicOr(&P.st->flags, (int)ST_NONFINITE);
+      atomicMin(&P.st->first_nonfinite, s_bad);
+    }
+    if (!skip_stencil && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&P.st->rhs_evals, 1);
+  }
+}
+
+
+// ---- admissibility diagnostics (error path only) ---------------------------
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_val(unsigned long long k) {
+  unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// pass 0: keys[0] = min rho, keys[1] = min p over the padded field;
+// pass 1: keys[2] / keys[3] = first padded flat index attaining them
+template <int MODE>
+__global__ void admissibility_kernel(const StencilParams P, int pass, unsigned long long* keys) {
+  const int W = P.ny + 4;
+  const long long total = (long long)(P.nx + 4) * W;
+  double sigma = 1.0, hnext = 1.0, rh = 1.0;
+  if (MODE == MODE_JV) sigma = fd_sigma(P.scal[0]);
+  if (MODE == MODE_JVN) {
+    hnext = P.scal[0];
+    rh = 1.0 / hnext;
+    sigma = fd_sigma(P.scal[1] / hnext);
+  }
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / W) - 2, c = (int)(e % W) - 2;
+    const RowRef R = row_ref(P, r);
+    bool yf;
+    const int js = map_ghost(c, P.ny, P.bcy, yf);
+    double u[NF];
+    load_cell<MODE>(P, R, js, yf, sigma, hnext, rh, u);
+    const double rho = u[0];
+    const double m2 = __dadd_rn(__dadd_rn(__dmul_rn(u[1], u[1]), __dmul_rn(u[2], u[2])), __dmul_rn(u[3], u[3]));
+    const double bb = __dadd_rn(__dadd_rn(__dmul_rn(u[4], u[4]), __dmul_rn(u[5], u[5])), __dmul_rn(u[6], u[6]));
+    const double kin = __dmul_rn(0.5, m2) / rho;
+    const double p = __dmul_rn(P.gm1, __dsub_rn(__dsub_rn(u[7], kin), __dmul_rn(P.bfac, bb)));
+    if (pass == 0) {
+      if (!isnan(rho)) atomicMin(&keys[0], ord_key(rho));
+      if (!isnan(p)) atomicMin(&keys[1], ord_key(p));
+    } else {
+      if (rho == key_val(keys[0])) atomicMin(&keys[2], (unsigned long long)e);
+      if (p == key_val(keys[1])) atomicMin(&keys[3], (unsigned long long)e);
+    }
+  }
+}
+
+cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* keys, cudaStream_t s) {
+  const long long total = (long long)(P.nx + 4) * (P.ny + 4);
+  const int G = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  for (int pass = 0; pass < 2; ++pass) {
+    if (mode == MODE_RHS) admissibility_kernel<MODE_RHS><<<G, 256, 0, s>>>(P, pass, keys);
+    else if (mode == MODE_JV) admissibility_kernel<MODE_JV><<<G, 256, 0, s>>>(P, pass, keys);
+    else admissibility_kernel<MODE_JVN><<<G, 256, 0, s>>>(P, pass, keys);
+  }
+  return cudaGetLastError();
+}
+
+template <int TY, int MODE, bool AUG>
+static cudaError_t launch_t(const StencilParams& P, cudaStream_t s) {
+  constexpr int QW = TY + 4, GYW = TY + 2;
+  const size_t sm = sizeof(double) * (3 * NQ * QW + 3 * NF * TY + 2 * NF * GYW);
+  auto k = stencil_kernel<TY, MODE, AUG>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
+  k<<<grid, TY, sm, s>>>(P);
+  return cudaGetLastError();
+}
+
+template <int TY>
+static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, cudaStream_t s) {
+  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false>(P, s);
+  if (mode == MODE_JV) return aug ? launch_t<TY, MODE_JV, true>(P, s) : launch_t<TY, MODE_JV, false>(P, s);
+  return aug ? launch_t<TY, MODE_JVN, true>(P, s) : launch_t<TY, MODE_JVN, false>(P, s);
+}
+
+int stencil_tile_width(int ny) { return ny <= 32 ? 32 : (ny <= 64 ? 64 : 128); }
+
+cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s) {
+  const int ty = stencil_tile_width(P.ny);
+  const int strips = (P.ny + ty - 1) / ty;
+  if (P.rows_per_cta <= 0) {
+    // one full wave of ~2 resident CTAs per SM; never fewer than 8 rows per CTA
+    const int target = 2 * num_sms;
+    const int chunks = (target + strips - 1) / strips;
+    int rows = (P.nx + chunks - 1) / chunks;
+    P.rows_per_cta = rows < 8 ? 8 : rows;
+  }
+  if (ty == 32) return launch_ty<32>(P, mode, aug, s);
+  if (ty == 64) return launch_ty<64>(P, mode, aug, s);
+  return launch_ty<128>(P, mode, aug, s);
+}
+
+}  // namespace emhd

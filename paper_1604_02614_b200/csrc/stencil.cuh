@@ -1,0 +1,40 @@
+// Parameters of the fused MHD RHS / Jv stencil kernel (stencil.cu).
+#pragma once
+#include "emhd_common.cuh"
+
+namespace emhd {
+
+enum : int { MODE_RHS = 0, MODE_JV = 1, MODE_JVN = 2 };
+
+struct StencilParams {
+  int nx, ny;                 // local interior rows (x) and columns (y)
+  int nxg;                    // global rows (for flat indices in error reports)
+  int x_off;                  // global row of local row 0
+  int bcx_lo, bcx_hi, bcy;    // Bc per side; BC_EXTERNAL = x-halo from neighbour rank
+  int rows_per_cta;           // <= 0: chosen by the launcher
+  int check;                  // admissibility checks on (mhd.py:116 check=True)
+  double gm1, mu, eta, heat, bfac;
+  double two_hx, r_two_hx, two_hy, r_two_hy;
+  const double* a;            // state (RHS input) or Jacobian base point
+  const double* a_halo;       // [2 sides][8][2 rows][ny] or null
+  const double* v;            // MODE_JV: direction; MODE_JVN: unnormalised w_prev
+  const double* v_halo;
+  const double* fa;           // F(a)
+  const double* scal;         // MODE_JV: {||v||_inf}; MODE_JVN: {h_next, max|w_top|}
+  double* out;
+  double* vout;               // MODE_JVN: v_j = w_prev / h_next (interior + tail)
+  long long n_top;            // 8 * nx * ny
+  int p;                      // augmented tail length (0: none)
+  int nb;                     // number of B columns in the epilogue
+  const double* bcol[5];
+  int bidx[5];                // q index multiplying bcol[k]
+  double ch;                  // c*h scale of the augmented operator
+  const double* qsrc;         // MODE_JV + tail: q (device, length p)
+  DevStatus* st;
+};
+
+cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s);
+int stencil_tile_width(int ny);
+cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* keys, cudaStream_t s);
+
+}  // namespace emhd

@@ -1,0 +1,115 @@
+"""Device plumbing: torch is used only to own fp64 device buffers and streams."""
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+F64 = torch.float64
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1604_02614_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+
+
+def device():
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def is_host(x):
+    return not isinstance(x, torch.Tensor)
+
+
+def to_device(x):
+    """fp64 contiguous CUDA tensor view/copy of x (numpy, list or tensor)."""
+    if isinstance(x, torch.Tensor):
+        if x.device.type != "cuda":
+            x = x.to(device())
+        if x.dtype != F64:
+            x = x.to(F64)
+        return x.contiguous()
+    arr = np.ascontiguousarray(np.asarray(x, dtype=float))
+    t = torch.from_numpy(arr)
+    return t.to(device(), non_blocking=False)
+
+
+def to_host(t):
+    return t.detach().to("cpu").numpy()
+
+
+def empty(n):
+    return torch.empty(int(n), dtype=F64, device=device())
+
+
+def zeros(n):
+    return torch.zeros(int(n), dtype=F64, device=device())
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Scratch:
+    """Small device scalars + pinned host mirror for one sync point."""
+
+    def __init__(self, n):
+        self.dev = torch.zeros(int(n), dtype=F64, device=device())
+        self.host = torch.zeros(int(n), dtype=F64, pin_memory=True)
+
+    def read(self, k=None):
+        k = self.dev.numel() if k is None else k
+        self.host[:k].copy_(self.dev[:k], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.host[:k].numpy()
+
+
+class Ctx:
+    """Owner of one libemhd context (one grid / physics / slab placement)."""
+
+    def __init__(self, geometry, physics, max_vectors):
+        require_cuda()
+        L = N.lib()
+        self.lib = L
+        h = N.c_vp()
+        self.geometry = geometry
+        self.physics = physics
+        N.check(L.emhd_ctx_create(ctypes_byref(h), ctypes_byref(geometry), ctypes_byref(physics),
+                                  int(max_vectors)), "ctx_create")
+        self.h = h
+        self.max_vectors = int(max_vectors)
+        self._stream = None
+
+    def sync_stream(self):
+        s = stream_handle()
+        if s != self._stream:
+            self.lib.emhd_set_stream(self.h, s)
+            self._stream = s
+        return self.h
+
+    def status(self):
+        st = N.Status()
+        N.check(self.lib.emhd_status_read(self.sync_stream(), ctypes_byref(st)), "status_read")
+        return st
+
+    def reset_status(self):
+        N.check(self.lib.emhd_status_reset(self.sync_stream()), "status_reset")
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) is not None and self.h.value:
+                self.lib.emhd_ctx_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def ctypes_byref(x):
+    import ctypes
+    return ctypes.byref(x)

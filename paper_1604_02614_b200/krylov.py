@@ -1,0 +1,557 @@
+"""GPU drop-in for the Krylov phi-function layer (reference krylov.py, phifuncs.py).
+
+Public names and semantics follow the reference: ``KrylovConfig``
+(krylov.py:71-82), ``KrylovStats`` (:55-68), ``ArnoldiBasis`` (:85-100),
+``PhiCombRequest`` (:103-124), ``KrylovConvergenceError`` (:31-36),
+``arnoldi`` (:191-206), ``residual_estimate`` (:209-231), ``phi_comb``
+(:241-324) and ``multi_scale_eval`` (:327-375).
+
+Device design:
+* the basis lives in HBM as (m_cap+1) contiguous rows of length ld (the
+  reference's V[n, m_cap+1] is column-strided, krylov.py:137);
+* one Arnoldi iteration = fused normalise + Jv stencil (csrc/stencil.cu), a
+  multi-dot sweep, an update + re-dot sweep and an update + norm sweep
+  (csrc/krylov.cu): CGS2, the reference's MGS + re-orthogonalisation
+  projector to round-off, in three streaming passes;
+* the small dense phi / exp of the Hessenberg matrix and the residual
+  surrogate run on the GPU (csrc/dense.cu); the host reads one double per
+  residual check and makes the reference's control decisions verbatim;
+* V_m y and the EpiRK stage axpys are one sweep over the basis (emhd_combine).
+"""
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as D
+from .fdjac import FdJacobianOperator, LinearOperator, _generic_ctx, _lincomb
+from .mhd import raise_status
+
+MAX_COMB_ORDER = 5
+BREAKDOWN_RTOL = 1e-12
+
+
+class KrylovConvergenceError(RuntimeError):
+    """Raised when the basis cap is reached with the substep at minimum."""
+
+    def __init__(self, message, residual):
+        super().__init__(message)
+        self.residual = residual
+
+
+@dataclass
+class KrylovStats:
+    operator_applies: int = 0
+    substeps: int = 0
+    max_basis_size: int = 0
+    projections: int = 0
+
+    def merge(self, other):
+        self.operator_applies += other.operator_applies
+        self.substeps += other.substeps
+        self.max_basis_size = max(self.max_basis_size, other.max_basis_size)
+        self.projections += other.projections
+
+
+@dataclass
+class KrylovConfig:
+    m_init: int = 10
+    m_max: int = 100
+    soft_cap: int = 25
+    grow_threshold: int = 10
+    substep_growth: float = 4.0 / 3.0
+    min_substep: float = 1.0 / 1024.0
+    max_substep: float = 1.0
+    reorthogonalize: bool = True
+
+
+@dataclass
+class ArnoldiBasis:
+    """Orthonormal basis V (n x m or n x (m+1)), Hessenberg H, seed norm beta."""
+
+    V: object
+    H: object
+    m: int
+    beta: float
+    breakdown: bool = False
+
+    @property
+    def h_next(self):
+        if self.breakdown or self.H.shape[0] == self.m:
+            return 0.0
+        return float(self.H[self.m, self.m - 1])
+
+
+@dataclass
+class PhiCombRequest:
+    """Query for w = sum_{k=1}^p phi_k(c*h*J) v_k (krylov.py:103-124)."""
+
+    operator: LinearOperator
+    h: float
+    c: float
+    vectors: list
+    tol: float
+
+    def __post_init__(self):
+        if not (0.0 < self.c <= 1.0):
+            raise ValueError(f"scale factor c must be in (0, 1], got {self.c}")
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+        p = len(self.vectors)
+        if p < 1 or p > MAX_COMB_ORDER:
+            raise ValueError(f"need 1 <= p <= {MAX_COMB_ORDER} vectors, got {p}")
+        n = self.operator.n
+        for k, v in enumerate(self.vectors, start=1):
+            shp = tuple(v.shape) if hasattr(v, "shape") else np.shape(v)
+            if shp != (n,):
+                raise ValueError(f"vector v_{k} has shape {shp}, expected ({n},)")
+
+
+def _ld(n):
+    return (n + 31) // 32 * 32
+
+
+class _Engine:
+    """How one Arnoldi iteration obtains w = A v_j."""
+
+    fused = False
+
+
+class _FusedFd(_Engine):
+    """FD Jacobian of the fused stencil, optionally augmented (phi_comb)."""
+
+    fused = True
+
+    def __init__(self, jop, p=0, ch=1.0, bcols=(), bidx=()):
+        self.jop, self.gpu, self.ctx = jop, jop.gpu, jop.ctx
+        self.p, self.ch = p, float(ch)
+        self.bcols = list(bcols)
+        self.bidx = list(bidx)
+        self._bptr = N.ptr_array([D.ptr(b) for b in self.bcols])
+        self._bidx = N.int_array(self.bidx)
+        self._vn = D.zeros(2)
+
+
+class _Generic(_Engine):
+    """Any LinearOperator (optionally wrapped by the augmented operator)."""
+
+    def __init__(self, op, n, p=0, ch=1.0, bcols=(), bidx=()):
+        self.op, self.n, self.p, self.ch = op, n, p, float(ch)
+        self.bcols, self.bidx = list(bcols), list(bidx)
+        self.ctx = getattr(op, "ctx", None) or _generic_ctx()
+
+
+class _Process:
+    """Device Arnoldi factorisation (reference _ArnoldiProcess, krylov.py:127-188)."""
+
+    def __init__(self, engine, seed, m_cap, n_top, p=0, layout=None, comm=None):
+        self.eng = engine
+        self.ctx = engine.ctx
+        self.lib = self.ctx.lib
+        self.n_top = n_top
+        self.p = p
+        self.naug = n_top + p
+        self.layout, self.comm = layout, comm
+        rank0 = layout is None or layout.rank == 0
+        self.len_upd = self.naug
+        self.len_dot = n_top + (p if rank0 else 0)
+        # global dimension (the reference's self.n)
+        self.n = (layout.nx_global * layout.ny * 8 if layout is not None else n_top) + p
+        self.m_cap = min(m_cap, self.n)
+        if self.m_cap + 1 > self.ctx.max_vectors - 4:
+            raise ValueError(f"basis cap {self.m_cap} exceeds the context limit")
+        self.ld = _ld(self.naug)
+        self.V = torch.zeros((self.m_cap + 1, self.ld), dtype=D.F64, device=D.device())
+        self.H = torch.zeros((self.m_cap + 1, max(self.m_cap, 1)), dtype=D.F64, device=D.device())
+        self.w = [torch.zeros(self.ld, dtype=D.F64, device=D.device()) for _ in range(2)]
+        k = self.m_cap + 4
+        self.d1 = D.zeros(k)
+        self.d2 = D.zeros(k)
+        self.nrm = D.zeros(2)
+        self.scal = D.Scratch(4)
+        self.nb = D.zeros(4)                 # {sum seed^2, max|seed|, beta, -}
+        self.beta_dev = self.nb[2:3]
+        self.m = 0
+        self.breakdown = False
+        self.applies = 0
+        self.cur = 0            # index of the w buffer holding the latest unnormalised vector
+        self._vm_ready = 0      # rows of V materialised
+        # beta = ||seed||_2, V[0] = seed / beta  (krylov.py:132-137)
+        sd = seed.reshape(-1)
+        h = self.ctx.sync_stream()
+        N.check(self.lib.emhd_norms(h, D.ptr(sd), self.len_dot, n_top, D.ptr(self.nb)), "norms")
+        self._allreduce_norms(self.nb)
+        b2 = float(self.nb[0].item())
+        self.beta = math.sqrt(b2)
+        if self.beta == 0.0:
+            raise ValueError("Arnoldi seed vector must be nonzero")
+        N.check(self.lib.emhd_div_scalar(h, D.ptr(sd), D.ptr(self.nb), 1, D.ptr(self.V[0]),
+                                         D.ptr(self.beta_dev), self.naug), "div_scalar")
+        self._vm_ready = 1
+
+    # -- collectives ----------------------------------------------------------
+    def _allreduce_sum(self, t):
+        if self.comm is not None:
+            self.comm.allreduce_sum(t)
+
+    def _allreduce_norms(self, t2):
+        if self.comm is not None and self.layout.distributed:
+            self.comm.allreduce_sum(t2[0:1])
+            self.comm.allreduce_max(t2[1:2])
+
+    # -- one iteration ----------------------------------------------------------
+    def _apply(self, j):
+        """w_out = A v_j; returns the index of the w buffer written."""
+        E = self.eng
+        h = self.ctx.sync_stream()
+        dst = 1 - self.cur if j > 0 else 0
+        out = self.w[dst]
+        if E.fused:
+            a, ah, fa = E.jop.a, E.jop.a_halo, E.jop.f_a
+            if j == 0:
+                v = self.V[0]
+                vh = E.gpu.halo(v[:self.n_top])
+                N.check(self.lib.emhd_norms(h, D.ptr(v), 0, self.n_top, D.ptr(E._vn)), "norms")
+                if self.layout is not None and self.layout.distributed:
+                    self.comm.allreduce_max(E._vn[1:2])
+                E._vn[0:1].copy_(E._vn[1:2])
+                if self.p:
+                    N.check(self.lib.emhd_jv_aug(h, D.ptr(a), D.ptr(ah), D.ptr(fa), D.ptr(v), D.ptr(vh),
+                                                 D.ptr(E._vn), D.ptr(v[self.n_top:]), self.p, E.ch,
+                                                 len(E.bcols), E._bptr, E._bidx, D.ptr(out)), "jv_aug")
+                else:
+                    N.check(self.lib.emhd_jv(h, D.ptr(a), D.ptr(ah), D.ptr(fa), D.ptr(v), D.ptr(vh),
+                                             D.ptr(E._vn), D.ptr(out)), "jv")
+                self._last = (1, v, vh, E._vn)
+            else:
+                wp = self.w[self.cur]
+                wh = E.gpu.halo(wp[:self.n_top])
+                N.check(self.lib.emhd_jv_normalized(h, D.ptr(a), D.ptr(ah), D.ptr(fa), D.ptr(wp),
+                                                    D.ptr(wh), D.ptr(self.scal.dev), D.ptr(self.V[j]),
+                                                    self.p, E.ch, len(E.bcols), E._bptr, E._bidx,
+                                                    D.ptr(out)), "jv_normalized")
+                self._vm_ready = j + 1
+                self._last = (2, wp, wh, self.scal.dev)
+        else:
+            if j > 0:
+                self._materialize(j)
+            v = self.V[j]
+            if self.p:
+                n = self.n_top
+                q = v[n:n + self.p].to("cpu").numpy()
+                top = D.to_device(E.op(v[:n])).reshape(-1)
+                terms = [(E.ch, top)] + [(float(q[k]), b) for b, k in zip(E.bcols, E.bidx)]
+                _lincomb(self.ctx, terms, out[:n])
+                tail = np.zeros(self.p)
+                tail[:self.p - 1] = q[1:]
+                out[n:n + self.p].copy_(torch.from_numpy(tail))
+            else:
+                r = D.to_device(E.op(v[:self.naug])).reshape(-1)
+                out[:self.naug].copy_(r)
+        self.cur = dst
+        return dst
+
+    def _materialize(self, upto):
+        """Write V[k] = w / h for the pending row k = upto (krylov.py:167)."""
+        if self._vm_ready > upto:
+            return
+        h = self.ctx.sync_stream()
+        N.check(self.lib.emhd_div_scalar(h, D.ptr(self.w[self.cur]), D.ptr(self.scal.dev), 0,
+                                         D.ptr(self.V[upto]), 0, self.naug), "div_scalar")
+        self._vm_ready = upto + 1
+
+    def extend(self):
+        """Add one basis vector; returns False on lucky breakdown (krylov.py:144-168)."""
+        if self.breakdown or self.m >= self.m_cap:
+            return False
+        j = self.m
+        wi = self._apply(j)
+        self.applies += 1
+        w = self.w[wi]
+        h = self.ctx.sync_stream()
+        nv = j + 1
+        # pass 1: h1 = V^T w and ||w||^2 (the breakdown scale, krylov.py:151)
+        N.check(self.lib.emhd_multidot(h, D.ptr(w), D.ptr(self.V), self.ld, nv, self.len_dot, 1,
+                                       D.ptr(self.d1)), "multidot")
+        self._allreduce_sum(self.d1[:nv + 1])
+        # w -= V h1 ; h2 = V^T w
+        N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d1),
+                                     self.len_upd, self.len_dot, self.n_top, 0, D.ptr(self.d2)), "update")
+        self._allreduce_sum(self.d2[:nv])
+        # w -= V h2 ; ||w||^2, max|w_top|
+        N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2),
+                                     self.len_upd, self.len_dot, self.n_top, 1, D.ptr(self.nrm)), "update")
+        self._allreduce_norms(self.nrm)
+        N.check(self.lib.emhd_arnoldi_finish(h, D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm),
+                                             D.ptr(self.d1[nv:]), j, D.ptr(self.H), self.H.shape[1],
+                                             D.ptr(self.scal.dev)), "arnoldi_finish")
+        self.m = j + 1
+        s = self.scal.read(3)
+        self.check_status()
+        if s[2] != 0.0:
+            self.breakdown = True
+            return False
+        return True
+
+    def check_status(self):
+        E = self.eng
+        if not E.fused:
+            return
+        st = self.ctx.status()
+        if st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE):
+            mode, v, vh, sc = self._last
+            a, ah = E.jop.a, E.jop.a_halo
+            if mode == 2:
+                # the failing state is a + sigma * V[j]; V[j] is materialised
+                v = self.V[self.m - 1]
+                vh = E.gpu.halo(v[:self.n_top])
+                sc = E._vn
+                N.check(self.lib.emhd_norms(self.ctx.sync_stream(), D.ptr(v), 0, self.n_top,
+                                            D.ptr(sc)), "norms")
+                sc[0:1].copy_(sc[1:2])
+            raise_status(self.ctx, st, (1, D.ptr(a), D.ptr(ah), D.ptr(v), D.ptr(vh), D.ptr(sc)))
+
+    # -- views ------------------------------------------------------------------
+    @property
+    def Hm(self):
+        return self.H[:self.m, :self.m]
+
+    @property
+    def h_next(self):
+        if self.breakdown:
+            return 0.0
+        return float(self.H[self.m, self.m - 1].item())
+
+    def basis(self, host=False):
+        m = self.m
+        if not self.breakdown:
+            self._materialize(m)
+        k = m if self.breakdown else m + 1
+        V = self.V[:k, :self.naug].T
+        H = self.H[:m, :m] if self.breakdown else self.H[:m + 1, :m]
+        if host:
+            V, H = D.to_host(V.contiguous()), D.to_host(H.contiguous())
+        else:
+            V, H = V, H.clone()
+        return ArnoldiBasis(V=V, H=H, m=m, beta=self.beta, breakdown=self.breakdown)
+
+    # -- small dense + combination ---------------------------------------------
+    def phi_coeffs(self, order, scales):
+        """Device Y[s] = beta phi_order(scale_s H_m) e1 and raw residuals (krylov.py:378-383)."""
+        if len(scales) > 4:
+            parts = [self.phi_coeffs(order, scales[k:k + 4]) for k in range(0, len(scales), 4)]
+            return torch.cat([p[0] for p in parts]), torch.cat([p[1] for p in parts])
+        S = len(scales)
+        sc = torch.tensor([float(x) for x in scales], dtype=D.F64).to(D.device())
+        one = torch.ones(S, dtype=D.F64).to(D.device())
+        Y = torch.empty((S, self.m), dtype=D.F64, device=D.device())
+        res = torch.empty(S, dtype=D.F64, device=D.device())
+        scal = None if self.breakdown else self.scal.dev
+        N.check(self.lib.emhd_phi_small(self.ctx.sync_stream(), D.ptr(self.H), self.H.shape[1], self.m,
+                                        order, S, D.ptr(sc), D.ptr(one),
+                                        D.ptr(scal) if scal is not None else D.ptr(self._brk()),
+                                        D.ptr(self.beta_dev), D.ptr(Y), D.ptr(res)), "phi_small")
+        return Y, res
+
+    def _brk(self):
+        if not hasattr(self, "_brk_t"):
+            self._brk_t = torch.tensor([0.0, 0.0, 1.0, 0.0], dtype=D.F64).to(D.device())
+        return self._brk_t
+
+    def combine(self, Y, outs, bases=None, coefs=None, length=None):
+        S = Y.shape[0]
+        length = self.n_top if length is None else length
+        bases = bases or [None] * S
+        coefs = coefs or [1.0] * S
+        N.check(self.lib.emhd_combine(self.ctx.sync_stream(), D.ptr(self.V), self.ld, self.m, D.ptr(Y), S,
+                                      N.ptr_array([D.ptr(b) for b in bases]), N.dbl_array(coefs),
+                                      N.ptr_array([D.ptr(o) for o in outs]), length), "combine")
+        return outs
+
+
+def _engine_for(op, n_top, p=0, ch=1.0, bcols=(), bidx=()):
+    if isinstance(op, FdJacobianOperator) and op.gpu is not None:
+        return _FusedFd(op, p, ch, bcols, bidx), op.gpu.layout, op.gpu.comm
+    return _Generic(op, n_top, p, ch, bcols, bidx), None, None
+
+
+def _dense_check(ctx):
+    st = ctx.status()
+    if st.flags & N.ST_DENSE:
+        ctx.reset_status()
+        raise FloatingPointError("overflow in augmented-matrix exponential")
+
+
+def arnoldi(op, v, m, reorthogonalize=True):
+    """m-step Arnoldi factorisation of ``op`` seeded with ``v`` (krylov.py:191-206)."""
+    host = D.is_host(v)
+    vd = D.to_device(v).reshape(-1)
+    eng, layout, comm = _engine_for(op, vd.numel())
+    n_glob = (layout.nx_global * layout.ny * 8) if layout is not None else vd.numel()
+    if m > n_glob:
+        raise ValueError(f"basis size {m} exceeds operator dimension {op.n}")
+    proc = _Process(eng, vd, m, vd.numel(), 0, layout, comm)
+    while proc.m < m and proc.extend():
+        pass
+    return proc.basis(host=host)
+
+
+def residual_estimate(basis, h, c, small_phi_seed):
+    """|h_{m+1,m}| |y_m| / ||y|| (krylov.py:209-231)."""
+    y = np.asarray(D.to_host(small_phi_seed) if isinstance(small_phi_seed, torch.Tensor)
+                   else small_phi_seed, dtype=float)
+    nrm = np.linalg.norm(y)
+    if nrm == 0.0:
+        return 0.0
+    return abs(basis.h_next) * abs(y[-1]) / nrm
+
+
+def _maxabs_many(ctx, vecs):
+    out = torch.zeros(2 * len(vecs), dtype=D.F64, device=D.device())
+    h = ctx.sync_stream()
+    for k, v in enumerate(vecs):
+        N.check(ctx.lib.emhd_norms(h, D.ptr(v), 0, v.numel(), D.ptr(out[2 * k:2 * k + 2])), "norms")
+    return out.view(-1, 2)[:, 1]
+
+
+def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
+    """phi_order(c_i h J) v for several scales from one basis (krylov.py:327-375).
+
+    ``_into`` (internal): list of (base, coef, out) triples to fuse the stage
+    axpy ``out = base + coef * result`` into the basis sweep.
+    """
+    cfg = cfg or KrylovConfig()
+    scales = list(scales)
+    if not scales or any(not (0.0 < c <= 1.0) for c in scales):
+        raise ValueError("scales must lie in (0, 1]")
+    stats = KrylovStats(projections=1)
+    host = D.is_host(v)
+    vd = D.to_device(v).reshape(-1)
+    eng, layout, comm = _engine_for(op, vd.numel())
+    n_top = vd.numel()
+    mx = _maxabs_many(eng.ctx, [vd])
+    if comm is not None:
+        comm.allreduce_max(mx)
+    if float(mx[0].item()) == 0.0:
+        outs = [torch.zeros(n_top, dtype=D.F64, device=D.device()) for _ in scales]
+        if _into:
+            for (base, coef, out), o in zip(_into, outs):
+                _lincomb(eng.ctx, [base, (coef, o)], out)
+        return ([D.to_host(o) for o in outs] if host else outs), stats
+    c_big = max(scales)
+    proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm)
+    m_target = min(cfg.m_init, proc.n)
+    while proc.m < m_target and proc.extend():
+        pass
+    while True:
+        _, res_raw = proc.phi_coeffs(order, [c_big * h])
+        r = float(res_raw[0].item())
+        _dense_check(eng.ctx)
+        res = r * c_big * h
+        if res <= tol or proc.breakdown or proc.m >= proc.n:
+            break
+        m_before = proc.m
+        proc.extend()
+        if proc.m == m_before:
+            stats.operator_applies += proc.applies
+            raise KrylovConvergenceError(
+                f"Krylov basis cap {cfg.m_max} reached in multi-scale "
+                f"evaluation (residual {res:.3e} > {tol:.3e})", residual=res)
+    stats.operator_applies += proc.applies
+    stats.max_basis_size = proc.m
+    stats.substeps = 1
+    Y, _ = proc.phi_coeffs(order, [c * h for c in scales])
+    _dense_check(eng.ctx)
+    outs = []
+    for k in range(0, len(scales), 4):
+        chunk = list(range(k, min(k + 4, len(scales))))
+        o = [torch.empty(n_top, dtype=D.F64, device=D.device()) for _ in chunk]
+        if _into:
+            bases = [_into[i][0] for i in chunk]
+            coefs = [_into[i][1] for i in chunk]
+            tgt = [_into[i][2] for i in chunk]
+            proc.combine(Y[chunk[0]:chunk[-1] + 1].contiguous(), tgt, bases, coefs)
+            o = tgt
+        else:
+            proc.combine(Y[chunk[0]:chunk[-1] + 1].contiguous(), o)
+        outs.extend(o)
+    return ([D.to_host(o) for o in outs] if host else outs), stats
+
+
+def phi_comb(req, cfg=None, _zero=None):
+    """w = sum_k phi_k(c h J) v_k by the augmented exponential (krylov.py:241-324).
+
+    ``_zero`` (internal): list of booleans marking vectors known to be zero,
+    skipping the device zero test.
+    """
+    cfg = cfg or KrylovConfig()
+    stats = KrylovStats(projections=1)
+    op = req.operator
+    p = len(req.vectors)
+    host = any(D.is_host(x) for x in req.vectors)
+    vs = [D.to_device(x).reshape(-1) for x in req.vectors]
+    n_top = vs[0].numel()
+    eng0, layout, comm = _engine_for(op, n_top)
+    zero = list(_zero) if _zero is not None else [None] * p
+    unknown = [k for k in range(p) if zero[k] is None]
+    if unknown:
+        mx = _maxabs_many(eng0.ctx, [vs[k] for k in unknown])
+        if comm is not None:
+            comm.allreduce_max(mx)
+        for k, val in zip(unknown, mx.cpu().numpy()):
+            zero[k] = float(val) == 0.0
+    if all(zero):
+        out = torch.zeros(n_top, dtype=D.F64, device=D.device())
+        return (D.to_host(out) if host else out), stats
+    ch = req.c * req.h
+    # columns of B are v_p ... v_1 (krylov.py:264); zero columns contribute nothing
+    cols = [(vs[p - 1 - k], k) for k in range(p) if not zero[p - 1 - k]]
+    eng, layout, comm = _engine_for(op, n_top, p, ch, [b for b, _ in cols], [k for _, k in cols])
+    naug_glob = ((layout.nx_global * layout.ny * 8) if layout is not None else n_top) + p
+    u = torch.zeros(n_top, dtype=D.F64, device=D.device())
+    seed = torch.zeros(_ld(n_top + p), dtype=D.F64, device=D.device())
+    t = 0.0
+    delta = 1.0
+    while t < 1.0:
+        delta = min(delta, cfg.max_substep, 1.0 - t)
+        q = np.array([t ** (p - 1 - i) / math.factorial(p - 1 - i) for i in range(p)])
+        seed[:n_top].copy_(u)
+        seed[n_top:n_top + p].copy_(torch.from_numpy(q))
+        proc = _Process(eng, seed[:n_top + p], min(cfg.m_max, naug_glob), n_top, p, layout, comm)
+        m_target = min(cfg.m_init, naug_glob)
+        while proc.m < m_target and proc.extend():
+            pass
+        while True:
+            Y, res_raw = proc.phi_coeffs(0, [delta])
+            r = float(res_raw[0].item())
+            _dense_check(eng.ctx)
+            res = r * delta
+            tol_sub = req.tol * max(delta, 1e-2)
+            if res <= tol_sub or proc.breakdown or proc.m >= proc.n:
+                break
+            if proc.m >= cfg.soft_cap and delta > cfg.min_substep:
+                delta = delta / 2.0
+                continue
+            m_before = proc.m
+            proc.extend()
+            if proc.m == m_before:
+                if delta > cfg.min_substep:
+                    delta = delta / 2.0
+                    continue
+                stats.operator_applies += proc.applies
+                raise KrylovConvergenceError(
+                    f"Krylov basis cap {cfg.m_max} reached at substep "
+                    f"{delta:.3e} (residual {res:.3e} > {tol_sub:.3e})", residual=res)
+        stats.operator_applies += proc.applies
+        u_new = torch.empty(n_top, dtype=D.F64, device=D.device())
+        proc.combine(Y, [u_new])
+        u = u_new
+        t = t + delta
+        stats.substeps += 1
+        stats.max_basis_size = max(stats.max_basis_size, proc.m)
+        if proc.m <= cfg.grow_threshold:
+            delta = delta * cfg.substep_growth
+    return (D.to_host(u) if host else u), stats
