@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 EpiRK/Krylov hot path on BASELINE config 2.
+
+Workload (BASELINE.json configs[2]): seeded smooth random 8-field
+state (16 random-phase Fourier modes per primitive) on a 1024 x 1024 grid,
+fp64, mu = eta = kappa = 1e-3, periodic x and y; a seeded unit start vector.
+One step = ``arnoldi(FdJacobianOperator(make_rhs(...), a), v, 40)``: 40
+Jv+Arnoldi iterations (each one fused normalise+Jv stencil, a multi-dot and
+two update sweeps — the reference's _ArnoldiProcess.extend, krylov.py:144-168).
+The config's 100 standalone Jv products are timed beside it and reported as
+grid-point updates/s.  Vectors are 64 MiB and the basis 2.7 GB, far larger
+than L2, so no L2 flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) the grid is slab-decomposed in x across ranks (NCCL
+halo exchange + all-reduces, strong scaling); timings are the max over ranks.
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port in oracle/, the reference itself being pure Python that cannot
+travel to the GPU box) on this host's cores, rank 0 only.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Jv+Arnoldi iterations/s (fp64)"
+UNIT = "iterations/s"
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=1024, help="grid is n x n")
+    p.add_argument("--m", type=int, default=40, help="Krylov dimension")
+    p.add_argument("--jv", type=int, default=100, help="standalone Jv products per step")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--quick", action="store_true", help="timed region only (for ncu)")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def config_dict(args, world):
+    return {
+        "workload": f"config2: {args.n}x{args.n} seeded Fourier state, "
+                    f"arnoldi(FdJacobianOperator(make_rhs), v, {args.m}) per step "
+                    f"+ {args.jv} standalone Jv products",
+        "grid": [args.n, args.n], "krylov_dim": args.m, "jv_products": args.jv,
+        "fields": 8, "mu": 1e-3, "eta": 1e-3, "kappa": 1e-3, "bc": "periodic/periodic",
+        "decomposition": f"x-slabs x{world}", "parallelism": f"slab{world}",
+        "l2": "inputs larger than L2 (64 MiB vectors, 2.7 GB basis); no flush needed",
+        "seed": 1604,
+    }
+
+
+def make_inputs(args):
+    from paper_1604_02614_b200.mhd import MhdParams
+    from paper_1604_02614_b200.problems import fourier_grid, fourier_state, unit_start_vector
+    g = fourier_grid(args.n)
+    prm = MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    U, rng = fourier_state(g, prm, seed=1604)
+    v = unit_start_vector(rng, U.size)
+    return g, prm, U, v
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------ kernel instrumentation
+LAUNCHERS = {
+    # name -> algorithmic HBM bytes of one launch, from its C-ABI arguments
+    "emhd_rhs": None, "emhd_jv": None, "emhd_jv_aug": None, "emhd_jv_normalized": None,
+    "emhd_multidot": None, "emhd_update": None, "emhd_norms": None, "emhd_arnoldi_finish": None,
+    "emhd_div_scalar": None, "emhd_phi_small": None, "emhd_combine": None, "emhd_lincomb": None,
+    "emhd_wrms": None, "emhd_pack_edges": None,
+}
+
+
+def alg_bytes(name, args, n_local):
+    W = 8.0 * n_local
+    if name == "emhd_rhs":
+        return 2 * W
+    if name in ("emhd_jv", "emhd_jv_aug"):
+        return 4 * W
+    if name == "emhd_jv_normalized":
+        return 5 * W             # read a, F(a), w_prev; write v_j and J v_j
+    if name == "emhd_multidot":
+        nvec, len_dot = args[4], args[5]
+        return 8.0 * (nvec + 1) * len_dot
+    if name == "emhd_update":
+        nvec, len_upd = args[4], args[6]
+        return 8.0 * (nvec + 2) * len_upd
+    if name == "emhd_norms":
+        return 8.0 * max(args[2], args[3])
+    if name == "emhd_div_scalar":
+        return 16.0 * args[6]
+    if name == "emhd_combine":
+        return 8.0 * (args[3] + args[5]) * args[9]
+    if name == "emhd_lincomb":
+        return 8.0 * (args[1] + 1) * args[8]
+    return 0.0
+
+
+class Instrument:
+    """Wraps the C-ABI launchers with CUDA events (current stream) and counters."""
+
+    def __init__(self, lib, n_local, events=True):
+        import torch
+        self.torch = torch
+        self.lib = lib
+        self.n_local = n_local
+        self.events = events
+        self.records = []
+        self.count = 0
+        self.orig = {}
+        for name in LAUNCHERS:
+            fn = getattr(lib, name)
+            self.orig[name] = fn
+            setattr(lib, name, self._wrap(name, fn))
+
+    def _wrap(self, name, fn):
+        torch = self.torch
+
+        def call(*a):
+            self.count += 1
+            if not self.events:
+                return fn(*a)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rc = fn(*a)
+            e1.record()
+            self.records.append((name, e0, e1, alg_bytes(name, a, self.n_local)))
+            return rc
+        return call
+
+    def restore(self):
+        for name, fn in self.orig.items():
+            setattr(self.lib, name, fn)
+
+    def table(self):
+        self.torch.cuda.synchronize()
+        agg = {}
+        for name, e0, e1, by in self.records:
+            ms = e0.elapsed_time(e1)
+            a = agg.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0.0})
+            a["launches"] += 1
+            a["ms"] += ms
+            a["bytes"] += by
+        return agg
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1604_02614_b200 as P
+    from paper_1604_02614_b200 import _native as N
+    from paper_1604_02614_b200.mhd import local_rows
+    from paper_1604_02614_b200.slab import Comm, make_layout
+
+    g, prm, U, v = make_inputs(args)
+    bc = P.BoundaryPolicy("periodic", "periodic")
+    layout = make_layout(g.nx, g.ny, bc.x, rank, world)
+    comm = Comm(layout)
+    f = P.make_rhs(prm, g, bc, layout=layout, comm=comm)
+    a_host = local_rows(U.reshape(-1), g, layout)
+    v_host = local_rows(v, g, layout)
+    a_pin = torch.from_numpy(a_host).pin_memory()
+    v_pin = torch.from_numpy(v_host).pin_memory()
+    a = a_pin.cuda()
+    vd = v_pin.cuda()
+    op = P.FdJacobianOperator(f, a)
+    n_local = a.numel()
+    cells_global = g.nx * g.ny
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        return P.arnoldi(op, vd, args.m)
+
+    def maxall(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        b = step()
+    assert b.m == args.m and not b.breakdown, "unexpected breakdown in the bench workload"
+
+    # ---- headline: K steps, device-timed, max over ranks
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with Clocks(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            b = step()
+        e1.record()
+        barrier()
+    t_ms = maxall(e0.elapsed_time(e1))
+    iters = args.m * args.steps
+    value = iters / (t_ms / 1e3)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_dict(args, world), "clocks": clk.summary()}
+    if args.quick:
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        return
+
+    # ---- 100 standalone Jv products (grid-point updates/s)
+    vn = torch.zeros(2, dtype=torch.float64, device="cuda")
+    op.vnorm_into(vd, vn)
+    jout = torch.empty_like(a)
+    vh = f.halo(vd)
+    for _ in range(3):
+        op.apply_device(vd, jout, vn, vh)
+    barrier()
+    j0, j1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    j0.record()
+    for _ in range(args.jv):
+        op.apply_device(vd, jout, vn, vh)
+    j1.record()
+    barrier()
+    jv_ms = maxall(j0.elapsed_time(j1))
+    jv_per_s = args.jv / (jv_ms / 1e3)
+    hbm, hbm_src = peaks()
+    jv_gbs = 4.0 * 8.0 * n_local * world / (jv_ms / 1e3 / args.jv) / 1e9
+    out["jv"] = {"products": args.jv, "jv_per_s": jv_per_s,
+                 "grid_point_updates_per_s": jv_per_s * cells_global,
+                 "us_per_jv": jv_ms * 1e3 / args.jv, "alg_GBps_per_gpu": jv_gbs / world,
+                 "frac_of_hbm": jv_gbs / world / hbm}
+
+    # ---- instrumented pass (same K steps): per-kernel launch times on the launching stream
+    lib = N.lib()
+    ins = Instrument(lib, n_local, events=True)
+    barrier()
+    for _ in range(args.steps):
+        step()
+    barrier()
+    table = ins.table()
+    launches_per_step = ins.count / args.steps
+    ins.restore()
+    kern = []
+    for name, a_ in sorted(table.items(), key=lambda kv: -kv[1]["ms"]):
+        avg_us = a_["ms"] * 1e3 / a_["launches"]
+        gbs = a_["bytes"] / (a_["ms"] / 1e3) / 1e9 if a_["ms"] > 0 else 0.0
+        kern.append({"kernel": name, "launches": a_["launches"], "avg_us": avg_us,
+                     "share_of_step": a_["ms"] / args.steps / (t_ms / args.steps),
+                     "alg_GBps": gbs, "frac": gbs / hbm})
+    top = kern[0]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(top["kernel"])
+    out["roofline"] = {"bound": "hbm", "achieved": top["alg_GBps"], "peak": hbm, "unit": "GB/s",
+                       "frac": top["alg_GBps"] / hbm, "traffic": traffic,
+                       "kernel": top["kernel"], "peak_source": hbm_src,
+                       "alg_bytes_rule": "multidot (nvec+1)*L*8, update (nvec+2)*L*8, "
+                                         "jv_normalized 5W, jv 4W, rhs 2W (SURVEY 8d)"}
+    out["kernels"] = kern
+    out["gpu_launches"] = int(round(launches_per_step * args.steps))
+    # whole-iteration roofline: (3j + 11) W per iteration, j = 0..m-1
+    W = 8.0 * n_local
+    alg_iter = sum((3 * j + 11) * W for j in range(args.m))
+    out["iteration_roofline"] = {"alg_GB_per_step_per_gpu": alg_iter / 1e9,
+                                 "achieved_GBps_per_gpu": alg_iter / (t_ms / args.steps / 1e3) / 1e9,
+                                 "frac": alg_iter / (t_ms / args.steps / 1e3) / 1e9 / hbm}
+
+    # ---- end to end through the public API with host buffers
+    if not args.no_e2e:
+        hb = torch.empty((args.m + 1) * args.m, dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            a_d = a_pin.to("cuda", non_blocking=True)
+            v_d = v_pin.to("cuda", non_blocking=True)
+            jop = P.FdJacobianOperator(f, a_d)
+            bb = P.arnoldi(jop, v_d, args.m)
+            hb.copy_(bb.H.reshape(-1), non_blocking=True)
+            return bb
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        q1.record()
+        barrier()
+        e2e_ms = maxall(q0.elapsed_time(q1))
+        out["e2e"] = {"value": iters / (e2e_ms / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": int(2 * 8 * n_local),
+                      "d2h_bytes_per_step": int(8 * (args.m + 1) * args.m),
+                      "ms_per_step": e2e_ms / args.steps,
+                      "path": "numpy-pinned host a, v -> FdJacobianOperator(make_rhs) -> arnoldi -> H"}
+
+    # ---- CPU baseline (rank 0, N = 1): the oracle port, bounded sample, extrapolated
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, g, prm, U, v)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args, g, prm, U, v, iters=3):
+    """Oracle Arnoldi at full size: time `iters` iterations, fit t_j = a + b j, sum to m."""
+    from oracle import jvp, krylov_cpu, stencil
+    bc = type("BC", (), {"x": "periodic", "y": "periodic"})()
+    f = stencil.rhs_closure(prm, g, bc)
+    a = U.reshape(-1)
+    op = jvp.FdJv(f, a)
+    proc = krylov_cpu.Arnoldi(op, v, args.m)
+    ts = []
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        proc.grow()
+        ts.append(time.perf_counter() - t0)
+    j = np.arange(iters)
+    b, a0 = np.polyfit(j, np.array(ts), 1) if iters > 1 else (0.0, ts[0])
+    total = sum(max(a0 + b * k, ts[0]) for k in range(args.m))
+    return {"value": args.m / total, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle (numpy restatement of krylov.py MGS2 + fdjac + mhd.rhs) "
+                      f"arnoldi on the full {args.n}^2 state: {iters} iterations timed "
+                      f"({', '.join('%.2fs' % t for t in ts)}), per-iteration cost fitted "
+                      f"linear in j and summed to m={args.m} (extrapolated); numpy "
+                      f"elementwise is single-threaded",
+            "measured_iter_s": ts}
+
+
+# ----------------------------------------------------------- reference arm
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import jvp, krylov_cpu, stencil
+    g, prm, U, v = make_inputs(args)
+    bc = type("BC", (), {"x": "periodic", "y": "periodic"})()
+    f = stencil.rhs_closure(prm, g, bc)
+    a = U.reshape(-1)
+    op = jvp.FdJv(f, a)
+    m_sample = 2
+
+    def step():
+        krylov_cpu.arnoldi(op, v, m_sample)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    T = time.perf_counter() - t0
+    value = m_sample * args.steps / T
+    cores = os.cpu_count()
+    sample = (f"oracle port (numpy restatement of the reference's arnoldi/MGS2 + "
+              f"FdJacobianOperator + mhd.rhs; the reference is pure Python) on the full "
+              f"{args.n}^2 config-2 state, {m_sample} Arnoldi iterations per step from a fresh "
+              f"basis (the cheapest iterations of the m={args.m} run)")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_dict(args, world), "impl": "reference",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
