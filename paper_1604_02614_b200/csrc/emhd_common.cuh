@@ -52,4 +52,34 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Reduce K per-lane values across a warp with K-1 + (5 - log2 K) double shuffles
+// (halving exchange, then a butterfly).  Afterwards lanes with (lane & (32/K - 1)) == 0
+// hold the warp total of value index multi_index<K>(lane) in v[0].
+template <int K>
+__device__ __forceinline__ void warp_reduce_multi(double (&v)[K], int lane) {
+  int k = K;
+  int off = 16;
+#pragma unroll
+  for (int st = 0; st < 5 && (K >> st) > 1; ++st, off >>= 1) {
+    k = K >> st;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < (K >> (st + 1)); ++i) {
+      const double send = upper ? v[i] : v[i + (K >> (st + 1))];
+      const double keep = upper ? v[i + (K >> (st + 1))] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  (void)k;
+  for (; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+}
+
+template <int K>
+__device__ __forceinline__ int multi_index(int lane) {
+  int idx = 0, off = 16;
+#pragma unroll
+  for (int b = K; b > 1; b >>= 1, off >>= 1) idx = idx * 2 + ((lane & off) ? 1 : 0);
+  return idx;
+}
+
 }  // namespace emhd

@@ -18,8 +18,8 @@
 namespace emhd {
 
 constexpr int KT = 256;          // threads per CTA
-constexpr int EPT = 2;           // elements per thread per tile (one double2)
-constexpr int TILE = KT * EPT;   // 512 elements per tile
+constexpr int EPT = 2;           // elements per double2
+constexpr int TILE = KT * EPT;   // 512 elements per combine tile
 constexpr int NWARP = KT / 32;
 
 // Last-CTA deterministic reduction of partials[nval][G] -> out[nval].
@@ -62,46 +62,63 @@ __device__ __forceinline__ void cta_store_partials(double* s_acc, int nval, doub
   }
 }
 
+__device__ __forceinline__ double2 ld2(const double* p, long long e, long long len) {
+  if (e + 1 < len) return __ldg(reinterpret_cast<const double2*>(p + e));
+  double2 r = make_double2(0.0, 0.0);
+  if (e < len) r.x = __ldg(p + e);
+  return r;
+}
+__device__ __forceinline__ double2 ld2_stream(const double* p, long long e, long long len) {
+  if (e + 1 < len) return __ldcs(reinterpret_cast<const double2*>(p + e));
+  double2 r = make_double2(0.0, 0.0);
+  if (e < len) r.x = __ldcs(p + e);
+  return r;
+}
+
 // out[i] = <w, V_i>, i < nvec (over len_dot); optional out[nvec] = <w, w>.
-__global__ void __launch_bounds__(KT) multidot_kernel(const double* __restrict__ w,
+// Each thread streams VEC double2 of w per tile and U basis vectors per step
+// (2*VEC*U independent 16-byte loads in flight); per (tile, vector) one warp
+// shuffle-reduction into a per-warp shared slot; deterministic CTA partials.
+template <int VEC, int U>
+__global__ void __launch_bounds__(KT, 4) multidot_kernel(const double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, long long len_dot, int self,
     double* partials, double* out, unsigned int* ticket) {
   extern __shared__ double s_acc[];            // [(nvec+1)][NWARP]
+  constexpr int TL = KT * 2 * VEC;
   const int nval = nvec + self;
   for (int k = threadIdx.x; k < nval * NWARP; k += KT) s_acc[k] = 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double selfacc = 0.0;
-  const long long ntiles = (len_dot + TILE - 1) / TILE;
+  const long long ntiles = (len_dot + TL - 1) / TL;
   for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-    const long long e = tl * TILE + (long long)threadIdx.x * EPT;
-    double2 wv = make_double2(0.0, 0.0);
-    if (e + 1 < len_dot) wv = __ldcs(reinterpret_cast<const double2*>(w + e));
-    else if (e < len_dot) wv.x = w[e];
-    selfacc = fma(wv.x, wv.x, fma(wv.y, wv.y, selfacc));
-    int i = 0;
-    for (; i + 4 <= nvec; i += 4) {
-      double2 x[4];
+    const long long e0 = tl * TL + 2LL * threadIdx.x;
+    double2 wv[VEC];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double* Vi = V + (size_t)(i + u) * ldv;
-        x[u] = make_double2(0.0, 0.0);
-        if (e + 1 < len_dot) x[u] = __ldcs(reinterpret_cast<const double2*>(Vi + e));
-        else if (e < len_dot) x[u].x = Vi[e];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        double d = warp_sum(fma(wv.x, x[u].x, wv.y * x[u].y));
-        if (lane == 0) s_acc[(i + u) * NWARP + warp] += d;
-      }
+    for (int s = 0; s < VEC; ++s) {
+      wv[s] = ld2_stream(w, e0 + (long long)s * 2 * KT, len_dot);
+      selfacc = fma(wv[s].x, wv[s].x, fma(wv[s].y, wv[s].y, selfacc));
     }
-    for (; i < nvec; ++i) {
-      const double* Vi = V + (size_t)i * ldv;
-      double2 x = make_double2(0.0, 0.0);
-      if (e + 1 < len_dot) x = __ldcs(reinterpret_cast<const double2*>(Vi + e));
-      else if (e < len_dot) x.x = Vi[e];
-      double d = warp_sum(fma(wv.x, x.x, wv.y * x.y));
-      if (lane == 0) s_acc[i * NWARP + warp] += d;
+    for (int i = 0; i < nvec; i += U) {
+      double2 x[U][VEC];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < VEC; ++s)
+          x[u][s] = (i + u < nvec) ? ld2_stream(V + (size_t)(i + u) * ldv, e0 + (long long)s * 2 * KT, len_dot)
+                                   : make_double2(0.0, 0.0);
+      double d[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        d[u] = 0.0;
+#pragma unroll
+        for (int s = 0; s < VEC; ++s) d[u] = fma(wv[s].x, x[u][s].x, fma(wv[s].y, x[u][s].y, d[u]));
+      }
+      warp_reduce_multi<U>(d, lane);
+      if ((lane & (32 / U - 1)) == 0) {
+        const int u = multi_index<U>(lane);
+        if (i + u < nvec) s_acc[(i + u) * NWARP + warp] += d[0];
+      }
     }
   }
   if (self) {
@@ -112,80 +129,60 @@ __global__ void __launch_bounds__(KT) multidot_kernel(const double* __restrict__
   finish_partials(partials, nval, gridDim.x, nullptr, out, ticket);
 }
 
-// w[0:len_upd] -= sum_i h[i] V_i ; then out[i] = <w_new, V_i> over len_dot.
-// mode 0: re-dot (CGS2 pass-2 projections); mode 1: out = {sum w^2 (len_dot), max|w| (len_max)}
-__global__ void __launch_bounds__(KT) update_kernel(double* __restrict__ w,
+// w[0:len_upd] -= sum_i h[i] V_i ; MODE 0: out[i] = <w_new, V_i> over len_dot (the
+// CGS2 re-projection; the second read of each V tile hits L1/L2, not DRAM);
+// MODE 1: out = {sum w^2 over len_dot, max|w| over len_max}.
+template <int MODE, int U>
+__global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, const double* __restrict__ h,
-    long long len_upd, long long len_dot, long long len_max, int mode,
+    long long len_upd, long long len_dot, long long len_max,
     double* partials, double* out, unsigned int* ticket) {
   extern __shared__ double sm[];
+  constexpr int TL = KT * 2;
   double* s_h = sm;                              // [nvec]
   double* s_acc = sm + ((nvec + 1) & ~1);        // [(nvec or 2)][NWARP]
-  const int nval = mode == 0 ? nvec : 2;
+  const int nval = MODE == 0 ? nvec : 2;
   for (int k = threadIdx.x; k < nvec; k += KT) s_h[k] = h[k];
   for (int k = threadIdx.x; k < nval * NWARP; k += KT) s_acc[k] = 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double ss = 0.0, mx = 0.0;
-  const long long ntiles = (len_upd + TILE - 1) / TILE;
+  const long long ntiles = (len_upd + TL - 1) / TL;
   for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-    const long long e = tl * TILE + (long long)threadIdx.x * EPT;
+    const long long e = tl * TL + 2LL * threadIdx.x;
     const bool full = e + 1 < len_upd;
-    double2 wv = make_double2(0.0, 0.0);
-    if (full) wv = *reinterpret_cast<const double2*>(w + e);
-    else if (e < len_upd) wv.x = w[e];
-    int i = 0;
-    for (; i + 4 <= nvec; i += 4) {
-      double2 x[4];
+    double2 wv = ld2(w, e, len_upd);
+    for (int i = 0; i < nvec; i += U) {
+      double2 x[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double* Vi = V + (size_t)(i + u) * ldv;
-        x[u] = make_double2(0.0, 0.0);
-        if (full) x[u] = __ldg(reinterpret_cast<const double2*>(Vi + e));
-        else if (e < len_upd) x[u].x = Vi[e];
-      }
+      for (int u = 0; u < U; ++u)
+        x[u] = (i + u < nvec) ? ld2(V + (size_t)(i + u) * ldv, e, len_upd) : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        wv.x = fma(-s_h[i + u], x[u].x, wv.x);
-        wv.y = fma(-s_h[i + u], x[u].y, wv.y);
+      for (int u = 0; u < U; ++u) {
+        if (i + u < nvec) {
+          const double hh = s_h[i + u];
+          wv.x = fma(-hh, x[u].x, wv.x);
+          wv.y = fma(-hh, x[u].y, wv.y);
+        }
       }
-    }
-    for (; i < nvec; ++i) {
-      const double* Vi = V + (size_t)i * ldv;
-      double2 x = make_double2(0.0, 0.0);
-      if (full) x = __ldg(reinterpret_cast<const double2*>(Vi + e));
-      else if (e < len_upd) x.x = Vi[e];
-      wv.x = fma(-s_h[i], x.x, wv.x);
-      wv.y = fma(-s_h[i], x.y, wv.y);
     }
     if (full) *reinterpret_cast<double2*>(w + e) = wv;
     else if (e < len_upd) w[e] = wv.x;
-    // mask entries beyond the dot / max ranges
     const double dx = (e < len_dot) ? wv.x : 0.0, dy = (e + 1 < len_dot) ? wv.y : 0.0;
-    if (mode == 0) {
-      int k = 0;
-      for (; k + 4 <= nvec; k += 4) {
-        double2 x[4];
+    if (MODE == 0) {
+      for (int i = 0; i < nvec; i += U) {
+        double2 x[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double* Vi = V + (size_t)(k + u) * ldv;
-          x[u] = make_double2(0.0, 0.0);
-          if (full) x[u] = __ldg(reinterpret_cast<const double2*>(Vi + e));
-          else if (e < len_upd) x[u].x = Vi[e];
-        }
+        for (int u = 0; u < U; ++u)
+          x[u] = (i + u < nvec) ? ld2_stream(V + (size_t)(i + u) * ldv, e, len_upd) : make_double2(0.0, 0.0);
+        double d[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          double d = warp_sum(fma(dx, x[u].x, dy * x[u].y));
-          if (lane == 0) s_acc[(k + u) * NWARP + warp] += d;
+        for (int u = 0; u < U; ++u) d[u] = fma(dx, x[u].x, dy * x[u].y);
+        warp_reduce_multi<U>(d, lane);
+        if ((lane & (32 / U - 1)) == 0) {
+          const int u = multi_index<U>(lane);
+          if (i + u < nvec) s_acc[(i + u) * NWARP + warp] += d[0];
         }
-      }
-      for (; k < nvec; ++k) {
-        const double* Vi = V + (size_t)k * ldv;
-        double2 x = make_double2(0.0, 0.0);
-        if (full) x = __ldg(reinterpret_cast<const double2*>(Vi + e));
-        else if (e < len_upd) x.x = Vi[e];
-        double d = warp_sum(fma(dx, x.x, dy * x.y));
-        if (lane == 0) s_acc[k * NWARP + warp] += d;
       }
     } else {
       ss = fma(dx, dx, fma(dy, dy, ss));
@@ -194,7 +191,7 @@ __global__ void __launch_bounds__(KT) update_kernel(double* __restrict__ w,
       mx = fmax(mx, fmax(mxx, mxy));
     }
   }
-  if (mode == 1) {
+  if (MODE == 1) {
     ss = warp_sum(ss);
     mx = warp_max(mx);
     if (lane == 0) { s_acc[0 * NWARP + warp] = ss; s_acc[1 * NWARP + warp] = mx; }
@@ -307,28 +304,32 @@ __global__ void __launch_bounds__(KT) combine_kernel(const double* __restrict__ 
   }
 }
 
-static int grid_for(long long len, int num_sms) {
-  long long tiles = (len + TILE - 1) / TILE;
-  long long g = 2LL * num_sms;
+static int grid_for(long long len, int tile, int num_sms) {
+  long long tiles = (len + tile - 1) / tile;
+  long long g = 4LL * num_sms;
   return (int)(tiles < g ? (tiles < 1 ? 1 : tiles) : g);
 }
 
 cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
                             int self, KWork& wk, double* out, cudaStream_t s) {
-  const int G = grid_for(len_dot, wk.num_sms);
+  const int G = grid_for(len_dot, KT * 4, wk.num_sms);
   const size_t sm = sizeof(double) * (size_t)(nvec + 1) * NWARP;
-  multidot_kernel<<<G, KT, sm, s>>>(w, V, ldv, nvec, len_dot, self, wk.partials, out, wk.ticket);
+  multidot_kernel<2, 4><<<G, KT, sm, s>>>(w, V, ldv, nvec, len_dot, self, wk.partials, out, wk.ticket);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
                           KWork& wk, double* out, cudaStream_t s) {
-  const int G = grid_for(len_upd, wk.num_sms);
+  const int G = grid_for(len_upd, KT * 2, wk.num_sms);
   const int nval = mode == 0 ? nvec : 2;
   const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)(nval > 0 ? nval : 1) * NWARP);
-  update_kernel<<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode,
-                                   wk.partials, out, wk.ticket);
+  if (mode == 0)
+    update_kernel<0, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
+                                           wk.partials, out, wk.ticket);
+  else
+    update_kernel<1, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
+                                           wk.partials, out, wk.ticket);
   return cudaGetLastError();
 }
 

@@ -87,6 +87,41 @@ __device__ __forceinline__ void load_cell(const StencilParams& P, const RowRef& 
   if (yflip) { u[2] = -u[2]; u[5] = -u[5]; }
 }
 
+// raw (unperturbed) inputs of one cell, fetched one row ahead of their use
+template <int MODE>
+struct RawCell {
+  double a[NF];
+  double v[MODE == MODE_RHS ? 1 : NF];
+};
+
+template <int MODE>
+__device__ __forceinline__ void fetch_cell(const StencilParams& P, const RowRef& R, int jsrc,
+                                           RawCell<MODE>& x) {
+  const double* A = R.halo ? P.a_halo : P.a;
+  const long long o = R.off + jsrc;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) x.a[f] = __ldg(A + o + f * R.fs);
+  if (MODE != MODE_RHS) {
+    const double* Vv = R.halo ? P.v_halo : P.v;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) x.v[f] = __ldg(Vv + o + f * R.fs);
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void combine_cell(const RawCell<MODE>& x, bool xflip, bool yflip,
+                                             double sigma, double hnext, double rh, double u[NF]) {
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    double val = x.a[f];
+    if (MODE == MODE_JV) val = __dadd_rn(val, __dmul_rn(sigma, x.v[f]));
+    if (MODE == MODE_JVN) val = __dadd_rn(val, __dmul_rn(sigma, div_const(x.v[f], hnext, rh)));
+    u[f] = val;
+  }
+  if (xflip) { u[1] = -u[1]; u[4] = -u[4]; }
+  if (yflip) { u[2] = -u[2]; u[5] = -u[5]; }
+}
+
 // pressure / admissibility / primitives (mhd.py:106-131, 176-181, 217-221)
 __device__ __forceinline__ void cell_prims(const StencilParams& P, const double u[NF],
                                            double* q, int qs, int& flag) {
@@ -271,22 +306,57 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
     const int je = cextra >= 0 ? map_ghost(j0 - 2 + cextra, P.ny, P.bcy, fe) : 0;
     const bool okm = col_ok(cmain), oke = cextra >= 0 && col_ok(cextra);
 
-    const int nsteps = (i1 - i0) + 4;
-    for (int s = 0; s < nsteps; ++s) {
-      const int r = i0 - 2 + s;                // prim row
-      // ---- primitives of row r
+    // prologue: primitives of rows i0-2 and i0-1
+    for (int r = i0 - 2; r < i0; ++r) {
+      const RowRef R = row_ref(P, r);
+      double* q = qring + ((r + 3) % 3) * NQ * QW;
+      double u[NF];
+      if (okm) {
+        load_cell<MODE>(P, R, jm, fm, sigma, hnext, rh, u);
+        cell_prims(P, u, q + cmain, QW, flag);
+      }
+      if (oke) {
+        load_cell<MODE>(P, R, je, fe, sigma, hnext, rh, u);
+        cell_prims(P, u, q + cextra, QW, flag);
+      }
+    }
+    // software pipeline: the raw inputs of row r+1 are in flight while the
+    // fluxes of row r-1 and the outputs of row r-2 are computed
+    RawCell<MODE> xm, xe;
+    double fa_pre[NF];                       // F(a) of the next output row, one step ahead
+    if (MODE != MODE_RHS && t < ncols_out) {
+      const long long o = (long long)i0 * P.ny + j0 + t;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o + (long long)f * P.nx * P.ny);
+    }
+    RowRef Rn = row_ref(P, i0);
+    if (okm) fetch_cell<MODE>(P, Rn, jm, xm);
+    if (oke) fetch_cell<MODE>(P, Rn, je, xe);
+    for (int r = i0; r <= i1 + 1; ++r) {
+      // ---- primitives of row r (prefetched)
       {
-        const RowRef R = row_ref(P, r);
         double* q = qring + ((r + 3) % 3) * NQ * QW;
         double u[NF];
         if (okm) {
-          load_cell<MODE>(P, R, jm, fm, sigma, hnext, rh, u);
+          combine_cell<MODE>(xm, Rn.flip, fm, sigma, hnext, rh, u);
           cell_prims(P, u, q + cmain, QW, flag);
+          if (MODE == MODE_JVN && r >= i0 && r < i1 && t < ncols_out) {
+            // v_j = w / h_next of an owned cell (krylov.py:167), from the fetched w
+            const long long o = (long long)r * P.ny + j0 + t;
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+              P.vout[o + (long long)f * P.nx * P.ny] = div_const(xm.v[f], hnext, rh);
+          }
         }
         if (oke) {
-          load_cell<MODE>(P, R, je, fe, sigma, hnext, rh, u);
+          combine_cell<MODE>(xe, Rn.flip, fe, sigma, hnext, rh, u);
           cell_prims(P, u, q + cextra, QW, flag);
         }
+      }
+      if (r + 1 <= i1 + 1) {
+        Rn = row_ref(P, r + 1);
+        if (okm) fetch_cell<MODE>(P, Rn, jm, xm);
+        if (oke) fetch_cell<MODE>(P, Rn, je, xe);
       }
       __syncthreads();
       // ---- fluxes of row rf = r - 1
@@ -342,15 +412,19 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
                   (unsigned long long)(P.x_off + ro) * P.ny + j0 + t;
               bad = gidx < bad ? gidx : bad;
             }
-            double jv = div_const(__dsub_rn(F, __ldg(P.fa + idx)), sigma, rsig);   // fdjac.py:49
+            double jv = div_const(__dsub_rn(F, fa_pre[f]), sigma, rsig);   // fdjac.py:49
             if (AUG) {
               jv = __dmul_rn(P.ch, jv);
               for (int k = 0; k < P.nb; ++k)
                 jv = __dadd_rn(jv, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
             }
             P.out[idx] = jv;
-            if (MODE == MODE_JVN) P.vout[idx] = div_const(__ldg(P.v + idx), hnext, rh);
           }
+        }
+        if (MODE != MODE_RHS && ro + 1 < i1) {
+          const long long o2 = o + P.ny;
+#pragma unroll
+          for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o2 + (long long)f * P.nx * P.ny);
         }
       }
     }
