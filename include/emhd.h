@@ -74,7 +74,7 @@ typedef struct emhd_status {
   int rhs_evals;                       /* stencil evaluations executed (device-counted) */
   unsigned long long first_nonfinite;  /* flat index of the first non-finite F(a+sigma v) */
   int breakdown;                       /* Arnoldi lucky breakdown seen */
-  int pad;
+  int fail_iter;                       /* epoch (emhd_set_epoch) of the first flagging stencil */
 } emhd_status;
 
 /* ---- context -------------------------------------------------------- */
@@ -84,6 +84,8 @@ int emhd_ctx_create(emhd_ctx** ctx, const emhd_geometry* g, const emhd_physics* 
 int emhd_ctx_destroy(emhd_ctx* ctx);
 int emhd_set_stream(emhd_ctx* ctx, void* cuda_stream);
 int emhd_num_sms(emhd_ctx* ctx);
+/* tag recorded (atomic min) in emhd_status.fail_iter by stencil launches that flag an error */
+int emhd_set_epoch(emhd_ctx* ctx, int epoch);
 /* synchronous read of the device status word (stream-ordered) */
 int emhd_status_read(emhd_ctx* ctx, emhd_status* out);
 int emhd_status_reset(emhd_ctx* ctx);
@@ -124,9 +126,12 @@ int emhd_update(emhd_ctx* ctx, double* w, const double* V, long long ldv, int nv
 /* out = {sum x^2 over len_sum, max|x| over len_max} */
 int emhd_norms(emhd_ctx* ctx, const double* x, long long len_sum, long long len_max, double* out);
 /* H[:j+1, j] = h1 + h2; hnext = sqrt(nrm[0]); breakdown if hnext <= 1e-12 max(sqrt(selfdot), 1);
- * scal = {hnext, nrm[1], breakdown} */
+ * scal = {hnext, nrm[1], breakdown}; brk_hist (optional) [j] = breakdown flag of iteration j.
+ * Once scal[2] != 0 the next emhd_jv_normalized launch does no work (lets a caller queue
+ * iterations ahead of its breakdown check). */
 int emhd_arnoldi_finish(emhd_ctx* ctx, const double* h1, const double* h2, const double* nrm,
-                        const double* selfdot, int j, double* H, long long ldh, double* scal);
+                        const double* selfdot, int j, double* H, long long ldh, double* scal,
+                        double* brk_hist);
 /* out = x / d (d = sqrt(*d) when take_sqrt); d_out receives d.  (krylov.py:137, :167) */
 int emhd_div_scalar(emhd_ctx* ctx, const double* x, const double* d, int take_sqrt, double* out,
                     double* d_out, long long n);

@@ -30,7 +30,7 @@ class Physics(ctypes.Structure):
 
 class Status(ctypes.Structure):
     _fields_ = [("flags", c_int), ("rhs_evals", c_int), ("first_nonfinite", ctypes.c_ulonglong),
-                ("breakdown", c_int), ("pad", c_int)]
+                ("breakdown", c_int), ("fail_iter", c_int)]
 
 
 class Report(ctypes.Structure):
@@ -57,7 +57,8 @@ _SIGS = {
     "emhd_multidot": (c_int, [c_vp, P, P, c_ll, c_int, c_ll, c_int, P]),
     "emhd_update": (c_int, [c_vp, P, P, c_ll, c_int, P, c_ll, c_ll, c_ll, c_int, P]),
     "emhd_norms": (c_int, [c_vp, P, c_ll, c_ll, P]),
-    "emhd_arnoldi_finish": (c_int, [c_vp, P, P, P, P, c_int, P, c_ll, P]),
+    "emhd_arnoldi_finish": (c_int, [c_vp, P, P, P, P, c_int, P, c_ll, P, P]),
+    "emhd_set_epoch": (c_int, [c_vp, c_int]),
     "emhd_div_scalar": (c_int, [c_vp, P, P, c_int, P, P, c_ll]),
     "emhd_phi_small": (c_int, [c_vp, P, c_ll, c_int, c_int, c_int, P, P, P, P, P, P]),
     "emhd_expm": (c_int, [c_vp, P, c_int, P, P]),

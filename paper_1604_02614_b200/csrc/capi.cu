@@ -26,6 +26,7 @@ struct emhd_ctx {
   double* dense = nullptr;            // dense workspace
   size_t dense_len = 0;
   StencilParams base{};
+  int epoch = 0;
 };
 
 static int cerr(cudaError_t e) {
@@ -113,10 +114,17 @@ extern "C" int emhd_set_stream(emhd_ctx* c, void* s) {
 
 extern "C" int emhd_num_sms(emhd_ctx* c) { return c ? c->num_sms : 0; }
 
+extern "C" int emhd_set_epoch(emhd_ctx* c, int epoch) {
+  if (!c) return EMHD_ERR_ARG;
+  c->epoch = epoch;
+  return EMHD_OK;
+}
+
 extern "C" int emhd_status_reset(emhd_ctx* c) {
   if (!c) return EMHD_ERR_ARG;
   DevStatus h{};
   h.first_nonfinite = ~0ull;
+  h.fail_iter = 0x7fffffff;
   // small H2D copy from a stack value must complete before return: use the pinned mirror
   *c->st_host = h;
   int rc = cerr(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevStatus), cudaMemcpyHostToDevice, c->stream));
@@ -133,7 +141,7 @@ extern "C" int emhd_status_read(emhd_ctx* c, emhd_status* out) {
   out->rhs_evals = c->st_host->rhs_evals;
   out->first_nonfinite = c->st_host->first_nonfinite;
   out->breakdown = c->st_host->breakdown;
-  out->pad = 0;
+  out->fail_iter = c->st_host->fail_iter;
   return EMHD_OK;
 }
 
@@ -149,6 +157,7 @@ static void set_epilogue(StencilParams& P, int p, double ch, int nb, const doubl
 extern "C" int emhd_rhs(emhd_ctx* c, const double* u, const double* u_halo, double* F) {
   if (!c || !u || !F) return EMHD_ERR_ARG;
   StencilParams P = c->base;
+  P.epoch = c->epoch;
   P.a = u; P.a_halo = u_halo; P.out = F;
   return cerr(launch_stencil(P, MODE_RHS, false, c->num_sms, c->stream));
 }
@@ -157,6 +166,7 @@ extern "C" int emhd_jv(emhd_ctx* c, const double* a, const double* a_halo, const
                        const double* v, const double* v_halo, const double* d_vnorm, double* out) {
   if (!c || !a || !fa || !v || !d_vnorm || !out) return EMHD_ERR_ARG;
   StencilParams P = c->base;
+  P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = v; P.v_halo = v_halo; P.scal = d_vnorm; P.out = out;
   return cerr(launch_stencil(P, MODE_JV, false, c->num_sms, c->stream));
 }
@@ -168,6 +178,7 @@ extern "C" int emhd_jv_aug(emhd_ctx* c, const double* a, const double* a_halo, c
   if (!c || !a || !fa || !u || !d_vnorm || !out || p < 1 || p > 5 || nb < 0 || nb > 5 || !d_q)
     return EMHD_ERR_ARG;
   StencilParams P = c->base;
+  P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = u; P.v_halo = u_halo; P.scal = d_vnorm; P.out = out;
   P.qsrc = d_q;
   set_epilogue(P, p, ch, nb, bcol, bidx);
@@ -181,6 +192,7 @@ extern "C" int emhd_jv_normalized(emhd_ctx* c, const double* a, const double* a_
   if (!c || !a || !fa || !w || !d_scal || !v_out || !out || p < 0 || p > 5 || nb < 0 || nb > 5)
     return EMHD_ERR_ARG;
   StencilParams P = c->base;
+  P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = w; P.v_halo = w_halo; P.scal = d_scal;
   P.out = out; P.vout = v_out;
   set_epilogue(P, p, ch, nb, bcol, bidx);
@@ -216,9 +228,11 @@ extern "C" int emhd_norms(emhd_ctx* c, const double* x, long long len_sum, long 
 }
 
 extern "C" int emhd_arnoldi_finish(emhd_ctx* c, const double* h1, const double* h2, const double* nrm,
-                                   const double* selfdot, int j, double* H, long long ldh, double* scal) {
+                                   const double* selfdot, int j, double* H, long long ldh, double* scal,
+                                   double* brk_hist) {
   if (!c || !h1 || !h2 || !nrm || !selfdot || !H || !scal || j < 0) return EMHD_ERR_ARG;
-  return cerr(launch_arnoldi_finish(h1, h2, nrm, selfdot, j, H, ldh, scal, c->st, 1e-12, c->stream));
+  return cerr(launch_arnoldi_finish(h1, h2, nrm, selfdot, j, H, ldh, scal, brk_hist, c->st, 1e-12,
+                                    c->stream));
 }
 
 extern "C" int emhd_div_scalar(emhd_ctx* c, const double* x, const double* d, int take_sqrt, double* out,
@@ -352,6 +366,7 @@ extern "C" int emhd_admissibility_report(emhd_ctx* c, int mode, const double* a,
                                          void* report) {
   if (!c || !a || !report || mode < 0 || mode > 2) return EMHD_ERR_ARG;
   StencilParams P = c->base;
+  P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.v = v; P.v_halo = v_halo; P.scal = scal;
   unsigned long long* keys = nullptr;
   int rc = cerr(cudaMalloc(&keys, 4 * sizeof(unsigned long long)));

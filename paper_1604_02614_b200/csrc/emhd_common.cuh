@@ -18,7 +18,7 @@ struct DevStatus {
   int rhs_evals;
   unsigned long long first_nonfinite;   // flat index of first non-finite Jv entry
   int breakdown;
-  int pad;
+  int fail_iter;                        // epoch of the first stencil launch that flagged
 };
 
 // Correctly rounded x / d for a constant divisor d with r = RN(1/d), using

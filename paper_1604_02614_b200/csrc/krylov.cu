@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(KT) norms_kernel(const double* __restrict__ x,
 // H[0:j+1, j] = h1 + h2 ; hnext = sqrt(ss) ; breakdown test (krylov.py:161-166);
 // scal = {hnext, max|w_top|} for the next fused normalise + Jv.
 __global__ void arnoldi_finish_kernel(const double* h1, const double* h2, const double* nrm,
-    const double* selfdot, int j, double* H, long long ldh, double* scal, DevStatus* st,
-    double rtol) {
+    const double* selfdot, int j, double* H, long long ldh, double* scal, double* brk_hist,
+    DevStatus* st, double rtol) {
   for (int i = threadIdx.x; i <= j; i += blockDim.x) H[(size_t)i * ldh + j] = h1[i] + h2[i];
   if (threadIdx.x == 0) {
     const double hnext = sqrt(nrm[0]);
@@ -258,6 +258,7 @@ __global__ void arnoldi_finish_kernel(const double* h1, const double* h2, const 
     scal[0] = hnext;
     scal[1] = nrm[1];
     scal[2] = brk ? 1.0 : 0.0;
+    if (brk_hist) brk_hist[j] = brk ? 1.0 : 0.0;
   }
 }
 
@@ -344,8 +345,8 @@ cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, 
 
 cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,
                                   const double* selfdot, int j, double* H, long long ldh, double* scal,
-                                  DevStatus* st, double rtol, cudaStream_t s) {
-  arnoldi_finish_kernel<<<1, 128, 0, s>>>(h1, h2, nrm, selfdot, j, H, ldh, scal, st, rtol);
+                                  double* brk_hist, DevStatus* st, double rtol, cudaStream_t s) {
+  arnoldi_finish_kernel<<<1, 128, 0, s>>>(h1, h2, nrm, selfdot, j, H, ldh, scal, brk_hist, st, rtol);
   return cudaGetLastError();
 }
 

@@ -25,7 +25,7 @@ cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, 
                          cudaStream_t s);
 cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,
                                   const double* selfdot, int j, double* H, long long ldh, double* scal,
-                                  DevStatus* st, double rtol, cudaStream_t s);
+                                  double* brk_hist, DevStatus* st, double rtol, cudaStream_t s);
 cudaError_t launch_combine(const double* V, long long ldv, int m, const double* Y, int S,
                            const CombineOut& co, long long len, int num_sms, cudaStream_t s);
 

@@ -252,6 +252,16 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
     sigma = fd_sigma(vn);
     rsig = 1.0 / sigma;
   } else if (MODE == MODE_JVN) {
+    if (P.scal[2] != 0.0) {
+      // the previous iteration broke down: this launch was queued ahead of the host's
+      // breakdown check; leave no trace (zero output, no flags, no RHS count)
+      for (long long r = i0; r < i1; ++r)
+        if (t < min(TY, P.ny - j0))
+#pragma unroll
+          for (int f = 0; f < NF; ++f) P.out[r * P.ny + j0 + t + (long long)f * P.nx * P.ny] = 0.0;
+      if (blockIdx.x == 0 && blockIdx.y == 0 && t < P.p) P.out[P.n_top + t] = 0.0;
+      return;
+    }
     hnext = P.scal[0];
     rh = 1.0 / hnext;
     const double vn = P.scal[1] / hnext;   // max|w/h| == fl(max|w| / h) (monotone rounding)
@@ -453,10 +463,14 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
   if (bad != ~0ull) atomicMin(&s_bad, bad);
   __syncthreads();
   if (t == 0) {
-    if (s_flag) atomicOr(&P.st->flags, s_flag);
+    if (s_flag) {
+      atomicOr(&P.st->flags, s_flag);
+      atomicMin(&P.st->fail_iter, P.epoch);
+    }
     if (s_bad != ~0ull) {
       atomicOr(&P.st->flags, (int)ST_NONFINITE);
       atomicMin(&P.st->first_nonfinite, s_bad);
+      atomicMin(&P.st->fail_iter, P.epoch);
     }
     if (!skip_stencil && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&P.st->rhs_evals, 1);
   }

@@ -31,6 +31,7 @@ struct StencilParams {
   double ch;                  // c*h scale of the augmented operator
   const double* qsrc;         // MODE_JV + tail: q (device, length p)
   DevStatus* st;
+  int epoch;                  // caller-defined launch tag recorded on failure
 };
 
 cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s);

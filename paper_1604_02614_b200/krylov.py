@@ -172,6 +172,10 @@ class _Process:
         self.d2 = D.zeros(k)
         self.nrm = D.zeros(2)
         self.scal = D.Scratch(4)
+        self.brk = D.zeros(self.m_cap + 1)
+        self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
+        self._settled = 0
+        self._pending = False
         self.nb = D.zeros(4)                 # {sum seed^2, max|seed|, beta, -}
         self.beta_dev = self.nb[2:3]
         self.m = 0
@@ -263,11 +267,17 @@ class _Process:
                                          D.ptr(self.V[upto]), 0, self.naug), "div_scalar")
         self._vm_ready = upto + 1
 
-    def extend(self):
-        """Add one basis vector; returns False on lucky breakdown (krylov.py:144-168)."""
+    def extend(self, sync=True):
+        """Add one basis vector; returns False on lucky breakdown (krylov.py:144-168).
+
+        With ``sync=False`` (fused engine only) the iteration is queued without
+        waiting for its breakdown test; ``settle()`` later resolves where the
+        factorisation stopped (a launch queued after a breakdown does no work).
+        """
         if self.breakdown or self.m >= self.m_cap:
             return False
         j = self.m
+        self.lib.emhd_set_epoch(self.ctx.sync_stream(), j)
         wi = self._apply(j)
         self.applies += 1
         w = self.w[wi]
@@ -287,31 +297,47 @@ class _Process:
         self._allreduce_norms(self.nrm)
         N.check(self.lib.emhd_arnoldi_finish(h, D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm),
                                              D.ptr(self.d1[nv:]), j, D.ptr(self.H), self.H.shape[1],
-                                             D.ptr(self.scal.dev)), "arnoldi_finish")
+                                             D.ptr(self.scal.dev), D.ptr(self.brk)), "arnoldi_finish")
         self.m = j + 1
-        s = self.scal.read(3)
-        self.check_status()
-        if s[2] != 0.0:
-            self.breakdown = True
-            return False
-        return True
+        if not sync and self.eng.fused:
+            self._pending = True
+            return True
+        return self.settle()
 
-    def check_status(self):
+    def settle(self):
+        """One host sync: breakdown position and the device status of queued iterations."""
+        self._pending = False
+        first = self._settled
+        self.brk_host[:self.m].copy_(self.brk[:self.m], non_blocking=True)
+        st = self.ctx.status() if self.eng.fused else None       # synchronises the stream
+        if not self.eng.fused:
+            torch.cuda.current_stream().synchronize()
+        flags = self.brk_host[first:self.m].numpy()
+        hit = np.flatnonzero(flags != 0.0)
+        if hit.size:
+            b = first + int(hit[0])
+            self.applies -= self.m - (b + 1)
+            self.m = b + 1
+            self.breakdown = True
+        self._settled = self.m
+        if st is not None:
+            self.check_status(st)
+        return not self.breakdown
+
+    def check_status(self, st):
         E = self.eng
-        if not E.fused:
-            return
-        st = self.ctx.status()
         if st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE):
-            mode, v, vh, sc = self._last
+            j = min(st.fail_iter, self.m - 1)
             a, ah = E.jop.a, E.jop.a_halo
-            if mode == 2:
-                # the failing state is a + sigma * V[j]; V[j] is materialised
-                v = self.V[self.m - 1]
-                vh = E.gpu.halo(v[:self.n_top])
-                sc = E._vn
-                N.check(self.lib.emhd_norms(self.ctx.sync_stream(), D.ptr(v), 0, self.n_top,
-                                            D.ptr(sc)), "norms")
-                sc[0:1].copy_(sc[1:2])
+            # the failing state is a + sigma V[j] with V[j] materialised
+            v = self.V[j]
+            vh = E.gpu.halo(v[:self.n_top])
+            sc = E._vn
+            N.check(self.lib.emhd_norms(self.ctx.sync_stream(), D.ptr(v), 0, self.n_top,
+                                        D.ptr(sc)), "norms")
+            if self.layout is not None and self.layout.distributed:
+                self.comm.allreduce_max(sc[1:2])
+            sc[0:1].copy_(sc[1:2])
             raise_status(self.ctx, st, (1, D.ptr(a), D.ptr(ah), D.ptr(v), D.ptr(vh), D.ptr(sc)))
 
     # -- views ------------------------------------------------------------------
@@ -394,8 +420,9 @@ def arnoldi(op, v, m, reorthogonalize=True):
     if m > n_glob:
         raise ValueError(f"basis size {m} exceeds operator dimension {op.n}")
     proc = _Process(eng, vd, m, vd.numel(), 0, layout, comm)
-    while proc.m < m and proc.extend():
+    while proc.m < m and proc.extend(sync=False):
         pass
+    proc.settle()
     return proc.basis(host=host)
 
 
@@ -444,8 +471,9 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
     c_big = max(scales)
     proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm)
     m_target = min(cfg.m_init, proc.n)
-    while proc.m < m_target and proc.extend():
+    while proc.m < m_target and proc.extend(sync=False):
         pass
+    proc.settle()
     while True:
         _, res_raw = proc.phi_coeffs(order, [c_big * h])
         r = float(res_raw[0].item())
@@ -522,8 +550,9 @@ def phi_comb(req, cfg=None, _zero=None):
         seed[n_top:n_top + p].copy_(torch.from_numpy(q))
         proc = _Process(eng, seed[:n_top + p], min(cfg.m_max, naug_glob), n_top, p, layout, comm)
         m_target = min(cfg.m_init, naug_glob)
-        while proc.m < m_target and proc.extend():
+        while proc.m < m_target and proc.extend(sync=False):
             pass
+        proc.settle()
         while True:
             Y, res_raw = proc.phi_coeffs(0, [delta])
             r = float(res_raw[0].item())

@@ -327,3 +327,48 @@ def test_config2_full_size_arnoldi_properties(P):
         lhs = op(V[:, j].contiguous())
         rhs = V[:, :j + 2] @ H[:j + 2, j]
         assert torch.linalg.norm(lhs - rhs).item() <= 1e-10 * torch.linalg.norm(lhs).item()
+
+
+def test_fused_arnoldi_breakdown_queued_iterations_are_inert(P):
+    """Uniform state + uniform direction: J v = 0, lucky breakdown at m = 1 (krylov.py:163-165).
+
+    The fused path queues iterations ahead of its breakdown test; they must leave
+    no trace (same m, H, RHS count as the oracle)."""
+    from oracle import jvp, krylov_cpu, stencil
+    g = P.Grid2D(16, 8, 0.0, 1.0, 0.0, 1.0)
+    prm = P.MhdParams(mu=1e-2, eta=1e-2, kappa=1e-2)
+    bc = P.BoundaryPolicy("periodic", "periodic")
+    U = np.zeros((8, 16, 8))
+    U[0] = 1.0
+    U[4] = 0.3
+    U[7] = 3.0
+    v = np.zeros_like(U)
+    v[0] = 1.0
+    f = P.make_rhs(prm, g, bc)
+    op = P.FdJacobianOperator(f, U.reshape(-1))
+    ev0 = f.ctx.status().rhs_evals
+    b = P.arnoldi(op, v.reshape(-1), 6)
+    ref = krylov_cpu.arnoldi(jvp.FdJv(stencil.rhs_closure(prm, g, bc), U.reshape(-1)), v.reshape(-1), 6)
+    assert b.breakdown and ref.broke and b.m == ref.m == 1
+    _, Href = ref.snapshot()
+    assert np.max(np.abs(b.H - Href)) <= 1e-14
+    assert f.ctx.status().rhs_evals - ev0 == 1
+
+
+def test_fused_arnoldi_raises_admissibility_like_reference(P):
+    from oracle import jvp, krylov_cpu, stencil
+    g = P.Grid2D(12, 10, 0.0, 1.0, 0.0, 1.0)
+    prm = P.MhdParams(mu=1e-3)
+    bc = P.BoundaryPolicy("periodic", "reflect")
+    rng = np.random.default_rng(9)
+    U = np.zeros((8, 12, 10))
+    U[0] = 1.0 + 0.1 * rng.random((12, 10))
+    U[7] = 1.5e-9 + 1e-10 * rng.random((12, 10))     # pressure ~ 1e-9: a sqrt(eps) step crosses 0
+    v = rng.standard_normal(U.size)
+    ref = jvp.FdJv(stencil.rhs_closure(prm, g, bc), U.reshape(-1))
+    with pytest.raises(stencil.InadmissibleState) as want:
+        krylov_cpu.arnoldi(ref, v, 4)
+    op = P.FdJacobianOperator(P.make_rhs(prm, g, bc), U.reshape(-1))
+    with pytest.raises(P.AdmissibilityError) as got:
+        P.arnoldi(op, v, 4)
+    assert str(got.value) == str(want.value)
