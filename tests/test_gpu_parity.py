@@ -371,4 +371,11 @@ def test_fused_arnoldi_raises_admissibility_like_reference(P):
     op = P.FdJacobianOperator(P.make_rhs(prm, g, bc), U.reshape(-1))
     with pytest.raises(P.AdmissibilityError) as got:
         P.arnoldi(op, v, 4)
-    assert str(got.value) == str(want.value)
+    # same kind and cell; the value may differ in its last bits (beta = ||v|| is a
+    # differently ordered sum on the device, SURVEY 7 hard part 1)
+    import re
+    pat = r"non-positive (\w+) at cell (\(\d+, \d+\)): (\S+)"
+    gk, gc, gv = re.match(pat, str(got.value)).groups()
+    wk, wc, wv = re.match(pat, str(want.value)).groups()
+    assert (gk, gc) == (wk, wc)
+    assert abs(float(gv) - float(wv)) <= 1e-6 * abs(float(wv))
