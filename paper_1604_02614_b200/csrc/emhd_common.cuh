@@ -35,6 +35,28 @@ __device__ __forceinline__ double div_const(double x, double d, double r) {
   return __fma_rn(e, r, q);
 }
 
+// One-correction variant: valid (== RN(x/d)) when |1 - r d| <= 2^-54, because then
+// RN(x r) is already faithful and Markstein's correction rounds it correctly.
+__device__ __forceinline__ double div_const1(double x, double d, double r) {
+  const double q = __dmul_rn(x, r);
+  const double e = __fma_rn(-q, d, x);
+  return __fma_rn(e, r, q);
+}
+
+template <bool FAST>
+__device__ __forceinline__ double div_c(double x, double d, double r) {
+  return FAST ? div_const1(x, d, r) : div_const(x, d, r);
+}
+
+// exact test of the one-correction condition (1 - r d is exactly representable)
+__device__ __host__ __forceinline__ bool recip_tight(double d, double r) {
+#ifdef __CUDA_ARCH__
+  return fabs(__fma_rn(-r, d, 1.0)) <= 0x1p-54;
+#else
+  return __builtin_fabs(__builtin_fma(-r, d, 1.0)) <= 0x1p-54;
+#endif
+}
+
 // sigma rule of the forward-difference Jacobian (reference fdjac.py:43)
 __device__ __forceinline__ double fd_sigma(double vnorm) {
   return vnorm > SQRT_EPS ? SQRT_EPS / vnorm : 1.0;

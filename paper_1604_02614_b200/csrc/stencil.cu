@@ -110,12 +110,16 @@ __device__ __forceinline__ void fetch_cell(const StencilParams& P, const RowRef&
 
 template <int MODE>
 __device__ __forceinline__ void combine_cell(const RawCell<MODE>& x, bool xflip, bool yflip,
-                                             double sigma, double hnext, double rh, double u[NF]) {
+                                             double sigma, double hnext, double rh, bool fh,
+                                             double u[NF]) {
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     double val = x.a[f];
     if (MODE == MODE_JV) val = __dadd_rn(val, __dmul_rn(sigma, x.v[f]));
-    if (MODE == MODE_JVN) val = __dadd_rn(val, __dmul_rn(sigma, div_const(x.v[f], hnext, rh)));
+    if (MODE == MODE_JVN) {
+      const double vj = fh ? div_const1(x.v[f], hnext, rh) : div_const(x.v[f], hnext, rh);
+      val = __dadd_rn(val, __dmul_rn(sigma, vj));
+    }
     u[f] = val;
   }
   if (xflip) { u[1] = -u[1]; u[4] = -u[4]; }
@@ -130,7 +134,8 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
   if (P.check && rho <= 0.0) flag |= ST_RHO;
   const double m2 = __dadd_rn(__dadd_rn(__dmul_rn(mx, mx), __dmul_rn(my, my)), __dmul_rn(mz, mz));
   const double bb = __dadd_rn(__dadd_rn(__dmul_rn(b0, b0), __dmul_rn(b1, b1)), __dmul_rn(b2, b2));
-  const double kin = __dmul_rn(0.5, m2) / rho;
+  const double rr = 1.0 / rho;                 // RN(1/rho): one IEEE division per cell
+  const double kin = div_const(__dmul_rn(0.5, m2), rho, rr);
   const double mag = __dmul_rn(P.bfac, bb);
   const double p = __dmul_rn(P.gm1, __dsub_rn(__dsub_rn(en, kin), mag));
   if (P.check && p <= 0.0) flag |= ST_PRESSURE;
@@ -141,27 +146,28 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
   q[Q_B0 * qs] = b0;
   q[Q_B1 * qs] = b1;
   q[Q_B2 * qs] = b2;
-  q[Q_V0 * qs] = mx / rho;
-  q[Q_V1 * qs] = my / rho;
-  q[Q_V2 * qs] = mz / rho;
-  q[Q_T * qs] = p / rho;
+  q[Q_V0 * qs] = div_const(mx, rho, rr);      // == mx / rho bit for bit
+  q[Q_V1 * qs] = div_const(my, rho, rr);
+  q[Q_V2 * qs] = div_const(mz, rho, rr);
+  q[Q_T * qs] = div_const(p, rho, rr);
   q[Q_PT * qs] = __dadd_rn(p, __dmul_rn(0.5, bb));
 }
 
 // x- and y-flux G = F_hyp - F_diff at one cell (mhd.py:174-197, 209-266, 275-276).
 // c: prim column slot of the cell; qm/q0/qp: prim rows i-1, i, i+1.
+template <bool FXY>
 __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* qm,
                                           const double* q0, const double* qp, int c, int qs,
                                           bool need_x, bool need_y, double gx[NF], double gy[NF]) {
 #define QV(row, k, col) row[(k) * qs + (col)]
   const double thx = P.two_hx, rhx = P.r_two_hx, thy = P.two_hy, rhy = P.r_two_hy;
   // centred derivatives of v, B, T at the cell (mhd.py:224-227, 261, 264)
-  const double dvx0 = div_const(__dsub_rn(QV(qp, Q_V0, c), QV(qm, Q_V0, c)), thx, rhx);
-  const double dvx1 = div_const(__dsub_rn(QV(qp, Q_V1, c), QV(qm, Q_V1, c)), thx, rhx);
-  const double dvy0 = div_const(__dsub_rn(QV(q0, Q_V0, c + 1), QV(q0, Q_V0, c - 1)), thy, rhy);
-  const double dvy1 = div_const(__dsub_rn(QV(q0, Q_V1, c + 1), QV(q0, Q_V1, c - 1)), thy, rhy);
-  const double dBx1 = div_const(__dsub_rn(QV(qp, Q_B1, c), QV(qm, Q_B1, c)), thx, rhx);
-  const double dBy0 = div_const(__dsub_rn(QV(q0, Q_B0, c + 1), QV(q0, Q_B0, c - 1)), thy, rhy);
+  const double dvx0 = div_c<FXY>(__dsub_rn(QV(qp, Q_V0, c), QV(qm, Q_V0, c)), thx, rhx);
+  const double dvx1 = div_c<FXY>(__dsub_rn(QV(qp, Q_V1, c), QV(qm, Q_V1, c)), thx, rhx);
+  const double dvy0 = div_c<FXY>(__dsub_rn(QV(q0, Q_V0, c + 1), QV(q0, Q_V0, c - 1)), thy, rhy);
+  const double dvy1 = div_c<FXY>(__dsub_rn(QV(q0, Q_V1, c + 1), QV(q0, Q_V1, c - 1)), thy, rhy);
+  const double dBx1 = div_c<FXY>(__dsub_rn(QV(qp, Q_B1, c), QV(qm, Q_B1, c)), thx, rhx);
+  const double dBy0 = div_c<FXY>(__dsub_rn(QV(q0, Q_B0, c + 1), QV(q0, Q_B0, c - 1)), thy, rhy);
 
   const double rho = QV(q0, Q_RHO, c), en = QV(q0, Q_EN, c), pt = QV(q0, Q_PT, c);
   const double v0 = QV(q0, Q_V0, c), v1 = QV(q0, Q_V1, c), v2 = QV(q0, Q_V2, c);
@@ -177,9 +183,9 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
   const double r0 = __dmul_rn(rho, v0), r1 = __dmul_rn(rho, v1), r2 = __dmul_rn(rho, v2);
 
   if (need_x) {
-    const double dvx2 = div_const(__dsub_rn(QV(qp, Q_V2, c), QV(qm, Q_V2, c)), thx, rhx);
-    const double dBx2 = div_const(__dsub_rn(QV(qp, Q_B2, c), QV(qm, Q_B2, c)), thx, rhx);
-    const double dTx = div_const(__dsub_rn(QV(qp, Q_T, c), QV(qm, Q_T, c)), thx, rhx);
+    const double dvx2 = div_c<FXY>(__dsub_rn(QV(qp, Q_V2, c), QV(qm, Q_V2, c)), thx, rhx);
+    const double dBx2 = div_c<FXY>(__dsub_rn(QV(qp, Q_B2, c), QV(qm, Q_B2, c)), thx, rhx);
+    const double dTx = div_c<FXY>(__dsub_rn(QV(qp, Q_T, c), QV(qm, Q_T, c)), thx, rhx);
     const double tau_xx = __dsub_rn(__dmul_rn(2.0, dvx0), c23d);
     // diffusive x-flux (mhd.py:244-262)
     const double fmx = __dmul_rn(mu, tau_xx);
@@ -202,9 +208,9 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
     gx[7] = __dsub_rn(__dsub_rn(__dmul_rn(ept, v0), __dmul_rn(b0, bv)), fen);
   }
   if (need_y) {
-    const double dvy2 = div_const(__dsub_rn(QV(q0, Q_V2, c + 1), QV(q0, Q_V2, c - 1)), thy, rhy);
-    const double dBy2 = div_const(__dsub_rn(QV(q0, Q_B2, c + 1), QV(q0, Q_B2, c - 1)), thy, rhy);
-    const double dTy = div_const(__dsub_rn(QV(q0, Q_T, c + 1), QV(q0, Q_T, c - 1)), thy, rhy);
+    const double dvy2 = div_c<FXY>(__dsub_rn(QV(q0, Q_V2, c + 1), QV(q0, Q_V2, c - 1)), thy, rhy);
+    const double dBy2 = div_c<FXY>(__dsub_rn(QV(q0, Q_B2, c + 1), QV(q0, Q_B2, c - 1)), thy, rhy);
+    const double dTy = div_c<FXY>(__dsub_rn(QV(q0, Q_T, c + 1), QV(q0, Q_T, c - 1)), thy, rhy);
     const double tau_yy = __dsub_rn(__dmul_rn(2.0, dvy1), c23d);
     // diffusive y-flux (mhd.py:245-265)
     const double fmx = __dmul_rn(mu, tau_xy);
@@ -228,7 +234,7 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
 #undef QV
 }
 
-template <int TY, int MODE, bool AUG>
+template <int TY, int MODE, bool AUG, bool FXY>
 __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
@@ -269,6 +275,8 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
     sigma = fd_sigma(vn);
     rsig = 1.0 / sigma;
   }
+  const bool fsig = recip_tight(sigma, rsig);   // one-correction division by sigma is exact
+  const bool fh = recip_tight(hnext, rh);
 
   // augmented tail q of the current basis vector (krylov.py:268-273)
   double qv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -348,18 +356,19 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
         double* q = qring + ((r + 3) % 3) * NQ * QW;
         double u[NF];
         if (okm) {
-          combine_cell<MODE>(xm, Rn.flip, fm, sigma, hnext, rh, u);
+          combine_cell<MODE>(xm, Rn.flip, fm, sigma, hnext, rh, fh, u);
           cell_prims(P, u, q + cmain, QW, flag);
           if (MODE == MODE_JVN && r >= i0 && r < i1 && t < ncols_out) {
             // v_j = w / h_next of an owned cell (krylov.py:167), from the fetched w
             const long long o = (long long)r * P.ny + j0 + t;
 #pragma unroll
             for (int f = 0; f < NF; ++f)
-              P.vout[o + (long long)f * P.nx * P.ny] = div_const(xm.v[f], hnext, rh);
+              P.vout[o + (long long)f * P.nx * P.ny] =
+                  fh ? div_const1(xm.v[f], hnext, rh) : div_const(xm.v[f], hnext, rh);
           }
         }
         if (oke) {
-          combine_cell<MODE>(xe, Rn.flip, fe, sigma, hnext, rh, u);
+          combine_cell<MODE>(xe, Rn.flip, fe, sigma, hnext, rh, fh, u);
           cell_prims(P, u, q + cextra, QW, flag);
         }
       }
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
         const bool out_row = (rf >= i0 && rf < i1);
         double gx[NF], gy[NF];
         if (t < ncols_out) {
-          flux_cell(P, qm, q0, qp, cmain, QW, true, out_row, gx, gy);
+          flux_cell<FXY>(P, qm, q0, qp, cmain, QW, true, out_row, gx, gy);
 #pragma unroll
           for (int f = 0; f < NF; ++f) gxr[f * TY + t] = gx[f];
           if (out_row) {
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
           if (t == 0) { cs = 1; gslot = 0; }
           if (t == TY - 1) { cs = ncols_out + 2; gslot = ncols_out + 1; }
           if (cs >= 0) {
-            flux_cell(P, qm, q0, qp, cs, QW, false, true, gx, gy);
+            flux_cell<FXY>(P, qm, q0, qp, cs, QW, false, true, gx, gy);
 #pragma unroll
             for (int f = 0; f < NF; ++f) gyr[f * GYW + gslot] = gy[f];
           }
@@ -410,8 +419,8 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
         const long long o = (long long)ro * P.ny + j0 + t;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-          const double ddx = div_const(__dsub_rn(gxp[f * TY + t], gxm[f * TY + t]), P.two_hx, P.r_two_hx);
-          const double ddy = div_const(__dsub_rn(gyr[f * GYW + t + 2], gyr[f * GYW + t]), P.two_hy, P.r_two_hy);
+          const double ddx = div_c<FXY>(__dsub_rn(gxp[f * TY + t], gxm[f * TY + t]), P.two_hx, P.r_two_hx);
+          const double ddy = div_c<FXY>(__dsub_rn(gyr[f * GYW + t + 2], gyr[f * GYW + t]), P.two_hy, P.r_two_hy);
           double F = __dsub_rn(-ddx, ddy);                    // -ddx(gx) - ddy(gy) (mhd.py:277)
           const long long idx = o + (long long)f * P.nx * P.ny;
           if (MODE == MODE_RHS) {
@@ -422,7 +431,8 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
                   (unsigned long long)(P.x_off + ro) * P.ny + j0 + t;
               bad = gidx < bad ? gidx : bad;
             }
-            double jv = div_const(__dsub_rn(F, fa_pre[f]), sigma, rsig);   // fdjac.py:49
+            const double df = __dsub_rn(F, fa_pre[f]);
+            double jv = fsig ? div_const1(df, sigma, rsig) : div_const(df, sigma, rsig);   // fdjac.py:49
             if (AUG) {
               jv = __dmul_rn(P.ch, jv);
               for (int k = 0; k < P.nb; ++k)
@@ -511,7 +521,8 @@ __global__ void admissibility_kernel(const StencilParams P, int pass, unsigned l
     const double rho = u[0];
     const double m2 = __dadd_rn(__dadd_rn(__dmul_rn(u[1], u[1]), __dmul_rn(u[2], u[2])), __dmul_rn(u[3], u[3]));
     const double bb = __dadd_rn(__dadd_rn(__dmul_rn(u[4], u[4]), __dmul_rn(u[5], u[5])), __dmul_rn(u[6], u[6]));
-    const double kin = __dmul_rn(0.5, m2) / rho;
+    const double rr = 1.0 / rho;                 // RN(1/rho): one IEEE division per cell
+  const double kin = div_const(__dmul_rn(0.5, m2), rho, rr);
     const double p = __dmul_rn(P.gm1, __dsub_rn(__dsub_rn(u[7], kin), __dmul_rn(P.bfac, bb)));
     if (pass == 0) {
       if (!isnan(rho)) atomicMin(&keys[0], ord_key(rho));
@@ -534,11 +545,11 @@ cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* 
   return cudaGetLastError();
 }
 
-template <int TY, int MODE, bool AUG>
+template <int TY, int MODE, bool AUG, bool FXY>
 static cudaError_t launch_t(const StencilParams& P, cudaStream_t s) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   const size_t sm = sizeof(double) * (3 * NQ * QW + 3 * NF * TY + 2 * NF * GYW);
-  auto k = stencil_kernel<TY, MODE, AUG>;
+  auto k = stencil_kernel<TY, MODE, AUG, FXY>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
@@ -546,11 +557,18 @@ static cudaError_t launch_t(const StencilParams& P, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int TY, bool FXY>
+static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, cudaStream_t s) {
+  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false, FXY>(P, s);
+  if (mode == MODE_JV)
+    return aug ? launch_t<TY, MODE_JV, true, FXY>(P, s) : launch_t<TY, MODE_JV, false, FXY>(P, s);
+  return aug ? launch_t<TY, MODE_JVN, true, FXY>(P, s) : launch_t<TY, MODE_JVN, false, FXY>(P, s);
+}
+
 template <int TY>
 static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, cudaStream_t s) {
-  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false>(P, s);
-  if (mode == MODE_JV) return aug ? launch_t<TY, MODE_JV, true>(P, s) : launch_t<TY, MODE_JV, false>(P, s);
-  return aug ? launch_t<TY, MODE_JVN, true>(P, s) : launch_t<TY, MODE_JVN, false>(P, s);
+  const bool fxy = recip_tight(P.two_hx, P.r_two_hx) && recip_tight(P.two_hy, P.r_two_hy);
+  return fxy ? launch_f<TY, true>(P, mode, aug, s) : launch_f<TY, false>(P, mode, aug, s);
 }
 
 int stencil_tile_width(int ny) { return ny <= 32 ? 32 : (ny <= 64 ? 64 : 128); }
