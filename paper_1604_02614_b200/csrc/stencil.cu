@@ -16,6 +16,7 @@
 // identical bits), the derivatives of a flux cell are shared by its x- and
 // y-flux, and halo recomputation only happens at strip edges (4 columns) and
 // chunk edges (4 rows).
+#include <cstdlib>
 #include "emhd_common.cuh"
 #include "stencil.cuh"
 
@@ -546,46 +547,56 @@ cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* 
 }
 
 template <int TY, int MODE, bool AUG, bool FXY>
-static cudaError_t launch_t(const StencilParams& P, cudaStream_t s) {
+static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   const size_t sm = sizeof(double) * (3 * NQ * QW + 3 * NF * TY + 2 * NF * GYW);
   auto k = stencil_kernel<TY, MODE, AUG, FXY>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
+  if (P.rows_per_cta <= 0) {
+    // exactly one wave of resident CTAs (all CTAs carry equal work); >= 8 rows per CTA
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, TY, sm);
+    const int strips = (P.ny + TY - 1) / TY;
+    const int target = (occ < 1 ? 1 : occ) * num_sms;
+    const int chunks = (target + strips - 1) / strips;
+    const int rows = (P.nx + chunks - 1) / chunks;
+    P.rows_per_cta = rows < 8 ? 8 : rows;
+  }
   dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
   k<<<grid, TY, sm, s>>>(P);
   return cudaGetLastError();
 }
 
 template <int TY, bool FXY>
-static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, cudaStream_t s) {
-  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false, FXY>(P, s);
+static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s) {
+  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false, FXY>(P, ns, s);
   if (mode == MODE_JV)
-    return aug ? launch_t<TY, MODE_JV, true, FXY>(P, s) : launch_t<TY, MODE_JV, false, FXY>(P, s);
-  return aug ? launch_t<TY, MODE_JVN, true, FXY>(P, s) : launch_t<TY, MODE_JVN, false, FXY>(P, s);
+    return aug ? launch_t<TY, MODE_JV, true, FXY>(P, ns, s) : launch_t<TY, MODE_JV, false, FXY>(P, ns, s);
+  return aug ? launch_t<TY, MODE_JVN, true, FXY>(P, ns, s) : launch_t<TY, MODE_JVN, false, FXY>(P, ns, s);
 }
 
 template <int TY>
-static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, cudaStream_t s) {
+static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s) {
   const bool fxy = recip_tight(P.two_hx, P.r_two_hx) && recip_tight(P.two_hy, P.r_two_hy);
-  return fxy ? launch_f<TY, true>(P, mode, aug, s) : launch_f<TY, false>(P, mode, aug, s);
+  return fxy ? launch_f<TY, true>(P, mode, aug, ns, s) : launch_f<TY, false>(P, mode, aug, ns, s);
 }
 
-int stencil_tile_width(int ny) { return ny <= 32 ? 32 : (ny <= 64 ? 64 : 128); }
+int stencil_tile_width(int ny) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* env = getenv("EMHD_STENCIL_TY");
+    forced = env ? atoi(env) : 0;
+  }
+  if (forced == 32 || forced == 64 || forced == 128) return forced;
+  return ny <= 32 ? 32 : (ny <= 64 ? 64 : 128);
+}
 
 cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s) {
   const int ty = stencil_tile_width(P.ny);
-  const int strips = (P.ny + ty - 1) / ty;
-  if (P.rows_per_cta <= 0) {
-    // one full wave of ~2 resident CTAs per SM; never fewer than 8 rows per CTA
-    const int target = 2 * num_sms;
-    const int chunks = (target + strips - 1) / strips;
-    int rows = (P.nx + chunks - 1) / chunks;
-    P.rows_per_cta = rows < 8 ? 8 : rows;
-  }
-  if (ty == 32) return launch_ty<32>(P, mode, aug, s);
-  if (ty == 64) return launch_ty<64>(P, mode, aug, s);
-  return launch_ty<128>(P, mode, aug, s);
+  if (ty == 32) return launch_ty<32>(P, mode, aug, num_sms, s);
+  if (ty == 64) return launch_ty<64>(P, mode, aug, num_sms, s);
+  return launch_ty<128>(P, mode, aug, num_sms, s);
 }
 
 }  // namespace emhd

@@ -146,7 +146,7 @@ class FdJacobianOperator(LinearOperator):
         scal = self._scr.dev[0:2]
         self.vnorm_into(vd, scal)
         out = self.apply_device(vd, vnorm_dev=scal, v_halo=vh)
-        raise_status(self.ctx, self.ctx.status(),
+        raise_status(self.ctx, self.ctx.status(), comm=self.gpu.comm, report_args=
                      (1, D.ptr(self.a), D.ptr(self.a_halo), D.ptr(vd), D.ptr(vh), D.ptr(scal)))
         return D.to_host(out) if host else out
 

@@ -321,6 +321,9 @@ class _Process:
             self.breakdown = True
         self._settled = self.m
         if st is not None:
+            if self.comm is not None and self.layout.distributed:
+                from .mhd import agree_status
+                st = agree_status(st, self.comm)
             self.check_status(st)
         return not self.breakdown
 
@@ -338,7 +341,8 @@ class _Process:
             if self.layout is not None and self.layout.distributed:
                 self.comm.allreduce_max(sc[1:2])
             sc[0:1].copy_(sc[1:2])
-            raise_status(self.ctx, st, (1, D.ptr(a), D.ptr(ah), D.ptr(v), D.ptr(vh), D.ptr(sc)))
+            raise_status(self.ctx, st, (1, D.ptr(a), D.ptr(ah), D.ptr(v), D.ptr(vh), D.ptr(sc)),
+                         self.comm)
 
     # -- views ------------------------------------------------------------------
     @property

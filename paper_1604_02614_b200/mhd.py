@@ -111,19 +111,49 @@ def energy_from(rho, v, B, p, params):
     return p / (params.gamma - 1.0) + kin + mag
 
 
-def raise_status(ctx, st, report_args=None):
+def agree_status(st, comm):
+    """Combine the status words of all slab ranks (OR of flags, min of indices).
+
+    Every rank must take the same exception path, or the next collective hangs.
+    """
+    if comm is None or not comm.layout.distributed:
+        return st
+    err = st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE | N.ST_DENSE)
+    t = torch.tensor([float(err & N.ST_RHO), float(err & N.ST_PRESSURE), float(err & N.ST_NONFINITE),
+                      float(err & N.ST_DENSE)], dtype=D.F64, device=D.device())
+    comm.allreduce_max(t)
+    mn = torch.tensor([float(st.first_nonfinite if st.first_nonfinite < 2 ** 62 else 2 ** 62),
+                       float(st.fail_iter)], dtype=D.F64, device=D.device())
+    comm.allreduce_min(mn)
+    out = N.Status()
+    bits = t.cpu().numpy()
+    out.flags = (st.flags & ~(N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE | N.ST_DENSE)) | \
+        sum(int(b) for b in bits)
+    mnv = mn.cpu().numpy()
+    out.rhs_evals = st.rhs_evals
+    out.first_nonfinite = int(mnv[0])
+    out.breakdown = st.breakdown
+    out.fail_iter = int(mnv[1])
+    out.local_flags = st.flags
+    return out
+
+
+def raise_status(ctx, st, report_args=None, comm=None):
     """Map the device status word to the reference's exception types.
 
     Priority follows the reference: density (mhd.py:123-125), then pressure
-    (:128-130), then a non-finite perturbed RHS (fdjac.py:45-48).
+    (:128-130), then a non-finite perturbed RHS (fdjac.py:45-48).  With a slab
+    communicator the decision is taken on the combined status of all ranks.
     """
+    st = agree_status(st, comm)
     flags = st.flags
+    local = getattr(st, "local_flags", flags)
     if not flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE):
         return
     ctx.reset_status()
     if flags & (N.ST_RHO | N.ST_PRESSURE):
         msg = None
-        if report_args is not None:
+        if report_args is not None and local & (N.ST_RHO | N.ST_PRESSURE):
             rep = N.Report()
             mode, a, ah, v, vh, sc = report_args
             N.check(ctx.lib.emhd_admissibility_report(ctx.sync_stream(), mode, a, ah, v, vh, sc,
@@ -183,7 +213,7 @@ class GpuRhs:
         return out
 
     def check_status(self, report_args=None):
-        raise_status(self.ctx, self.ctx.status(), report_args)
+        raise_status(self.ctx, self.ctx.status(), report_args, self.comm)
 
     def __call__(self, y):
         host = D.is_host(y)

@@ -1,0 +1,123 @@
+"""Multi-rank slab path on ONE GPU: 2 and 3 processes share cuda:0, exchange halos and reduce
+through gloo (CPU staging).  No kernel ever waits on another rank (the exchange is host-side),
+so this is safe on one device; it exercises the full distributed GPU code path — halo packing,
+EXTERNAL-boundary stencils, all-reduced Arnoldi sums, cross-rank status agreement — against the
+reference fixtures."""
+
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from conftest import GOLDEN, ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, size, port):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    torch.cuda.set_device(0)
+    try:
+        import paper_1604_02614_b200 as P
+        from paper_1604_02614_b200.mhd import local_rows
+        from paper_1604_02614_b200.slab import Comm, make_layout
+        from conftest import case_objects, golden
+
+        class StagingComm(Comm):
+            def exchange(self, sendbuf, recvbuf):
+                s = sendbuf.cpu()
+                r = torch.zeros_like(s)
+                super().exchange(s, r)
+                recvbuf.copy_(r)
+                return recvbuf
+
+            def _red(self, t, fn):
+                c = t.cpu()
+                fn(c)
+                t.copy_(c)
+                return t
+
+            def allreduce_sum(self, t):
+                return self._red(t, super().allreduce_sum)
+
+            def allreduce_max(self, t):
+                return self._red(t, super().allreduce_max)
+
+            def allreduce_min(self, t):
+                return self._red(t, super().allreduce_min)
+
+        # (a)+(b): RHS and Jv bit-identical to the single-domain reference
+        z = golden("rhs_jv_cases.npz")
+        for k in (0, 3, 4):
+            g, prm, bc = case_objects(z, k)
+            L = make_layout(g.nx, g.ny, bc.x, rank, size)
+            f = P.make_rhs(prm, g, bc, layout=L, comm=StagingComm(L))
+            a = local_rows(z[f"c{k}_U"].reshape(-1), g, L)
+            assert np.array_equal(f(a), local_rows(z[f"c{k}_F"].reshape(-1), g, L)), (k, "rhs")
+            op = P.FdJacobianOperator(f, a)
+            Jv = op(local_rows(z[f"c{k}_v"], g, L))
+            assert np.array_equal(Jv, local_rows(z[f"c{k}_Jv"], g, L)), (k, "jv")
+
+        # (c): FD Arnoldi across slabs
+        zk = golden("krylov_mhd.npz")
+        gt, pt = zk["grid"], zk["params"]
+        g = P.Grid2D(int(gt[0]), int(gt[1]), gt[2], gt[3], gt[4], gt[5])
+        prm = P.MhdParams(mu=pt[0], eta=pt[1], kappa=pt[2], gamma=pt[3], b_half=bool(pt[4]))
+        bc = P.BoundaryPolicy("periodic", "reflect")
+        L = make_layout(g.nx, g.ny, bc.x, rank, size)
+        f = P.make_rhs(prm, g, bc, layout=L, comm=StagingComm(L))
+        op = P.FdJacobianOperator(f, local_rows(zk["a"], g, L), local_rows(zk["fa"], g, L))
+        b = P.arnoldi(op, local_rows(zk["v"], g, L), 12)
+        assert b.m == 12
+        assert np.linalg.norm(b.H - zk["H"]) <= 1e-8 * np.linalg.norm(zk["H"])
+        outs, st = P.multi_scale_eval(op, 0.5, local_rows(0.5 * zk["fa"], g, L),
+                                      [0.5, 2.0 / 3.0, 1.0], 1e-10)
+        assert [st.operator_applies, st.substeps, st.max_basis_size] == list(zk["ms_stats"])
+        n = zk["a"].size
+        w, st = P.phi_comb(P.PhiCombRequest(
+            operator=op, h=0.5, c=1.0,
+            vectors=[np.zeros(L.n_local), np.zeros(L.n_local), local_rows(zk["vec3"], g, L),
+                     local_rows(0.5 * zk["vec3"], g, L)], tol=1e-10))
+        assert [st.operator_applies, st.substeps, st.max_basis_size] == list(zk["pc_stats"])
+        want = local_rows(zk["pc_w"], g, L)
+        assert np.linalg.norm(w - want) <= 1e-8 * np.linalg.norm(zk["pc_w"])
+
+        # (d): one EpiRK4 step of config 0 (64^2) across slabs, identical counters
+        z0 = golden("config0_recon64.npz")
+        with open(os.path.join(GOLDEN, "config0_stats.json")) as fh:
+            s1 = json.load(fh)["step1"]
+        g = P.ReconnectionSpec().grid(64, 64)
+        prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+        bc = P.default_bc("reconnection")
+        L = make_layout(g.nx, g.ny, bc.x, rank, size)
+        f = P.make_rhs(prm, g, bc, layout=L, comm=StagingComm(L))
+        y1, S = P.epirk4_step(f, local_rows(z0["U0"].reshape(-1), g, L), 0.1, 1e-10)
+        want = local_rows(z0["y1"], g, L)
+        assert np.linalg.norm(y1 - want) <= 1e-8 * np.linalg.norm(z0["y1"]) / np.sqrt(size)
+        for key, v in s1.items():
+            assert getattr(S, key) == v, key
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size", [2, 3])
+def test_slab_ranks_on_one_gpu_match_reference(size):
+    mp.spawn(_worker, args=(size, _port()), nprocs=size, join=True)

@@ -1,0 +1,128 @@
+#!/usr/bin/env python
+"""Trajectory workloads of BASELINE configs 0, 1, 3, 4 on the GPU path (secondary to bench.py).
+
+    python tools/run_configs.py --config 0        # reconnection 64^2, EpiRK4 dt=0.1 x 20
+    python tools/run_configs.py --config 1        # KH shear 256^2, EpiRK5P1 tol 1e-6 to t=2
+    python tools/run_configs.py --config 3 --n 512 --steps 5     # config 3 physics, smaller grid
+    python tools/run_configs.py --config 4 --n 1024 --steps 2 --dt 0.05 --eta 1e-4 --pr 1
+
+Prints one JSON line per run: wall time, StepStats, Jv+Arnoldi iterations/s, C*steps/s and
+(--check) the relative L2 distance to the oracle run on the same inputs.
+"""
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def stats_dict(st):
+    keys = ["steps_accepted", "steps_rejected", "projections", "rhs_evals", "operator_applies",
+            "substeps", "max_basis_size"]
+    return {k: getattr(st, k) for k in keys}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=0)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--t-end", type=float, default=None)
+    ap.add_argument("--dt", type=float, default=None)
+    ap.add_argument("--eta", type=float, default=None)
+    ap.add_argument("--pr", type=float, default=1.0)
+    ap.add_argument("--m-max", type=int, default=100)
+    ap.add_argument("--check", action="store_true", help="also run the CPU oracle and compare")
+    a = ap.parse_args()
+    import torch
+    import paper_1604_02614_b200 as P
+    from paper_1604_02614_b200.problems import kh_shear_grid, kh_shear_ic
+
+    cfg = P.KrylovConfig(m_max=a.m_max)
+    if a.config == 0:
+        n = a.n or 64
+        g = P.ReconnectionSpec().grid(n, n)
+        prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+        bc = P.default_bc("reconnection")
+        y0 = P.reconnection_ic(g, params=prm).reshape(-1)
+        run = dict(kind="fixed", method="epirk4", t_end=a.t_end or 2.0, dt=a.dt or 0.1, tol=1e-10)
+    elif a.config == 1:
+        n = a.n or 256
+        g = kh_shear_grid(n)
+        prm = P.MhdParams(mu=1e-4, eta=1e-4, kappa=1e-4)
+        bc = P.BoundaryPolicy("periodic", "reflect")
+        y0 = kh_shear_ic(g, prm).reshape(-1)
+        run = dict(kind="adaptive", t_end=a.t_end or 2.0, tol=1e-6)
+    elif a.config == 3:
+        n = a.n or 2048
+        g = P.ReconnectionSpec().grid(n, n)
+        prm = P.MhdParams(mu=1e-4, eta=1e-4, kappa=1e-3)
+        bc = P.default_bc("reconnection")
+        y0 = P.reconnection_ic(g, params=prm).reshape(-1)
+        run = dict(kind="adaptive", t_end=a.t_end or 1e9, tol=1e-6, max_steps=a.steps or 50)
+    elif a.config == 4:
+        n = a.n or 4096
+        eta = a.eta or 1e-4
+        g = P.ReconnectionSpec().grid(n, n)
+        prm = P.MhdParams(mu=a.pr * eta, eta=eta, kappa=1e-3)
+        bc = P.default_bc("reconnection")
+        y0 = P.reconnection_ic(g, params=prm).reshape(-1)
+        steps = a.steps or 10
+        dt = a.dt or 0.05
+        run = dict(kind="fixed", method="epirk4", t_end=dt * steps, dt=dt, tol=1e-10)
+        cfg = P.KrylovConfig(m_max=max(a.m_max, 128))
+    else:
+        raise SystemExit("config must be 0, 1, 3 or 4")
+
+    f = P.make_rhs(prm, g, bc)
+    yd = torch.from_numpy(y0).cuda()
+
+    def go(rhs, y):
+        if run["kind"] == "fixed":
+            return P.integrate_fixed(run["method"], rhs, y, 0.0, run["t_end"], run["dt"],
+                                     tol_krylov=run["tol"], cfg=cfg, max_steps=a.steps)
+        return P.integrate_adaptive(rhs, y, 0.0, run["t_end"], P.StepController(tol=run["tol"]),
+                                    cfg=cfg, recoverable=(P.AdmissibilityError,),
+                                    max_steps=run.get("max_steps"))
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    y, st = go(f, yd)
+    torch.cuda.synchronize()
+    T = time.perf_counter() - t0
+    out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
+           "iterations_per_s": st.operator_applies / T,
+           "cell_steps_per_s": g.nx * g.ny * st.steps_accepted / T}
+    if a.check:
+        from oracle import epirk_cpu, stencil
+        from oracle.krylov_cpu import Knobs
+        fo = stencil.rhs_closure(prm, g, bc)
+        kn = Knobs(m_max=cfg.m_max)
+        t0 = time.perf_counter()
+        if run["kind"] == "fixed":
+            yo, so = epirk_cpu.run_fixed(run["method"], fo, y0, 0.0, run["t_end"], run["dt"],
+                                         tol=run["tol"], knobs=kn, max_steps=a.steps)
+        else:
+            yo, so = epirk_cpu.run_adaptive(fo, y0, 0.0, run["t_end"],
+                                            epirk_cpu.Controller(tol=run["tol"]), knobs=kn,
+                                            recoverable=(stencil.InadmissibleState,),
+                                            max_steps=run.get("max_steps"))
+        Tc = time.perf_counter() - t0
+        yh = y.cpu().numpy()
+        out["oracle_seconds"] = Tc
+        out["oracle_stats"] = {k: getattr(so, k) for k in out["stats"]}
+        out["rel_l2_vs_oracle"] = float(np.linalg.norm(yh - yo) / np.linalg.norm(yo))
+        out["counters_identical"] = out["oracle_stats"] == out["stats"]
+        out["speedup_vs_oracle"] = Tc / T
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
