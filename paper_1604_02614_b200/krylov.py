@@ -164,19 +164,26 @@ class _Process:
         if self.m_cap + 1 > self.ctx.max_vectors - 4:
             raise ValueError(f"basis cap {self.m_cap} exceeds the context limit")
         self.ld = _ld(self.naug)
-        self.V = torch.zeros((self.m_cap + 1, self.ld), dtype=D.F64, device=D.device())
-        self.H = torch.zeros((self.m_cap + 1, max(self.m_cap, 1)), dtype=D.F64, device=D.device())
-        self.w = [torch.zeros(self.ld, dtype=D.F64, device=D.device()) for _ in range(2)]
+        # V and w are never read beyond their written lengths: no zero-fill of 2.7 GB
+        self.V = torch.empty((self.m_cap + 1, self.ld), dtype=D.F64, device=D.device())
+        self.w = [torch.empty(self.ld, dtype=D.F64, device=D.device()) for _ in range(2)]
         k = self.m_cap + 4
-        self.d1 = D.zeros(k)
-        self.d2 = D.zeros(k)
-        self.nrm = D.zeros(2)
+        hw = max(self.m_cap, 1)
+        # one zero-filled block for H and every small scalar area (a single fill launch)
+        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + (self.m_cap + 1) + 4,
+                                  dtype=D.F64, device=D.device())
+        o = (self.m_cap + 1) * hw
+        self.H = self._small[:o].view(self.m_cap + 1, hw)
+        self.d1 = self._small[o:o + k]
+        self.d2 = self._small[o + k:o + 2 * k]
+        self.nrm = self._small[o + 2 * k:o + 2 * k + 2]
+        o2 = o + 2 * k + 2
+        self.brk = self._small[o2:o2 + self.m_cap + 1]
+        self.nb = self._small[o2 + self.m_cap + 1:o2 + self.m_cap + 5]   # {sum seed^2, max|seed|, beta, -}
         self.scal = D.Scratch(4)
-        self.brk = D.zeros(self.m_cap + 1)
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
         self._settled = 0
         self._pending = False
-        self.nb = D.zeros(4)                 # {sum seed^2, max|seed|, beta, -}
         self.beta_dev = self.nb[2:3]
         self.m = 0
         self.breakdown = False
