@@ -148,7 +148,7 @@ LAUNCHERS = {
     "emhd_rhs": None, "emhd_jv": None, "emhd_jv_aug": None, "emhd_jv_normalized": None,
     "emhd_multidot": None, "emhd_update": None, "emhd_norms": None, "emhd_arnoldi_finish": None,
     "emhd_div_scalar": None, "emhd_phi_small": None, "emhd_combine": None, "emhd_lincomb": None,
-    "emhd_wrms": None, "emhd_pack_edges": None,
+    "emhd_wrms": None, "emhd_pack_edges": None, "emhd_update_finish": None,
 }
 
 
@@ -163,7 +163,7 @@ def alg_bytes(name, args, n_local):
     if name == "emhd_multidot":
         nvec, len_dot = args[4], args[5]
         return 8.0 * (nvec + 1) * len_dot
-    if name == "emhd_update":
+    if name in ("emhd_update", "emhd_update_finish"):
         nvec, len_upd = args[4], args[6]
         return 8.0 * (nvec + 2) * len_upd
     if name == "emhd_norms":

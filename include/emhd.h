@@ -123,6 +123,12 @@ int emhd_multidot(emhd_ctx* ctx, const double* w, const double* V, long long ldv
  * mode 1: out = {sum w^2 over len_dot, max|w| over len_max} */
 int emhd_update(emhd_ctx* ctx, double* w, const double* V, long long ldv, int nvec, const double* h,
                 long long len_upd, long long len_dot, long long len_max, int mode, double* out);
+/* emhd_update(mode 1) + emhd_arnoldi_finish in one launch (single rank: the norms need no
+ * all-reduce before the column bookkeeping). */
+int emhd_update_finish(emhd_ctx* ctx, double* w, const double* V, long long ldv, int nvec,
+                       const double* h2, long long len_upd, long long len_dot, long long len_max,
+                       double* nrm, const double* h1, const double* selfdot, int j, double* H,
+                       long long ldh, double* scal, double* brk_hist);
 /* out = {sum x^2 over len_sum, max|x| over len_max} */
 int emhd_norms(emhd_ctx* ctx, const double* x, long long len_sum, long long len_max, double* out);
 /* H[:j+1, j] = h1 + h2; hnext = sqrt(nrm[0]); breakdown if hnext <= 1e-12 max(sqrt(selfdot), 1);

@@ -57,6 +57,8 @@ _SIGS = {
     "emhd_multidot": (c_int, [c_vp, P, P, c_ll, c_int, c_ll, c_int, P]),
     "emhd_update": (c_int, [c_vp, P, P, c_ll, c_int, P, c_ll, c_ll, c_ll, c_int, P]),
     "emhd_norms": (c_int, [c_vp, P, c_ll, c_ll, P]),
+    "emhd_update_finish": (c_int, [c_vp, P, P, c_ll, c_int, P, c_ll, c_ll, c_ll, P, P, P, c_int, P,
+                                   c_ll, P, P]),
     "emhd_arnoldi_finish": (c_int, [c_vp, P, P, P, P, c_int, P, c_ll, P, P]),
     "emhd_set_epoch": (c_int, [c_vp, c_int]),
     "emhd_div_scalar": (c_int, [c_vp, P, P, c_int, P, P, c_ll]),

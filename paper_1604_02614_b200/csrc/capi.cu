@@ -221,6 +221,21 @@ extern "C" int emhd_update(emhd_ctx* c, double* w, const double* V, long long ld
   return cerr(launch_update(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode, k, out, c->stream));
 }
 
+extern "C" int emhd_update_finish(emhd_ctx* c, double* w, const double* V, long long ldv, int nvec,
+                                  const double* h2, long long len_upd, long long len_dot,
+                                  long long len_max, double* nrm, const double* h1,
+                                  const double* selfdot, int j, double* H, long long ldh, double* scal,
+                                  double* brk_hist) {
+  if (!c || !w || !V || !h2 || !nrm || !h1 || !selfdot || !H || !scal || nvec < 1 ||
+      nvec > c->max_vectors || j < 0)
+    return EMHD_ERR_ARG;
+  KWork k = kwork(c);
+  FinishArgs F;
+  F.h1 = h1; F.h2 = h2; F.selfdot = selfdot; F.j = j; F.H = H; F.ldh = ldh; F.scal = scal;
+  F.brk_hist = brk_hist; F.st = c->st; F.rtol = 1e-12;
+  return cerr(launch_update(w, V, ldv, nvec, h2, len_upd, len_dot, len_max, 1, k, nrm, c->stream, F));
+}
+
 extern "C" int emhd_norms(emhd_ctx* c, const double* x, long long len_sum, long long len_max, double* out) {
   if (!c || !x || !out) return EMHD_ERR_ARG;
   KWork k = kwork(c);

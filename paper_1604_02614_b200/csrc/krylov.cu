@@ -132,11 +132,27 @@ __global__ void __launch_bounds__(KT, 4) multidot_kernel(const double* __restric
 // w[0:len_upd] -= sum_i h[i] V_i ; MODE 0: out[i] = <w_new, V_i> over len_dot (the
 // CGS2 re-projection; the second read of each V tile hits L1/L2, not DRAM);
 // MODE 1: out = {sum w^2 over len_dot, max|w| over len_max}.
+__device__ __forceinline__ void finish_column(const FinishArgs& F, const double* nrm) {
+  // krylov.py:161-166: H[:j+1, j] = h1 + h2, hnext = ||w||, breakdown test, scal for the next Jv
+  for (int i = threadIdx.x; i <= F.j; i += blockDim.x) F.H[(size_t)i * F.ldh + F.j] = F.h1[i] + F.h2[i];
+  if (threadIdx.x == 0) {
+    const double hnext = sqrt(nrm[0]);
+    const double scale = sqrt(F.selfdot[0]);
+    const bool brk = hnext <= F.rtol * fmax(scale, 1.0);
+    if (brk) F.st->breakdown = 1;
+    else F.H[(size_t)(F.j + 1) * F.ldh + F.j] = hnext;
+    F.scal[0] = hnext;
+    F.scal[1] = nrm[1];
+    F.scal[2] = brk ? 1.0 : 0.0;
+    if (F.brk_hist) F.brk_hist[F.j] = brk ? 1.0 : 0.0;
+  }
+}
+
 template <int MODE, int U>
 __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, const double* __restrict__ h,
     long long len_upd, long long len_dot, long long len_max,
-    double* partials, double* out, unsigned int* ticket) {
+    double* partials, double* out, unsigned int* ticket, const FinishArgs fin) {
   extern __shared__ double sm[];
   constexpr int TL = KT * 2;
   double* s_h = sm;                              // [nvec]
@@ -205,7 +221,11 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     __shared__ int kinds_s[2];
     if (threadIdx.x == 0) { kinds_s[0] = 0; kinds_s[1] = 1; }
     __syncthreads();
-    finish_partials(partials, 2, gridDim.x, kinds_s, out, ticket);
+    const bool last = finish_partials(partials, 2, gridDim.x, kinds_s, out, ticket);
+    if (last && fin.H) {
+      __syncthreads();
+      finish_column(fin, out);
+    }
   } else {
     cta_store_partials(s_acc, nval, partials, gridDim.x);
     finish_partials(partials, nval, gridDim.x, nullptr, out, ticket);
@@ -245,21 +265,10 @@ __global__ void __launch_bounds__(KT) norms_kernel(const double* __restrict__ x,
 __global__ void arnoldi_finish_kernel(const double* h1, const double* h2, const double* nrm,
     const double* selfdot, int j, double* H, long long ldh, double* scal, double* brk_hist,
     DevStatus* st, double rtol) {
-  for (int i = threadIdx.x; i <= j; i += blockDim.x) H[(size_t)i * ldh + j] = h1[i] + h2[i];
-  if (threadIdx.x == 0) {
-    const double hnext = sqrt(nrm[0]);
-    const double scale = sqrt(selfdot[0]);
-    const bool brk = hnext <= rtol * fmax(scale, 1.0);
-    if (brk) {
-      st->breakdown = 1;
-    } else {
-      H[(size_t)(j + 1) * ldh + j] = hnext;
-    }
-    scal[0] = hnext;
-    scal[1] = nrm[1];
-    scal[2] = brk ? 1.0 : 0.0;
-    if (brk_hist) brk_hist[j] = brk ? 1.0 : 0.0;
-  }
+  FinishArgs F;
+  F.h1 = h1; F.h2 = h2; F.selfdot = selfdot; F.j = j; F.H = H; F.ldh = ldh; F.scal = scal;
+  F.brk_hist = brk_hist; F.st = st; F.rtol = rtol;
+  finish_column(F, nrm);
 }
 
 // out[s] = base[s] (+) coef[s] * sum_i Y[s*m + i] V_i   (S <= 4 outputs, one sweep over V)
@@ -321,16 +330,16 @@ cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int
 
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
-                          KWork& wk, double* out, cudaStream_t s) {
+                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin) {
   const int G = grid_for(len_upd, KT * 2, wk.num_sms);
   const int nval = mode == 0 ? nvec : 2;
   const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)(nval > 0 ? nval : 1) * NWARP);
   if (mode == 0)
     update_kernel<0, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket);
+                                           wk.partials, out, wk.ticket, fin);
   else
     update_kernel<1, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket);
+                                           wk.partials, out, wk.ticket, fin);
   return cudaGetLastError();
 }
 

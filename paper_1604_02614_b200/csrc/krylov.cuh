@@ -10,6 +10,19 @@ struct KWork {
   int num_sms;
 };
 
+struct FinishArgs {         // optional Arnoldi column bookkeeping fused into update mode 1
+  const double* h1;
+  const double* h2;
+  const double* selfdot;
+  int j;
+  double* H;                 // null: not fused
+  long long ldh;
+  double* scal;
+  double* brk_hist;
+  DevStatus* st;
+  double rtol;
+};
+
 struct CombineOut {
   const double* base[4];     // optional base vector per output (null: plain V y)
   double coef[4];            // out = base + coef * (V y)
@@ -20,7 +33,7 @@ cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int
                             int self, KWork& wk, double* out, cudaStream_t s);
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
-                          KWork& wk, double* out, cudaStream_t s);
+                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin = FinishArgs{});
 cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, KWork& wk, double* out,
                          cudaStream_t s);
 cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,

@@ -127,6 +127,41 @@ __device__ __forceinline__ void combine_cell(const RawCell<MODE>& x, bool xflip,
   if (yflip) { u[2] = -u[2]; u[5] = -u[5]; }
 }
 
+// --- cp.async staging of raw rows (Ampere+ LDGSTS; no register cost) -------------
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// raw ring layout: [slot][array (a, v)][field][column slot]
+template <int MODE, int QW>
+__device__ __forceinline__ void fetch_async(const StencilParams& P, const RowRef& R, int jsrc, int c,
+                                            double* slot) {
+  constexpr int NA = MODE == MODE_RHS ? 1 : 2;
+  const double* A = R.halo ? P.a_halo : P.a;
+  const long long o = R.off + jsrc;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) cp_async8(slot + f * QW + c, A + o + f * R.fs);
+  if (NA == 2) {
+    const double* Vv = R.halo ? P.v_halo : P.v;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) cp_async8(slot + (NF + f) * QW + c, Vv + o + f * R.fs);
+  }
+}
+
+template <int MODE, int QW>
+__device__ __forceinline__ void consume_raw(const double* slot, int c, RawCell<MODE>& x) {
+#pragma unroll
+  for (int f = 0; f < NF; ++f) x.a[f] = slot[f * QW + c];
+  if (MODE != MODE_RHS) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) x.v[f] = slot[(NF + f) * QW + c];
+  }
+}
+
 // pressure / admissibility / primitives (mhd.py:106-131, 176-181, 217-221)
 __device__ __forceinline__ void cell_prims(const StencilParams& P, const double u[NF],
                                            double* q, int qs, int& flag) {
@@ -243,6 +278,8 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
   double* qring = smem;                             // [3][NQ][QW]
   double* gxring = qring + 3 * NQ * QW;             // [3][NF][TY]
   double* gyring = gxring + 3 * NF * TY;            // [2][NF][GYW]
+  constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
+  double* rawring = gyring + 2 * NF * GYW;          // [2][NARR*NF][QW] raw rows in flight
 
   const int t = threadIdx.x;
   const int j0 = blockIdx.x * TY;
@@ -339,25 +376,38 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
         cell_prims(P, u, q + cextra, QW, flag);
       }
     }
-    // software pipeline: the raw inputs of row r+1 are in flight while the
-    // fluxes of row r-1 and the outputs of row r-2 are computed
-    RawCell<MODE> xm, xe;
+    // software pipeline: raw inputs of rows r+1 and r+2 stream into a 2-slot shared
+    // ring by cp.async while the fluxes of row r-1 and outputs of row r-2 are computed;
+    // every thread consumes only the cells it copied itself, so no barrier guards the ring
     double fa_pre[NF];                       // F(a) of the next output row, one step ahead
     if (MODE != MODE_RHS && t < ncols_out) {
       const long long o = (long long)i0 * P.ny + j0 + t;
 #pragma unroll
       for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o + (long long)f * P.nx * P.ny);
     }
-    RowRef Rn = row_ref(P, i0);
-    if (okm) fetch_cell<MODE>(P, Rn, jm, xm);
-    if (oke) fetch_cell<MODE>(P, Rn, je, xe);
+    constexpr int SLOT = NARR * NF * QW;
+    for (int k = 0; k < 2; ++k) {
+      const int rr = i0 + k;
+      if (rr <= i1 + 1) {
+        const RowRef R = row_ref(P, rr);
+        if (okm) fetch_async<MODE, QW>(P, R, jm, cmain, rawring + k * SLOT);
+        if (oke) fetch_async<MODE, QW>(P, R, je, cextra, rawring + k * SLOT);
+      }
+      cp_commit();
+    }
     for (int r = i0; r <= i1 + 1; ++r) {
-      // ---- primitives of row r (prefetched)
+      const int slot = (r - i0) & 1;
+      double* sraw = rawring + slot * SLOT;
+      cp_wait<1>();                          // row r has landed (row r+1 may still be in flight)
+      // ---- primitives of row r
       {
+        const RowRef Rr = row_ref(P, r);
         double* q = qring + ((r + 3) % 3) * NQ * QW;
         double u[NF];
         if (okm) {
-          combine_cell<MODE>(xm, Rn.flip, fm, sigma, hnext, rh, fh, u);
+          RawCell<MODE> xm;
+          consume_raw<MODE, QW>(sraw, cmain, xm);
+          combine_cell<MODE>(xm, Rr.flip, fm, sigma, hnext, rh, fh, u);
           cell_prims(P, u, q + cmain, QW, flag);
           if (MODE == MODE_JVN && r >= i0 && r < i1 && t < ncols_out) {
             // v_j = w / h_next of an owned cell (krylov.py:167), from the fetched w
@@ -369,15 +419,19 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
           }
         }
         if (oke) {
-          combine_cell<MODE>(xe, Rn.flip, fe, sigma, hnext, rh, fh, u);
+          RawCell<MODE> xe;
+          consume_raw<MODE, QW>(sraw, cextra, xe);
+          combine_cell<MODE>(xe, Rr.flip, fe, sigma, hnext, rh, fh, u);
           cell_prims(P, u, q + cextra, QW, flag);
         }
       }
-      if (r + 1 <= i1 + 1) {
-        Rn = row_ref(P, r + 1);
-        if (okm) fetch_cell<MODE>(P, Rn, jm, xm);
-        if (oke) fetch_cell<MODE>(P, Rn, je, xe);
+      // refill the consumed slot with row r+2
+      if (r + 2 <= i1 + 1) {
+        const RowRef R2 = row_ref(P, r + 2);
+        if (okm) fetch_async<MODE, QW>(P, R2, jm, cmain, sraw);
+        if (oke) fetch_async<MODE, QW>(P, R2, je, cextra, sraw);
       }
+      cp_commit();
       __syncthreads();
       // ---- fluxes of row rf = r - 1
       const int rf = r - 1;
@@ -549,7 +603,8 @@ cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* 
 template <int TY, int MODE, bool AUG, bool FXY>
 static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   constexpr int QW = TY + 4, GYW = TY + 2;
-  const size_t sm = sizeof(double) * (3 * NQ * QW + 3 * NF * TY + 2 * NF * GYW);
+  constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
+  const size_t sm = sizeof(double) * (3 * NQ * QW + 3 * NF * TY + 2 * NF * GYW + 2 * NARR * NF * QW);
   auto k = stencil_kernel<TY, MODE, AUG, FXY>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

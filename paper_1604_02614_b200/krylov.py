@@ -298,13 +298,21 @@ class _Process:
         N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d1),
                                      self.len_upd, self.len_dot, self.n_top, 0, D.ptr(self.d2)), "update")
         self._allreduce_sum(self.d2[:nv])
-        # w -= V h2 ; ||w||^2, max|w_top|
-        N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2),
-                                     self.len_upd, self.len_dot, self.n_top, 1, D.ptr(self.nrm)), "update")
-        self._allreduce_norms(self.nrm)
-        N.check(self.lib.emhd_arnoldi_finish(h, D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm),
-                                             D.ptr(self.d1[nv:]), j, D.ptr(self.H), self.H.shape[1],
-                                             D.ptr(self.scal.dev), D.ptr(self.brk)), "arnoldi_finish")
+        # w -= V h2 ; ||w||^2, max|w_top| ; column bookkeeping (fused when single-rank)
+        if self.comm is None or not self.layout.distributed:
+            N.check(self.lib.emhd_update_finish(
+                h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2), self.len_upd, self.len_dot,
+                self.n_top, D.ptr(self.nrm), D.ptr(self.d1), D.ptr(self.d1[nv:]), j, D.ptr(self.H),
+                self.H.shape[1], D.ptr(self.scal.dev), D.ptr(self.brk)), "update_finish")
+        else:
+            N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2),
+                                         self.len_upd, self.len_dot, self.n_top, 1, D.ptr(self.nrm)),
+                    "update")
+            self._allreduce_norms(self.nrm)
+            N.check(self.lib.emhd_arnoldi_finish(h, D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm),
+                                                 D.ptr(self.d1[nv:]), j, D.ptr(self.H),
+                                                 self.H.shape[1], D.ptr(self.scal.dev), D.ptr(self.brk)),
+                    "arnoldi_finish")
         self.m = j + 1
         if not sync and self.eng.fused:
             self._pending = True
