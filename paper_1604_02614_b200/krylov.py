@@ -181,6 +181,7 @@ class _Process:
         self.brk = self._small[o2:o2 + self.m_cap + 1]
         self.nb = self._small[o2 + self.m_cap + 1:o2 + self.m_cap + 5]   # {sum seed^2, max|seed|, beta, -}
         self.scal = D.Scratch(4)
+        self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
         self._settled = 0
         self._pending = False
@@ -319,14 +320,15 @@ class _Process:
             return True
         return self.settle()
 
-    def settle(self):
-        """One host sync: breakdown position and the device status of queued iterations."""
+    def settle(self, res_dev=None):
+        """One host sync: breakdown position, device status of queued iterations and (when
+        given) the residual estimates just computed on the device; returns them."""
         self._pending = False
         first = self._settled
         self.brk_host[:self.m].copy_(self.brk[:self.m], non_blocking=True)
-        st = self.ctx.status() if self.eng.fused else None       # synchronises the stream
-        if not self.eng.fused:
-            torch.cuda.current_stream().synchronize()
+        if res_dev is not None:
+            self.res_host[:res_dev.numel()].copy_(res_dev, non_blocking=True)
+        st = self.ctx.status()                 # synchronises the stream
         flags = self.brk_host[first:self.m].numpy()
         hit = np.flatnonzero(flags != 0.0)
         if hit.size:
@@ -335,11 +337,16 @@ class _Process:
             self.m = b + 1
             self.breakdown = True
         self._settled = self.m
-        if st is not None:
-            if self.comm is not None and self.layout.distributed:
-                from .mhd import agree_status
-                st = agree_status(st, self.comm)
+        if self.comm is not None and self.layout.distributed:
+            from .mhd import agree_status
+            st = agree_status(st, self.comm)
+        if self.eng.fused:
             self.check_status(st)
+        if st.flags & N.ST_DENSE:
+            self.ctx.reset_status()
+            raise FloatingPointError("overflow in augmented-matrix exponential")
+        if res_dev is not None:
+            return self.res_host[:res_dev.numel()].numpy().copy()
         return not self.breakdown
 
     def check_status(self, st):
@@ -495,13 +502,12 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
     proc.settle()
     while True:
         _, res_raw = proc.phi_coeffs(order, [c_big * h])
-        r = float(res_raw[0].item())
-        _dense_check(eng.ctx)
+        r = float(proc.settle(res_raw)[0])          # the iteration's only host sync
         res = r * c_big * h
         if res <= tol or proc.breakdown or proc.m >= proc.n:
             break
         m_before = proc.m
-        proc.extend()
+        proc.extend(sync=False)
         if proc.m == m_before:
             stats.operator_applies += proc.applies
             raise KrylovConvergenceError(
@@ -511,7 +517,8 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
     stats.max_basis_size = proc.m
     stats.substeps = 1
     Y, _ = proc.phi_coeffs(order, [c * h for c in scales])
-    _dense_check(eng.ctx)
+    if _into is None:
+        raise_status(eng.ctx, eng.ctx.status(), None, comm)    # dense overflow of the last phi
     outs = []
     for k in range(0, len(scales), 4):
         chunk = list(range(k, min(k + 4, len(scales))))
@@ -574,8 +581,7 @@ def phi_comb(req, cfg=None, _zero=None):
         proc.settle()
         while True:
             Y, res_raw = proc.phi_coeffs(0, [delta])
-            r = float(res_raw[0].item())
-            _dense_check(eng.ctx)
+            r = float(proc.settle(res_raw)[0])      # the iteration's only host sync
             res = r * delta
             tol_sub = req.tol * max(delta, 1e-2)
             if res <= tol_sub or proc.breakdown or proc.m >= proc.n:
@@ -584,7 +590,7 @@ def phi_comb(req, cfg=None, _zero=None):
                 delta = delta / 2.0
                 continue
             m_before = proc.m
-            proc.extend()
+            proc.extend(sync=False)
             if proc.m == m_before:
                 if delta > cfg.min_substep:
                     delta = delta / 2.0

@@ -148,9 +148,11 @@ def raise_status(ctx, st, report_args=None, comm=None):
     st = agree_status(st, comm)
     flags = st.flags
     local = getattr(st, "local_flags", flags)
-    if not flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE):
+    if not flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE | N.ST_DENSE):
         return
     ctx.reset_status()
+    if not flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE):
+        raise FloatingPointError("overflow in augmented-matrix exponential")
     if flags & (N.ST_RHO | N.ST_PRESSURE):
         msg = None
         if report_args is not None and local & (N.ST_RHO | N.ST_PRESSURE):

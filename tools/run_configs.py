@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--pr", type=float, default=1.0)
     ap.add_argument("--m-max", type=int, default=100)
     ap.add_argument("--check", action="store_true", help="also run the CPU oracle and compare")
+    ap.add_argument("--repeat", type=int, default=2, help="time the last of N identical runs")
+    ap.add_argument("--profile", action="store_true", help="cProfile the timed run (host view)")
     a = ap.parse_args()
     import torch
     import paper_1604_02614_b200 as P
@@ -92,11 +94,22 @@ def main():
                                     cfg=cfg, recoverable=(P.AdmissibilityError,),
                                     max_steps=run.get("max_steps"))
 
+    for _ in range(max(a.repeat - 1, 0)):
+        go(f, yd)                      # warm-up runs (module loading, allocator)
     torch.cuda.synchronize()
+    prof = None
+    if a.profile:
+        import cProfile
+        prof = cProfile.Profile()
+        prof.enable()
     t0 = time.perf_counter()
     y, st = go(f, yd)
     torch.cuda.synchronize()
     T = time.perf_counter() - t0
+    if prof is not None:
+        prof.disable()
+        import pstats
+        pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(25)
     out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
            "iterations_per_s": st.operator_applies / T,
            "cell_steps_per_s": g.nx * g.ny * st.steps_accepted / T}
