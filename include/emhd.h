@@ -149,6 +149,12 @@ int emhd_phi_small(emhd_ctx* ctx, const double* H, long long ldh, int m, int ord
                    const double* scales, const double* res_scale, const double* scal,
                    const double* beta, double* Y, double* res);
 
+/* As emhd_phi_small with the S scales passed as a HOST array (copied into the launch) and
+ * res[s] unscaled.  Saves the device scratch and its host-to-device copy per residual check. */
+int emhd_phi_small_h(emhd_ctx* ctx, const double* H, long long ldh, int m, int order, int S,
+                     const double* host_scales, const double* scal, const double* beta, double* Y,
+                     double* res);
+
 /* E = expm(A), n x n row-major device matrices; work: device scratch of n + 4 doubles.
  * Synchronous.  (scipy.linalg.expm as called by phi_dense, phifuncs.py:97,104) */
 int emhd_expm(emhd_ctx* ctx, const double* A, int n, double* E, double* work);
@@ -174,6 +180,18 @@ int emhd_wrms(emhd_ctx* ctx, const double* err, const double* y, double tol, lon
 int emhd_admissibility_report(emhd_ctx* ctx, int mode, const double* a, const double* a_halo,
                               const double* v, const double* v_halo, const double* scal,
                               void* report);
+
+/* ---- single-rank Arnoldi driver ------------------------------------ */
+/* args: a plain struct of device pointers and sizes (layout in paper_1604_02614_b200/_native.py,
+ * ArnoldiArgs): a, F(a), V, ldv, H, ldh, w0, w1, d1, d2, nrm, vn, scal, brk, n_top, len_dot,
+ * len_upd, p, nb, ch, bcol[5], bidx[5].  Launches iteration j of _ArnoldiProcess.extend
+ * (krylov.py:144-168) — (normalise +) Jv, multi-dot, update + re-dot, update + norms +
+ * column bookkeeping — as one stream-ordered call. */
+int emhd_arnoldi_iter(emhd_ctx* ctx, const void* args, int j);
+/* Copy brk[0:nbrk] and res[0:nres] into host_out (pinned), then read the status word: the one
+ * host synchronisation of a residual check. */
+int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res, int nres,
+                  double* host_out, emhd_status* st);
 
 /* ---- slab halos ------------------------------------------------------ */
 /* sendbuf[2][8][2][ny] = rows {0,1} and {nx-2, nx-1} of every field of x */

@@ -33,6 +33,13 @@ class Status(ctypes.Structure):
                 ("breakdown", c_int), ("fail_iter", c_int)]
 
 
+class ArnoldiArgs(ctypes.Structure):
+    _fields_ = [("a", P), ("fa", P), ("V", P), ("ldv", c_ll), ("H", P), ("ldh", c_ll),
+                ("w0", P), ("w1", P), ("d1", P), ("d2", P), ("nrm", P), ("vn", P), ("scal", P),
+                ("brk", P), ("n_top", c_ll), ("len_dot", c_ll), ("len_upd", c_ll), ("p", c_int),
+                ("nb", c_int), ("ch", c_dbl), ("bcol", P * 5), ("bidx", c_int * 5)]
+
+
 class Report(ctypes.Structure):
     _fields_ = [("which", c_int), ("i", c_int), ("j", c_int), ("pad", c_int), ("value", c_dbl)]
 
@@ -64,6 +71,9 @@ _SIGS = {
     "emhd_div_scalar": (c_int, [c_vp, P, P, c_int, P, P, c_ll]),
     "emhd_phi_small": (c_int, [c_vp, P, c_ll, c_int, c_int, c_int, P, P, P, P, P, P]),
     "emhd_expm": (c_int, [c_vp, P, c_int, P, P]),
+    "emhd_phi_small_h": (c_int, [c_vp, P, c_ll, c_int, c_int, c_int, DP, P, P, P, P]),
+    "emhd_arnoldi_iter": (c_int, [c_vp, c_vp, c_int]),
+    "emhd_readback": (c_int, [c_vp, P, c_int, P, c_int, P, ctypes.POINTER(Status)]),
     "emhd_combine": (c_int, [c_vp, P, c_ll, c_int, P, c_int, PP, DP, PP, c_ll]),
     "emhd_lincomb": (c_int, [c_vp, c_int, PP, DP, IP, c_dbl, c_int, P, c_ll, c_ll, P]),
     "emhd_wrms": (c_int, [c_vp, P, P, c_dbl, c_ll, P]),

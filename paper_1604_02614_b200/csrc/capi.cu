@@ -258,9 +258,10 @@ extern "C" int emhd_div_scalar(emhd_ctx* c, const double* x, const double* d, in
 
 static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, int order, int S,
                           const double* scales, const double* res_scale, const double* scal,
-                          const double* beta, double* Y, double* res, double* E_out) {
-  if (!c || !H || m < 1 || order < 0 || order > 4 || S < 1 || S > DENSE_MAX_SCALES || !scales ||
-      !res_scale || !beta || !Y || !res)
+                          const double* beta, double* Y, double* res, double* E_out,
+                          const double* host_scales = nullptr) {
+  if (!c || !H || m < 1 || order < 0 || order > 4 || S < 1 || S > DENSE_MAX_SCALES ||
+      (!host_scales && (!scales || !res_scale)) || !beta || !Y || !res)
     return EMHD_ERR_ARG;
   const size_t n = (size_t)(order + 1) * m;
   const size_t per = 11 * n * n + 3 * n + 64;
@@ -280,6 +281,10 @@ static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, in
   std::memset(&P, 0, sizeof(P));
   P.H = H; P.ldh = ldh; P.m = m; P.order = order; P.scales = scales; P.res_scale = res_scale;
   P.scal = scal; P.beta = beta; P.Y = Y; P.res = res; P.st = c->st; P.E_out = E_out;
+  if (host_scales) {
+    P.scales_by_value = 1;
+    for (int s = 0; s < S; ++s) { P.sv[s] = host_scales[s]; P.rv[s] = 1.0; }
+  }
   for (int s = 0; s < S; ++s) {
     double* b = c->dense + per * s;
     size_t nn = n * n;
@@ -296,6 +301,15 @@ extern "C" int emhd_phi_small(emhd_ctx* c, const double* H, long long ldh, int m
                               const double* scales, const double* res_scale, const double* scal,
                               const double* beta, double* Y, double* res) {
   return phi_small_impl(c, H, ldh, m, order, S, scales, res_scale, scal, beta, Y, res, nullptr);
+}
+
+// scales given as a HOST array (no device scratch, no H2D copy); res[s] is the raw residual
+extern "C" int emhd_phi_small_h(emhd_ctx* c, const double* H, long long ldh, int m, int order, int S,
+                                const double* host_scales, const double* scal, const double* beta,
+                                double* Y, double* res) {
+  if (!host_scales) return EMHD_ERR_ARG;
+  return phi_small_impl(c, H, ldh, m, order, S, nullptr, nullptr, scal, beta, Y, res, nullptr,
+                        host_scales);
 }
 
 // E = expm(A) for an n x n device matrix (scratch: 4 doubles + n doubles in `work`)
@@ -411,4 +425,72 @@ extern "C" int emhd_admissibility_report(emhd_ctx* c, int mode, const double* a,
   }
   if (R->which && c->g.x_offset) R->i += c->g.x_offset;
   return EMHD_OK;
+}
+
+// ---- single-rank Arnoldi driver: one C call per iteration ---------------------------
+struct emhd_arnoldi_args_s {
+  const double* a; const double* fa;
+  double* V; long long ldv;
+  double* H; long long ldh;
+  double* w0; double* w1;
+  double* d1; double* d2; double* nrm; double* vn; double* scal; double* brk;
+  long long n_top; long long len_dot; long long len_upd;
+  int p; int nb; double ch;
+  const double* bcol[5]; int bidx[5];
+};
+
+// Iteration j of krylov.py:144-168 on one rank: (normalise w_{j-1} +) Jv, pass-1 multi-dot with
+// the breakdown scale, update + re-projection, update + norms + column bookkeeping.  Writes
+// w_{j} into w0/w1 (j even/odd) and V[j] (j > 0), H[:, j], scal, brk[j].
+extern "C" int emhd_arnoldi_iter(emhd_ctx* c, const void* args, int j) {
+  if (!c || !args || j < 0) return EMHD_ERR_ARG;
+  const emhd_arnoldi_args_s* A = (const emhd_arnoldi_args_s*)args;
+  if (j + 1 > c->max_vectors) return EMHD_ERR_ARG;
+  c->epoch = j;
+  double* out = (j % 2 == 0) ? A->w0 : A->w1;
+  StencilParams P = c->base;
+  P.epoch = j;
+  P.a = A->a; P.fa = A->fa; P.out = out;
+  set_epilogue(P, A->p, A->ch, A->nb, A->bcol, A->bidx);
+  KWork k = kwork(c);
+  int rc;
+  if (j == 0) {
+    // sigma of the seed direction: max|V[0][:n]| into vn[1] (norms writes {sum, max})
+    rc = cerr(launch_norms(A->V, 0, A->n_top, k, A->vn, c->stream));
+    if (rc) return rc;
+    P.v = A->V; P.scal = A->vn + 1;
+    if (A->p > 0) P.qsrc = A->V + A->n_top;
+    rc = cerr(launch_stencil(P, MODE_JV, A->p > 0, c->num_sms, c->stream));
+  } else {
+    P.v = (j % 2 == 0) ? A->w1 : A->w0;
+    P.scal = A->scal;
+    P.vout = A->V + (size_t)j * A->ldv;
+    rc = cerr(launch_stencil(P, MODE_JVN, A->p > 0, c->num_sms, c->stream));
+  }
+  if (rc) return rc;
+  const int nv = j + 1;
+  rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream));
+  if (!rc) rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
+                                   A->d2, c->stream));
+  if (rc) return rc;
+  FinishArgs F;
+  F.h1 = A->d1; F.h2 = A->d2; F.selfdot = A->d1 + nv; F.j = j; F.H = A->H; F.ldh = A->ldh;
+  F.scal = A->scal; F.brk_hist = A->brk; F.st = c->st; F.rtol = 1e-12;
+  return cerr(launch_update(out, A->V, A->ldv, nv, A->d2, A->len_upd, A->len_dot, A->n_top, 1, k,
+                            A->nrm, c->stream, F));
+}
+
+// One sync point: host_out[0:nbrk] = brk[0:nbrk], host_out[nbrk:nbrk+nres] = res[0:nres]
+// (host_out should be pinned), then the status word; returns after the stream drained.
+extern "C" int emhd_readback(emhd_ctx* c, const double* brk, int nbrk, const double* res, int nres,
+                             double* host_out, emhd_status* st) {
+  if (!c || !host_out || !st || nbrk < 0 || nres < 0) return EMHD_ERR_ARG;
+  int rc = 0;
+  if (nbrk > 0) rc = cerr(cudaMemcpyAsync(host_out, brk, sizeof(double) * nbrk, cudaMemcpyDeviceToHost,
+                                          c->stream));
+  if (!rc && nres > 0)
+    rc = cerr(cudaMemcpyAsync(host_out + nbrk, res, sizeof(double) * nres, cudaMemcpyDeviceToHost,
+                              c->stream));
+  if (rc) return rc;
+  return emhd_status_read(c, st);
 }

@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   DenseWork W = P.work[sidx];
   double* A = W.a;
   double* E = W.e;
-  const double sc = P.scales[sidx];
+  const double sc = P.scales_by_value ? P.sv[sidx] : P.scales[sidx];
   const double hn = P.scal ? P.scal[0] : 0.0;
   const bool brk = P.scal ? (P.scal[2] != 0.0) : true;
   const double beta = P.beta[0];
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
     const double ylast = E[(size_t)(m - 1) * n + P.order * m] * beta;
     const double hnext = brk ? 0.0 : hn;
     double r = (nrm == 0.0) ? 0.0 : fabs(hnext) * fabs(ylast) / nrm;
-    P.res[sidx] = r * P.res_scale[sidx];
+    P.res[sidx] = r * (P.scales_by_value ? P.rv[sidx] : P.res_scale[sidx]);
   }
 }
 

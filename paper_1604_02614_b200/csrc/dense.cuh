@@ -25,7 +25,10 @@ struct PhiSmallArgs {
   double* res;              // [S] residual estimates
   DenseWork work[DENSE_MAX_SCALES];
   DevStatus* st;
-  double* E_out;            // optional: full n x n exponential of scale_0 * A (S = 1)
+  double* E_out;
+  int scales_by_value;       // 1: use sv / rv instead of the device arrays
+  double sv[DENSE_MAX_SCALES];
+  double rv[DENSE_MAX_SCALES];            // optional: full n x n exponential of scale_0 * A (S = 1)
 };
 
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s);

@@ -616,7 +616,13 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
     const int target = (occ < 1 ? 1 : occ) * num_sms;
     const int chunks = (target + strips - 1) / strips;
     const int rows = (P.nx + chunks - 1) / chunks;
-    P.rows_per_cta = rows < 8 ? 8 : rows;
+    static int min_rows = -1;
+    if (min_rows < 0) {
+      const char* env = getenv("EMHD_MIN_ROWS");
+      min_rows = env ? atoi(env) : 2;
+      if (min_rows < 1) min_rows = 1;
+    }
+    P.rows_per_cta = rows < min_rows ? min_rows : rows;
   }
   dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
   k<<<grid, TY, sm, s>>>(P);

@@ -185,6 +185,9 @@ class _Process:
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
         self._settled = 0
         self._pending = False
+        self.Ybuf = torch.empty(4 * (self.m_cap + 1), dtype=D.F64, device=D.device())
+        self.resbuf = torch.empty(8, dtype=D.F64, device=D.device())
+        self.host_rb = torch.zeros(self.m_cap + 16, dtype=D.F64, pin_memory=True)
         self.beta_dev = self.nb[2:3]
         self.m = 0
         self.breakdown = False
@@ -203,6 +206,24 @@ class _Process:
         N.check(self.lib.emhd_div_scalar(h, D.ptr(sd), D.ptr(self.nb), 1, D.ptr(self.V[0]),
                                          D.ptr(self.beta_dev), self.naug), "div_scalar")
         self._vm_ready = 1
+        # single-rank fused engine: one C call per iteration (emhd_arnoldi_iter)
+        self.fast = engine.fused and (layout is None or not layout.distributed)
+        if self.fast:
+            E = engine
+            A = N.ArnoldiArgs()
+            A.a, A.fa = D.ptr(E.jop.a), D.ptr(E.jop.f_a)
+            A.V, A.ldv = D.ptr(self.V), self.ld
+            A.H, A.ldh = D.ptr(self.H), self.H.shape[1]
+            A.w0, A.w1 = D.ptr(self.w[0]), D.ptr(self.w[1])
+            A.d1, A.d2, A.nrm = D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm)
+            A.vn, A.scal, A.brk = D.ptr(E._vn), D.ptr(self.scal.dev), D.ptr(self.brk)
+            A.n_top, A.len_dot, A.len_upd = self.n_top, self.len_dot, self.len_upd
+            A.p, A.nb, A.ch = self.p, len(E.bcols), E.ch
+            for k, b in enumerate(E.bcols):
+                A.bcol[k] = D.ptr(b)
+                A.bidx[k] = E.bidx[k]
+            self._args = A
+            self._args_ref = D.ctypes_byref(A)
 
     # -- collectives ----------------------------------------------------------
     def _allreduce_sum(self, t):
@@ -285,6 +306,18 @@ class _Process:
         if self.breakdown or self.m >= self.m_cap:
             return False
         j = self.m
+        if self.fast:
+            N.check(self.lib.emhd_arnoldi_iter(self.ctx.sync_stream(), self._args_ref, j), "arnoldi_iter")
+            self.applies += 1
+            self.cur = j % 2
+            if j > 0:
+                self._vm_ready = j + 1
+            self._last = (2 if j else 1, None, None, None)
+            self.m = j + 1
+            if not sync:
+                self._pending = True
+                return True
+            return self.settle()
         self.lib.emhd_set_epoch(self.ctx.sync_stream(), j)
         wi = self._apply(j)
         self.applies += 1
@@ -325,11 +358,23 @@ class _Process:
         given) the residual estimates just computed on the device; returns them."""
         self._pending = False
         first = self._settled
-        self.brk_host[:self.m].copy_(self.brk[:self.m], non_blocking=True)
-        if res_dev is not None:
-            self.res_host[:res_dev.numel()].copy_(res_dev, non_blocking=True)
-        st = self.ctx.status()                 # synchronises the stream
-        flags = self.brk_host[first:self.m].numpy()
+        nres = 0 if res_dev is None else res_dev.numel()
+        if self.fast:
+            st = N.Status()
+            nb = self.m - first
+            N.check(self.lib.emhd_readback(self.ctx.sync_stream(), D.ptr(self.brk) + 8 * first, nb,
+                                           D.ptr(res_dev) if nres else None, nres,
+                                           D.ptr(self.host_rb), D.ctypes_byref(st)), "readback")
+            hb = self.host_rb.numpy()
+            flags = hb[:nb]
+            if nres:
+                self.res_host[:nres].copy_(self.host_rb[nb:nb + nres])
+        else:
+            self.brk_host[:self.m].copy_(self.brk[:self.m], non_blocking=True)
+            if res_dev is not None:
+                self.res_host[:nres].copy_(res_dev, non_blocking=True)
+            st = self.ctx.status()                 # synchronises the stream
+            flags = self.brk_host[first:self.m].numpy()
         hit = np.flatnonzero(flags != 0.0)
         if hit.size:
             b = first + int(hit[0])
@@ -394,18 +439,19 @@ class _Process:
     def phi_coeffs(self, order, scales):
         """Device Y[s] = beta phi_order(scale_s H_m) e1 and raw residuals (krylov.py:378-383)."""
         if len(scales) > 4:
-            parts = [self.phi_coeffs(order, scales[k:k + 4]) for k in range(0, len(scales), 4)]
+            parts = []
+            for k in range(0, len(scales), 4):
+                Yk, rk = self.phi_coeffs(order, scales[k:k + 4])
+                parts.append((Yk.clone(), rk.clone()))      # the next call reuses the buffers
             return torch.cat([p[0] for p in parts]), torch.cat([p[1] for p in parts])
         S = len(scales)
-        sc = torch.tensor([float(x) for x in scales], dtype=D.F64).to(D.device())
-        one = torch.ones(S, dtype=D.F64).to(D.device())
-        Y = torch.empty((S, self.m), dtype=D.F64, device=D.device())
-        res = torch.empty(S, dtype=D.F64, device=D.device())
+        Y = self.Ybuf[:S * self.m].view(S, self.m)
+        res = self.resbuf[:S]
         scal = None if self.breakdown else self.scal.dev
-        N.check(self.lib.emhd_phi_small(self.ctx.sync_stream(), D.ptr(self.H), self.H.shape[1], self.m,
-                                        order, S, D.ptr(sc), D.ptr(one),
-                                        D.ptr(scal) if scal is not None else D.ptr(self._brk()),
-                                        D.ptr(self.beta_dev), D.ptr(Y), D.ptr(res)), "phi_small")
+        N.check(self.lib.emhd_phi_small_h(self.ctx.sync_stream(), D.ptr(self.H), self.H.shape[1], self.m,
+                                          order, S, N.dbl_array(scales),
+                                          D.ptr(scal) if scal is not None else D.ptr(self._brk()),
+                                          D.ptr(self.beta_dev), D.ptr(Y), D.ptr(res)), "phi_small")
         return Y, res
 
     def _brk(self):
