@@ -136,11 +136,15 @@ __device__ void axpby_mat(double* out, const double* const* terms, const double*
   __syncthreads();
 }
 
-// Gauss–Jordan with partial pivoting on M = [Q | R] (n x 2n): R <- Q^{-1} R
-__device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac) {
+// Gauss–Jordan with partial pivoting on M = [Q | R] (n x 2n): R <- Q^{-1} R.
+// The pivot row is staged (scaled) in shared memory, rows are distributed over warps and
+// columns over lanes: no integer division in the elimination, one broadcast read per column.
+__device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac, double* prow) {
   const int w2 = 2 * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NWD = DT / 32;
   for (int k = 0; k < n; ++k) {
-    // pivot: largest |M[i][k]| for i >= k, lowest index on ties
+    // pivot: largest |M[i][k]| for i >= k, lowest index on ties (deterministic)
     double best = -1.0; int bi = n;
     for (int i = k + threadIdx.x; i < n; i += DT) {
       const double a = fabs(M[i * w2 + k]);
@@ -151,34 +155,37 @@ __device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac) 
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = best; ired[threadIdx.x >> 5] = bi; }
+    if (lane == 0) { red[warp] = best; ired[warp] = bi; }
     __syncthreads();
     if (threadIdx.x == 0) {
       double b = -1.0; int ii = n;
-      for (int w = 0; w < DT / 32; ++w)
+      for (int w = 0; w < NWD; ++w)
         if (red[w] > b || (red[w] == b && ired[w] < ii)) { b = red[w]; ii = ired[w]; }
-      ired[DT / 32] = ii;
-      red[DT / 32] = b;
+      ired[NWD] = ii;
+      red[NWD] = b;
     }
     __syncthreads();
-    const int piv = ired[DT / 32];
-    if (!(red[DT / 32] > 0.0)) return false;
-    if (piv != k)
-      for (int c = threadIdx.x; c < w2; c += DT) {
-        const double a = M[k * w2 + c];
-        M[k * w2 + c] = M[piv * w2 + c];
-        M[piv * w2 + c] = a;
-      }
+    const int piv = ired[NWD];
+    if (!(red[NWD] > 0.0)) return false;
+    const double d = M[piv * w2 + k];
+    // stage the scaled pivot row (columns > k) and swap rows k <-> piv
+    for (int c = k + 1 + threadIdx.x; c < w2; c += DT) {
+      const double pv = M[piv * w2 + c] / d;
+      prow[c] = pv;
+      if (piv != k) M[piv * w2 + c] = M[k * w2 + c];
+      M[k * w2 + c] = pv;
+    }
+    for (int i = threadIdx.x; i < n; i += DT) {
+      const int src = (i == piv) ? k : i;              // row piv now holds old row k
+      fac[i] = (i == k) ? 0.0 : M[src * w2 + k];
+    }
     __syncthreads();
-    const double d = M[k * w2 + k];
-    __syncthreads();
-    for (int c = k + threadIdx.x; c < w2; c += DT) M[k * w2 + c] /= d;
-    for (int i = threadIdx.x; i < n; i += DT) fac[i] = (i == k) ? 0.0 : M[i * w2 + k];
-    __syncthreads();
-    const int width = w2 - k - 1;
-    for (int e = threadIdx.x; e < n * width; e += DT) {
-      const int i = e / width, c = k + 1 + e % width;
-      if (i != k) M[i * w2 + c] = fma(-fac[i], M[k * w2 + c], M[i * w2 + c]);
+    if (piv != k && threadIdx.x == 0) M[piv * w2 + k] = M[k * w2 + k];
+    for (int i = warp; i < n; i += NWD) {
+      const double f = fac[i];
+      if (i == k || f == 0.0) continue;
+      double* row = M + (size_t)i * w2;
+      for (int c = k + 1 + lane; c < w2; c += 32) row[c] = fma(-f, prow[c], row[c]);
     }
     __syncthreads();
   }
@@ -187,7 +194,7 @@ __device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac) 
 
 // E = exp(A), A overwritten by scaling; returns false on failure.
 __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA, double* sB, double* red,
-                          int* ired) {
+                          int* ired, double* prow) {
   double* A2 = W.m[0];
   double* A4 = W.m[1];
   double* A6 = W.m[2];
@@ -289,7 +296,7 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
     M[r * 2 * n + n + c] = Vm[e] + U[e];
   }
   __syncthreads();
-  if (!gj_solve(M, n, red, ired, fac)) return false;
+  if (!gj_solve(M, n, red, ired, fac, prow)) return false;
   for (int e = threadIdx.x; e < n * n; e += DT) E[e] = M[(e / n) * 2 * n + n + e % n];
   __syncthreads();
   for (int k = 0; k < s; ++k) {
@@ -307,8 +314,15 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   __shared__ double sB[16 * 64];
   __shared__ double red[DT / 32 + 1];
   __shared__ int ired[DT / 32 + 1];
+  extern __shared__ double prow[];                 // [2n] staged pivot row
   const int sidx = blockIdx.x;
-  const int m = P.m, n = (P.order + 1) * m;
+  // phi_order(X) e1 from the (m + order)-dimensional augmentation
+  //   [[X, e1, 0 ..], [0, 0, 1 ..], .., [0 .. 0]]   (exp top-right column = phi_order(X) e1),
+  // the Expokit form of the reference's ((order+1) m)-dimensional block matrix
+  // (phifuncs.py:97-104): same phi to round-off, (order+1)^3 m^3 / (m+order)^3 less work.
+  // With E_out (emhd_expm, order 0) the matrix is exactly sc * H.
+  const int m = P.m, n = m + P.order;
+  const int col = (P.order == 0) ? 0 : m + P.order - 1;
   DenseWork W = P.work[sidx];
   double* A = W.a;
   double* E = W.e;
@@ -316,19 +330,19 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   const double hn = P.scal ? P.scal[0] : 0.0;
   const bool brk = P.scal ? (P.scal[2] != 0.0) : true;
   const double beta = P.beta[0];
-  // build the block upper-bidiagonal matrix [[sc*H, I, 0..], [0, 0, I..], ...]
   for (int e = threadIdx.x; e < n * n; e += DT) {
     const int r = e / n, c = e % n;
     double v = 0.0;
     if (r < m && c < m) v = sc * P.H[(size_t)r * P.ldh + c];
-    else if (c == r + m) v = 1.0;
+    else if (r == 0 && c == m) v = 1.0;
+    else if (r >= m && c == r + 1) v = 1.0;
     A[e] = v;
   }
   __syncthreads();
   bool finite = true;
   for (int e = threadIdx.x; e < m * m; e += DT) if (!isfinite(A[(e / m) * n + e % m])) finite = false;
   finite = __syncthreads_and(finite);
-  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired);
+  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow);
   if (ok) {
     bool fin2 = true;
     for (int e = threadIdx.x; e < n * n; e += DT) if (!isfinite(E[e])) fin2 = false;
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   }
   double ss = 0.0;
   for (int i = threadIdx.x; i < m; i += DT) {
-    const double yv = E[(size_t)i * n + P.order * m] * beta;
+    const double yv = E[(size_t)i * n + col] * beta;
     P.Y[(size_t)sidx * m + i] = yv;
     ss += yv * yv;
   }
@@ -354,7 +368,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
     double t = 0.0;
     for (int w = 0; w < DT / 32; ++w) t += red[w];
     const double nrm = sqrt(t);
-    const double ylast = E[(size_t)(m - 1) * n + P.order * m] * beta;
+    const double ylast = E[(size_t)(m - 1) * n + col] * beta;
     const double hnext = brk ? 0.0 : hn;
     double r = (nrm == 0.0) ? 0.0 : fabs(hnext) * fabs(ylast) / nrm;
     P.res[sidx] = r * (P.scales_by_value ? P.rv[sidx] : P.res_scale[sidx]);
@@ -362,7 +376,8 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
 }
 
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s) {
-  phi_small_kernel<<<nscales, DT, 0, s>>>(P);
+  const int n = P.m + P.order;
+  phi_small_kernel<<<nscales, DT, sizeof(double) * 2 * n, s>>>(P);
   return cudaGetLastError();
 }
 
