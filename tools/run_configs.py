@@ -68,7 +68,10 @@ def main():
         prm = P.MhdParams(mu=1e-4, eta=1e-4, kappa=1e-3)
         bc = P.default_bc("reconnection")
         y0 = P.reconnection_ic(g, params=prm).reshape(-1)
-        run = dict(kind="adaptive", t_end=a.t_end or 1e9, tol=1e-6, max_steps=a.steps or 50)
+        # the reference has no step-count stop: integrate towards a far t_end with the
+        # max_steps driver extension and an explicit first step
+        run = dict(kind="adaptive", t_end=a.t_end or 1e3, tol=1e-6, max_steps=a.steps or 50,
+                   h_init=a.dt or 0.05)
     elif a.config == 4:
         n = a.n or 4096
         eta = a.eta or 1e-4
@@ -90,7 +93,8 @@ def main():
         if run["kind"] == "fixed":
             return P.integrate_fixed(run["method"], rhs, y, 0.0, run["t_end"], run["dt"],
                                      tol_krylov=run["tol"], cfg=cfg, max_steps=a.steps)
-        return P.integrate_adaptive(rhs, y, 0.0, run["t_end"], P.StepController(tol=run["tol"]),
+        return P.integrate_adaptive(rhs, y, 0.0, run["t_end"],
+                                    P.StepController(tol=run["tol"], h_init=run.get("h_init")),
                                     cfg=cfg, recoverable=(P.AdmissibilityError,),
                                     max_steps=run.get("max_steps"))
 
@@ -124,7 +128,8 @@ def main():
                                          tol=run["tol"], knobs=kn, max_steps=a.steps)
         else:
             yo, so = epirk_cpu.run_adaptive(fo, y0, 0.0, run["t_end"],
-                                            epirk_cpu.Controller(tol=run["tol"]), knobs=kn,
+                                            epirk_cpu.Controller(tol=run["tol"], h_init=run.get("h_init")),
+                                            knobs=kn,
                                             recoverable=(stencil.InadmissibleState,),
                                             max_steps=run.get("max_steps"))
         Tc = time.perf_counter() - t0
