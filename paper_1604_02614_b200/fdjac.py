@@ -51,6 +51,20 @@ class LinearOperator:
         return op
 
 
+def host_rhs(f):
+    """Adapt a NumPy right-hand side ``y -> F(y)`` to device vectors.
+
+    For small user-defined (non-MHD) systems such as the reference's test problems; the
+    user's function itself runs wherever the user wrote it to run.
+    """
+    def g(y):
+        if isinstance(y, torch.Tensor):
+            return D.to_device(np.asarray(f(D.to_host(y)), dtype=float))
+        return f(y)
+    g.__wrapped__ = f
+    return g
+
+
 def unwrap_gpu_rhs(rhs):
     """The fused stencil behind rhs (directly or through a counting wrapper)."""
     seen = 0

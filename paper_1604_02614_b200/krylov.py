@@ -538,7 +538,11 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
         outs = [torch.zeros(n_top, dtype=D.F64, device=D.device()) for _ in scales]
         if _into:
             for (base, coef, out), o in zip(_into, outs):
-                _lincomb(eng.ctx, [base, (coef, o)], out)
+                if base is None:
+                    out.zero_()
+                else:
+                    _lincomb(eng.ctx, [base, (coef, o)], out)   # y_n + a * 0, exact order
+            outs = [t[2] for t in _into]
         return ([D.to_host(o) for o in outs] if host else outs), stats
     c_big = max(scales)
     proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm)
