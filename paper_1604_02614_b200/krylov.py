@@ -31,6 +31,9 @@ from .fdjac import FdJacobianOperator, LinearOperator, _generic_ctx, _lincomb
 from .mhd import raise_status
 
 MAX_COMB_ORDER = 5
+# single-rank fused engines drive each Arnoldi iteration with one C call (emhd_arnoldi_iter);
+# False routes through the per-kernel C entry points (same kernels; used for per-launch timing)
+FAST_DRIVER = True
 BREAKDOWN_RTOL = 1e-12
 
 
@@ -207,7 +210,7 @@ class _Process:
                                          D.ptr(self.beta_dev), self.naug), "div_scalar")
         self._vm_ready = 1
         # single-rank fused engine: one C call per iteration (emhd_arnoldi_iter)
-        self.fast = engine.fused and (layout is None or not layout.distributed)
+        self.fast = FAST_DRIVER and engine.fused and (layout is None or not layout.distributed)
         if self.fast:
             E = engine
             A = N.ArnoldiArgs()

@@ -103,6 +103,8 @@ def main():
         traffic = {}
         for c in caps:
             api = C_API.get(base_name(c["kernel"]))
+            if base_name(c["kernel"]) == "update_kernel" and "<1" in c["kernel"]:
+                api = "emhd_update_finish"      # mode 1 (+ fused column bookkeeping)
             if api and api not in traffic and "dram_read_bytes" in c:
                 traffic[api] = c["dram_read_bytes"] + c["dram_write_bytes"]
         with open(os.path.join(HERE, "traffic.json"), "w") as fh:
