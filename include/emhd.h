@@ -181,6 +181,12 @@ int emhd_admissibility_report(emhd_ctx* ctx, int mode, const double* a, const do
                               const double* v, const double* v_halo, const double* scal,
                               void* report);
 
+/* ---- diagnostics --------------------------------------- */
+/* d = centred div B (mhd.py:288-296), *dmax = max |d| over this rank (device scalar) */
+int emhd_div_b(emhd_ctx* ctx, const double* U, const double* U_halo, double* d, double* dmax);
+/* J = curl B, (3, nx, ny) (mhd.py:299-309) */
+int emhd_current_j(emhd_ctx* ctx, const double* U, const double* U_halo, double* J);
+
 /* ---- single-rank Arnoldi driver ------------------------------------ */
 /* args: a plain struct of device pointers and sizes (layout in paper_1604_02614_b200/_native.py,
  * ArnoldiArgs): a, F(a), V, ldv, H, ldh, w0, w1, d1, d2, nrm, vn, scal, brk, n_top, len_dot,

@@ -494,3 +494,21 @@ extern "C" int emhd_readback(emhd_ctx* c, const double* brk, int nbrk, const dou
   if (rc) return rc;
   return emhd_status_read(c, st);
 }
+
+// div B (mhd.py:288-296): d[nx*ny] and *dmax = max |d| (device scalar, overwritten)
+extern "C" int emhd_div_b(emhd_ctx* c, const double* U, const double* U_halo, double* d, double* dmax) {
+  if (!c || !U || !d || !dmax) return EMHD_ERR_ARG;
+  StencilParams P = c->base;
+  P.a = U; P.a_halo = U_halo;
+  int rc = cerr(cudaMemsetAsync(dmax, 0, sizeof(double), c->stream));
+  if (!rc) rc = cerr(launch_diag(P, 0, d, (unsigned long long*)dmax, c->stream));
+  return rc;
+}
+
+// J = curl B (mhd.py:299-309): J[3][nx][ny]
+extern "C" int emhd_current_j(emhd_ctx* c, const double* U, const double* U_halo, double* J) {
+  if (!c || !U || !J) return EMHD_ERR_ARG;
+  StencilParams P = c->base;
+  P.a = U; P.a_halo = U_halo;
+  return cerr(launch_diag(P, 1, J, nullptr, c->stream));
+}

@@ -589,6 +589,62 @@ __global__ void admissibility_kernel(const StencilParams P, int pass, unsigned l
   }
 }
 
+// ---- diagnostics: div B and J = curl B with one ghost layer (mhd.py:288-309) -------------
+// which = 0: out[nx*ny] = div B, *dmax = max |div B| (bit pattern max of non-negative doubles);
+// which = 1: out[3][nx][ny] = (d_y Bz, -d_x Bz, d_x By - d_y Bx).
+__global__ void diag_kernel(const StencilParams P, int which, double* out, unsigned long long* dmax) {
+  const long long total = (long long)P.nx * P.ny;
+  unsigned long long best = 0ull;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / P.ny), j = (int)(e % P.ny);
+    // x-neighbours (i +- 1, j) and y-neighbours (i, j +- 1), ghosts mapped as apply_ghosts(width=1)
+    const RowRef Rm = row_ref(P, i - 1), Rp = row_ref(P, i + 1), R0 = row_ref(P, i);
+    bool fl, fr;
+    const int jl = map_ghost(j - 1, P.ny, P.bcy, fl), jr = map_ghost(j + 1, P.ny, P.bcy, fr);
+    auto fld = [&](const RowRef& R, int jj, int f) {
+      const double* A = R.halo ? P.a_halo : P.a;
+      return __ldg(A + R.off + jj + (long long)f * R.fs);
+    };
+    double bx_ip = fld(Rp, j, 4), bx_im = fld(Rm, j, 4);
+    if (Rp.flip) bx_ip = -bx_ip;
+    if (Rm.flip) bx_im = -bx_im;
+    double by_jp = fld(R0, jr, 5), by_jm = fld(R0, jl, 5);
+    if (fr) by_jp = -by_jp;
+    if (fl) by_jm = -by_jm;
+    if (which == 0) {
+      const double d = __dadd_rn(div_const(__dsub_rn(bx_ip, bx_im), P.two_hx, P.r_two_hx),
+                                 div_const(__dsub_rn(by_jp, by_jm), P.two_hy, P.r_two_hy));
+      out[e] = d;
+      const unsigned long long key = (unsigned long long)__double_as_longlong(fabs(d));
+      best = key > best ? key : best;
+    } else {
+      const double bz_jp = fld(R0, jr, 6), bz_jm = fld(R0, jl, 6);
+      const double bz_ip = fld(Rp, j, 6), bz_im = fld(Rm, j, 6);
+      const double by_ip = fld(Rp, j, 5), by_im = fld(Rm, j, 5);
+      double bx_jp = fld(R0, jr, 4), bx_jm = fld(R0, jl, 4);
+      out[e] = div_const(__dsub_rn(bz_jp, bz_jm), P.two_hy, P.r_two_hy);
+      out[e + total] = -div_const(__dsub_rn(bz_ip, bz_im), P.two_hx, P.r_two_hx);
+      out[e + 2 * total] = __dsub_rn(div_const(__dsub_rn(by_ip, by_im), P.two_hx, P.r_two_hx),
+                                     div_const(__dsub_rn(bx_jp, bx_jm), P.two_hy, P.r_two_hy));
+    }
+  }
+  if (which == 0) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+      best = ob > best ? ob : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(dmax, best);
+  }
+}
+
+cudaError_t launch_diag(StencilParams P, int which, double* out, unsigned long long* dmax, cudaStream_t s) {
+  const long long total = (long long)P.nx * P.ny;
+  const int G = (int)((total + 255) / 256 < 8192 ? (total + 255) / 256 : 8192);
+  diag_kernel<<<G, 256, 0, s>>>(P, which, out, dmax);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* keys, cudaStream_t s) {
   const long long total = (long long)(P.nx + 4) * (P.ny + 4);
   const int G = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);

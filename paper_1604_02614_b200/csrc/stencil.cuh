@@ -36,6 +36,7 @@ struct StencilParams {
 
 cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s);
 int stencil_tile_width(int ny);
+cudaError_t launch_diag(StencilParams P, int which, double* out, unsigned long long* dmax, cudaStream_t s);
 cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* keys, cudaStream_t s);
 
 }  // namespace emhd

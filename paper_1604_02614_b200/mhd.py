@@ -242,3 +242,42 @@ def local_rows(y_global, grid, layout):
     if isinstance(sl, torch.Tensor):
         return sl.contiguous().reshape(-1)
     return np.ascontiguousarray(sl).reshape(-1)
+
+
+_DIAG = {}
+
+
+def _diag_ctx(grid, bc, layout=None, comm=None):
+    key = (grid, bc, layout)
+    if key not in _DIAG:
+        _DIAG[key] = GpuRhs(MhdParams(), grid, bc, check=False, layout=layout, comm=comm)
+    return _DIAG[key]
+
+
+def div_B(U, grid, bc, layout=None, comm=None):
+    """Centred divergence of the in-plane field and its max |.| (mhd.py:288-296), on the GPU."""
+    host = D.is_host(U)
+    f = _diag_ctx(grid, bc, layout, comm)
+    u = D.to_device(U).reshape(-1)
+    nxl = f.layout.nx_local
+    d = torch.empty(nxl * grid.ny, dtype=D.F64, device=D.device())
+    mx = D.zeros(1)
+    N.check(f.ctx.lib.emhd_div_b(f.ctx.sync_stream(), D.ptr(u), D.ptr(f.halo(u)), D.ptr(d), D.ptr(mx)),
+            "div_b")
+    f.comm.allreduce_max(mx)
+    d = d.view(nxl, grid.ny)
+    peak = float(mx.item())
+    return (D.to_host(d) if host else d), peak
+
+
+def current_J(U, grid, bc, layout=None, comm=None):
+    """Centred current J = curl B, shape (3, nx, ny) (mhd.py:299-309), on the GPU."""
+    host = D.is_host(U)
+    f = _diag_ctx(grid, bc, layout, comm)
+    u = D.to_device(U).reshape(-1)
+    nxl = f.layout.nx_local
+    J = torch.empty(3 * nxl * grid.ny, dtype=D.F64, device=D.device())
+    N.check(f.ctx.lib.emhd_current_j(f.ctx.sync_stream(), D.ptr(u), D.ptr(f.halo(u)), D.ptr(J)),
+            "current_j")
+    J = J.view(3, nxl, grid.ny)
+    return D.to_host(J) if host else J

@@ -77,6 +77,10 @@ def rhs_cases():
         small = v * (0.25 * R.fdjac.SQRT_EPS / np.max(np.abs(v)))   # unscaled branch (sigma = 1)
         cases[f"c{k}_vsmall"] = small
         cases[f"c{k}_Jvsmall"] = op(small)
+        d, peak = Rm.div_B(U, g, bc)                     # diagnostics (mhd.py:288-309)
+        cases[f"c{k}_divB"] = d
+        cases[f"c{k}_divBmax"] = np.array([peak])
+        cases[f"c{k}_J"] = Rm.current_J(U, g, bc)
     cases["ncases"] = np.array([len(specs)])
     np.savez_compressed(os.path.join(OUT, "rhs_jv_cases.npz"), **cases)
 

@@ -379,3 +379,25 @@ def test_fused_arnoldi_raises_admissibility_like_reference(P):
     wk, wc, wv = re.match(pat, str(want.value)).groups()
     assert (gk, gc) == (wk, wc)
     assert abs(float(gv) - float(wv)) <= 1e-6 * abs(float(wv))
+
+
+def test_div_b_and_current_j_bitwise(P):
+    z = golden("rhs_jv_cases.npz")
+    for k in range(int(z["ncases"][0])):
+        g, prm, bc = case_objects(z, k)
+        d, peak = P.div_B(z[f"c{k}_U"], g, bc)
+        assert np.array_equal(d, z[f"c{k}_divB"]), k
+        assert peak == z[f"c{k}_divBmax"][0], k
+        assert np.array_equal(P.current_J(z[f"c{k}_U"], g, bc), z[f"c{k}_J"]), k
+
+
+def test_rhs_preserves_discrete_divergence(P):
+    # reference test_mhd.py:191-201 on the GPU outputs: dB/dt is discretely divergence-free
+    g = P.ReconnectionSpec().grid(32, 16)
+    bc = P.default_bc("reconnection")
+    U = P.reconnection_ic(g)
+    dU = P.make_rhs(P.MhdParams(mu=1e-2, eta=1e-3, kappa=1e-2), g, bc)(U.reshape(-1)).reshape(U.shape)
+    dB = np.zeros_like(U)
+    dB[4:7] = dU[4:7]
+    _, peak = P.div_B(dB, g, bc)
+    assert peak <= 1e-14

@@ -159,3 +159,11 @@ def test_config0_full_trajectory():
     assert np.linalg.norm(y - z["y20"]) <= 1e-9 * np.linalg.norm(z["y20"])
     for k, v in st.items():
         assert getattr(T, k) == v, k
+
+
+def test_divergence_oracle_bitwise():
+    z = golden("rhs_jv_cases.npz")
+    for k in range(int(z["ncases"][0])):
+        g, P, bc = case_objects(z, k)
+        d, peak = stencil.divergence_B(z[f"c{k}_U"], g, bc)
+        assert np.array_equal(d, z[f"c{k}_divB"]) and peak == z[f"c{k}_divBmax"][0]
