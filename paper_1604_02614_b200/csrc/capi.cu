@@ -264,7 +264,7 @@ static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, in
       (!host_scales && (!scales || !res_scale)) || !beta || !Y || !res)
     return EMHD_ERR_ARG;
   const size_t n = (size_t)m + order;
-  const size_t per = 11 * n * n + 3 * n + 64;
+  const size_t per = 11 * n * n + 5 * n + 64;
   const size_t need = per * S;
   if (need > c->dense_len) {
     cudaError_t e = cudaStreamSynchronize(c->stream);

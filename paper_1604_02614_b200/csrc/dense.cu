@@ -193,8 +193,9 @@ __device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac, 
 }
 
 // E = exp(A), A overwritten by scaling; returns false on failure.
+// E = exp(A) (vcol < 0), or only vout = exp(A) e_vcol (vcol >= 0; E then holds a scaled factor)
 __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA, double* sB, double* red,
-                          int* ired, double* prow) {
+                          int* ired, double* prow, int vcol, double* vout) {
   double* A2 = W.m[0];
   double* A4 = W.m[1];
   double* A6 = W.m[2];
@@ -241,10 +242,11 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
     // rescale from the already-applied 2^-s0 to 2^-s (A), then rebuild powers
     const double extra = sc2 / sc;
     for (int e = threadIdx.x; e < n * n; e += DT) A[e] *= extra;
+    // powers of 2^-s A: exact power-of-two rescaling of A^2, A^4, A^6 (bit-identical to
+    // recomputing them from the scaled A, three matrix products cheaper)
+    const double s2 = ldexp(1.0, -2 * s), s4 = ldexp(1.0, -4 * s), s6 = ldexp(1.0, -6 * s);
+    for (int e = threadIdx.x; e < n * n; e += DT) { A2[e] *= s2; A4[e] *= s4; A6[e] *= s6; }
     __syncthreads();
-    mm(A2, A, A, n, sA, sB);
-    mm(A4, A2, A2, n, sA, sB);
-    mm(A6, A4, A2, n, sA, sB);
     mdeg = 13;
   }
   // Pade numerator (V + U) and denominator (V - U)
@@ -299,11 +301,36 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
   if (!gj_solve(M, n, red, ired, fac, prow)) return false;
   for (int e = threadIdx.x; e < n * n; e += DT) E[e] = M[(e / n) * 2 * n + n + e % n];
   __syncthreads();
+  if (vcol >= 0 && s <= 7) {
+    // only the column E^(2^s) e_vcol is needed: 2^s matrix-vector products instead of s
+    // squarings (2^s n^2 vs s n^3 work); result left in vout[0:n]
+    double* xa = vout;
+    double* xb = vout + n;
+    for (int i = threadIdx.x; i < n; i += DT) xa[i] = E[(size_t)i * n + vcol];
+    __syncthreads();
+    for (int k = 1; k < (1 << s); ++k) {
+      for (int i = threadIdx.x; i < n; i += DT) {
+        double acc = 0.0;
+        const double* row = E + (size_t)i * n;
+        for (int c = 0; c < n; ++c) acc = fma(row[c], xa[c], acc);
+        xb[i] = acc;
+      }
+      __syncthreads();
+      double* tmp = xa; xa = xb; xb = tmp;
+    }
+    if (xa != vout)
+      for (int i = threadIdx.x; i < n; i += DT) vout[i] = xa[i];
+    __syncthreads();
+    return true;
+  }
   for (int k = 0; k < s; ++k) {
     mm(T, E, E, n, sA, sB);
     for (int e = threadIdx.x; e < n * n; e += DT) E[e] = T[e];
     __syncthreads();
   }
+  if (vcol >= 0)
+    for (int i = threadIdx.x; i < n; i += DT) vout[i] = E[(size_t)i * n + vcol];
+  __syncthreads();
   return true;
 }
 
@@ -342,10 +369,15 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   bool finite = true;
   for (int e = threadIdx.x; e < m * m; e += DT) if (!isfinite(A[(e / m) * n + e % m])) finite = false;
   finite = __syncthreads_and(finite);
-  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow);
+  double* ycol = W.vec + 3 * n;                    // [2n] column result / ping-pong
+  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol);
   if (ok) {
     bool fin2 = true;
-    for (int e = threadIdx.x; e < n * n; e += DT) if (!isfinite(E[e])) fin2 = false;
+    if (P.E_out) {
+      for (int e = threadIdx.x; e < n * n; e += DT) if (!isfinite(E[e])) fin2 = false;
+    } else {
+      for (int i = threadIdx.x; i < n; i += DT) if (!isfinite(ycol[i])) fin2 = false;
+    }
     ok = __syncthreads_and(fin2);
   }
   if (!ok) {
@@ -357,7 +389,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   }
   double ss = 0.0;
   for (int i = threadIdx.x; i < m; i += DT) {
-    const double yv = E[(size_t)i * n + col] * beta;
+    const double yv = ycol[i] * beta;
     P.Y[(size_t)sidx * m + i] = yv;
     ss += yv * yv;
   }
@@ -368,7 +400,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
     double t = 0.0;
     for (int w = 0; w < DT / 32; ++w) t += red[w];
     const double nrm = sqrt(t);
-    const double ylast = E[(size_t)(m - 1) * n + col] * beta;
+    const double ylast = ycol[m - 1] * beta;
     const double hnext = brk ? 0.0 : hn;
     double r = (nrm == 0.0) ? 0.0 : fabs(hnext) * fabs(ylast) / nrm;
     P.res[sidx] = r * (P.scales_by_value ? P.rv[sidx] : P.res_scale[sidx]);
