@@ -155,6 +155,13 @@ int emhd_phi_small_h(emhd_ctx* ctx, const double* H, long long ldh, int m, int o
                      const double* host_scales, const double* scal, const double* beta, double* Y,
                      double* res);
 
+/* Speculative batch of residual checks on one factorisation: CTA s uses basis size ms[s] (host
+ * int array), scale host_scales[s]; h_{m+1,m} from H (0 when brk_hist[m-1] != 0); Y rows of
+ * stride ldy; res[s] unscaled.  S <= 8. */
+int emhd_phi_small_batch(emhd_ctx* ctx, const double* H, long long ldh, const int* ms, int order, int S,
+                         const double* host_scales, const double* brk_hist, const double* beta,
+                         double* Y, long long ldy, double* res);
+
 /* E = expm(A), n x n row-major device matrices; work: device scratch of n + 4 doubles.
  * Synchronous.  (scipy.linalg.expm as called by phi_dense, phifuncs.py:97,104) */
 int emhd_expm(emhd_ctx* ctx, const double* A, int n, double* E, double* work);

@@ -256,35 +256,22 @@ extern "C" int emhd_div_scalar(emhd_ctx* c, const double* x, const double* d, in
   return cerr(launch_div_scalar(x, d, take_sqrt, out, d_out, n, c->num_sms, c->stream));
 }
 
-static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, int order, int S,
-                          const double* scales, const double* res_scale, const double* scal,
-                          const double* beta, double* Y, double* res, double* E_out,
-                          const double* host_scales = nullptr) {
-  if (!c || !H || m < 1 || order < 0 || order > 4 || S < 1 || S > DENSE_MAX_SCALES ||
-      (!host_scales && (!scales || !res_scale)) || !beta || !Y || !res)
-    return EMHD_ERR_ARG;
-  const size_t n = (size_t)m + order;
+static int ensure_dense(emhd_ctx* c, size_t need) {
+  if (need <= c->dense_len) return EMHD_OK;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cerr(e);
+  cudaFree(c->dense);
+  c->dense = nullptr;
+  c->dense_len = 0;
+  size_t want = need < (size_t)4 * 11 * 256 * 256 ? (size_t)4 * 11 * 256 * 256 + 4096 : need;
+  e = cudaMalloc(&c->dense, want * sizeof(double));
+  if (e != cudaSuccess) return cerr(e);
+  c->dense_len = want;
+  return EMHD_OK;
+}
+
+static void carve_dense(emhd_ctx* c, PhiSmallArgs& P, int S, size_t n) {
   const size_t per = 11 * n * n + 5 * n + 64;
-  const size_t need = per * S;
-  if (need > c->dense_len) {
-    cudaError_t e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) return cerr(e);
-    cudaFree(c->dense);
-    c->dense = nullptr;
-    c->dense_len = 0;
-    size_t want = need < (size_t)4 * 11 * 256 * 256 ? (size_t)4 * 11 * 256 * 256 + 4096 : need;
-    e = cudaMalloc(&c->dense, want * sizeof(double));
-    if (e != cudaSuccess) return cerr(e);
-    c->dense_len = want;
-  }
-  PhiSmallArgs P;
-  std::memset(&P, 0, sizeof(P));
-  P.H = H; P.ldh = ldh; P.m = m; P.order = order; P.scales = scales; P.res_scale = res_scale;
-  P.scal = scal; P.beta = beta; P.Y = Y; P.res = res; P.st = c->st; P.E_out = E_out;
-  if (host_scales) {
-    P.scales_by_value = 1;
-    for (int s = 0; s < S; ++s) { P.sv[s] = host_scales[s]; P.rv[s] = 1.0; }
-  }
   for (int s = 0; s < S; ++s) {
     double* b = c->dense + per * s;
     size_t nn = n * n;
@@ -294,6 +281,55 @@ static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, in
     P.work[s].m[7] = b + 9 * nn;     // n x 2n
     P.work[s].vec = b + 11 * nn;
   }
+}
+
+static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, int order, int S,
+                          const double* scales, const double* res_scale, const double* scal,
+                          const double* beta, double* Y, double* res, double* E_out,
+                          const double* host_scales = nullptr) {
+  if (!c || !H || m < 1 || order < 0 || order > 4 || S < 1 || S > DENSE_MAX_SCALES ||
+      (!host_scales && (!scales || !res_scale)) || !beta || !Y || !res)
+    return EMHD_ERR_ARG;
+  const size_t n = (size_t)m + order;
+  const size_t per = 11 * n * n + 5 * n + 64;
+  int rc = ensure_dense(c, per * S);
+  if (rc) return rc;
+  PhiSmallArgs P;
+  std::memset(&P, 0, sizeof(P));
+  P.H = H; P.ldh = ldh; P.m = m; P.order = order; P.scales = scales; P.res_scale = res_scale;
+  P.scal = scal; P.beta = beta; P.Y = Y; P.res = res; P.st = c->st; P.E_out = E_out;
+  if (host_scales) {
+    P.scales_by_value = 1;
+    for (int s = 0; s < S; ++s) { P.sv[s] = host_scales[s]; P.rv[s] = 1.0; }
+  }
+  carve_dense(c, P, S, n);
+  return cerr(launch_phi_small(P, S, c->stream));
+}
+
+// Speculative residual checks: CTA s evaluates y_s = beta phi_order(scales[s] H_{ms[s]}) e1 and
+// the raw residual |h_{m+1,m}| |y_m| / ||y|| for basis size ms[s] (host arrays), h_{m+1,m} read
+// from H and zeroed by brk_hist[m-1]; Y rows of stride ldy.
+extern "C" int emhd_phi_small_batch(emhd_ctx* c, const double* H, long long ldh, const int* ms, int order,
+                                    int S, const double* host_scales, const double* brk_hist,
+                                    const double* beta, double* Y, long long ldy, double* res) {
+  if (!c || !H || !ms || !host_scales || !brk_hist || !beta || !Y || !res || S < 1 ||
+      S > DENSE_MAX_SCALES || order < 0 || order > 4)
+    return EMHD_ERR_ARG;
+  int mmax = 0;
+  for (int s = 0; s < S; ++s) {
+    if (ms[s] < 1 || ms[s] > ldy) return EMHD_ERR_ARG;
+    mmax = ms[s] > mmax ? ms[s] : mmax;
+  }
+  const size_t n = (size_t)mmax + order;
+  const size_t per = 11 * n * n + 5 * n + 64;
+  int rc = ensure_dense(c, per * S);
+  if (rc) return rc;
+  PhiSmallArgs P;
+  std::memset(&P, 0, sizeof(P));
+  P.H = H; P.ldh = ldh; P.m = mmax; P.order = order; P.beta = beta; P.Y = Y; P.res = res;
+  P.st = c->st; P.batch = 1; P.brk_hist = brk_hist; P.ldy = ldy; P.scales_by_value = 1;
+  for (int s = 0; s < S; ++s) { P.mb[s] = ms[s]; P.sv[s] = host_scales[s]; P.rv[s] = 1.0; }
+  carve_dense(c, P, S, n);
   return cerr(launch_phi_small(P, S, c->stream));
 }
 

@@ -348,14 +348,24 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   // the Expokit form of the reference's ((order+1) m)-dimensional block matrix
   // (phifuncs.py:97-104): same phi to round-off, (order+1)^3 m^3 / (m+order)^3 less work.
   // With E_out (emhd_expm, order 0) the matrix is exactly sc * H.
-  const int m = P.m, n = m + P.order;
+  // batch mode: CTA s checks basis size mb[s] of the same factorisation (speculative
+  // residual checks of several m at once); h_{m+1,m} and the breakdown flag come from H
+  const int m = P.batch ? P.mb[sidx] : P.m, n = m + P.order;
   const int col = (P.order == 0) ? 0 : m + P.order - 1;
   DenseWork W = P.work[sidx];
   double* A = W.a;
   double* E = W.e;
+  double* Yrow = P.Y + (size_t)sidx * (P.batch ? P.ldy : P.m);
   const double sc = P.scales_by_value ? P.sv[sidx] : P.scales[sidx];
-  const double hn = P.scal ? P.scal[0] : 0.0;
-  const bool brk = P.scal ? (P.scal[2] != 0.0) : true;
+  double hn;
+  bool brk;
+  if (P.batch) {
+    brk = P.brk_hist[m - 1] != 0.0;
+    hn = brk ? 0.0 : P.H[(size_t)m * P.ldh + (m - 1)];
+  } else {
+    hn = P.scal ? P.scal[0] : 0.0;
+    brk = P.scal ? (P.scal[2] != 0.0) : true;
+  }
   const double beta = P.beta[0];
   for (int e = threadIdx.x; e < n * n; e += DT) {
     const int r = e / n, c = e % n;
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   double ss = 0.0;
   for (int i = threadIdx.x; i < m; i += DT) {
     const double yv = ycol[i] * beta;
-    P.Y[(size_t)sidx * m + i] = yv;
+    Yrow[i] = yv;
     ss += yv * yv;
   }
   ss = warp_sum(ss);
@@ -408,7 +418,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
 }
 
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s) {
-  const int n = P.m + P.order;
+  const int n = P.m + P.order;              // the largest m of a batch
   phi_small_kernel<<<nscales, DT, sizeof(double) * 2 * n, s>>>(P);
   return cudaGetLastError();
 }

@@ -4,7 +4,7 @@
 
 namespace emhd {
 
-constexpr int DENSE_MAX_SCALES = 4;
+constexpr int DENSE_MAX_SCALES = 8;
 
 struct DenseWork {
   double* a;        // n x n input (scaled in place)
@@ -27,6 +27,10 @@ struct PhiSmallArgs {
   DevStatus* st;
   double* E_out;
   int scales_by_value;       // 1: use sv / rv instead of the device arrays
+  int batch;                // 1: CTA s evaluates basis size mb[s], h_next from H / brk_hist
+  int mb[DENSE_MAX_SCALES];
+  const double* brk_hist;
+  long long ldy;            // row stride of Y in batch mode
   double sv[DENSE_MAX_SCALES];
   double rv[DENSE_MAX_SCALES];            // optional: full n x n exponential of scale_0 * A (S = 1)
 };

@@ -85,6 +85,9 @@ class Ctx:
         self.h = h
         self.max_vectors = int(max_vectors)
         self._stream = None
+        # RHS evaluations the device counted for speculative Arnoldi iterations that were
+        # discarded (the reference never performs them); subtracted from StepStats.rhs_evals
+        self.rhs_discount = 0
 
     def sync_stream(self):
         s = stream_handle()

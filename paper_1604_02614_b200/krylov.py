@@ -31,6 +31,9 @@ from .fdjac import FdJacobianOperator, LinearOperator, _generic_ctx, _lincomb
 from .mhd import raise_status
 
 MAX_COMB_ORDER = 5
+# speculation depth of the batched residual checks (0: automatic from the vector size,
+# 1: off — one residual check per Arnoldi iteration, as the reference orders them)
+SPEC_DEPTH_OVERRIDE = 0
 # single-rank fused engines drive each Arnoldi iteration with one C call (emhd_arnoldi_iter);
 # False routes through the per-kernel C entry points (same kernels; used for per-launch timing)
 FAST_DRIVER = True
@@ -188,7 +191,8 @@ class _Process:
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
         self._settled = 0
         self._pending = False
-        self.Ybuf = torch.empty(4 * (self.m_cap + 1), dtype=D.F64, device=D.device())
+        self._brk_seen = {}
+        self.Ybuf = torch.empty(8 * (self.m_cap + 1), dtype=D.F64, device=D.device())
         self.resbuf = torch.empty(8, dtype=D.F64, device=D.device())
         self.host_rb = torch.zeros(self.m_cap + 16, dtype=D.F64, pin_memory=True)
         self.beta_dev = self.nb[2:3]
@@ -356,9 +360,10 @@ class _Process:
             return True
         return self.settle()
 
-    def settle(self, res_dev=None):
+    def settle(self, res_dev=None, check=True):
         """One host sync: breakdown position, device status of queued iterations and (when
-        given) the residual estimates just computed on the device; returns them."""
+        given) the residual estimates just computed on the device; returns them.  With
+        ``check=False`` the status word is kept in ``self.last_status`` for the caller."""
         self._pending = False
         first = self._settled
         nres = 0 if res_dev is None else res_dev.numel()
@@ -378,6 +383,8 @@ class _Process:
                 self.res_host[:nres].copy_(res_dev, non_blocking=True)
             st = self.ctx.status()                 # synchronises the stream
             flags = self.brk_host[first:self.m].numpy()
+        for k, fv in enumerate(flags):
+            self._brk_seen[first + k] = float(fv)
         hit = np.flatnonzero(flags != 0.0)
         if hit.size:
             b = first + int(hit[0])
@@ -388,6 +395,11 @@ class _Process:
         if self.comm is not None and self.layout.distributed:
             from .mhd import agree_status
             st = agree_status(st, self.comm)
+        self.last_status = st
+        if not check:
+            if res_dev is not None:
+                return self.res_host[:nres].numpy().copy()
+            return not self.breakdown
         if self.eng.fused:
             self.check_status(st)
         if st.flags & N.ST_DENSE:
@@ -456,6 +468,51 @@ class _Process:
                                           D.ptr(scal) if scal is not None else D.ptr(self._brk()),
                                           D.ptr(self.beta_dev), D.ptr(Y), D.ptr(res)), "phi_small")
         return Y, res
+
+    def batch_size(self):
+        """Speculation depth of the residual checks: deep when an iteration is cheap relative
+        to a small dense exponential (small grids), none on very large grids."""
+        if not self.fast or SPEC_DEPTH_OVERRIDE == 1:
+            return 1
+        if SPEC_DEPTH_OVERRIDE:
+            return SPEC_DEPTH_OVERRIDE
+        n = self.n_top
+        return 8 if n <= (1 << 21) else (4 if n <= (1 << 23) else (2 if n <= (1 << 25) else 1))
+
+    def phi_batch(self, order, scale, ms):
+        """Residuals (device) of phi_order(scale H_m) e1 for every m in ms, one launch."""
+        S = len(ms)
+        Y = self.Ybuf[:S * (self.m_cap + 1)].view(S, self.m_cap + 1)
+        res = self.resbuf[:S]
+        N.check(self.lib.emhd_phi_small_batch(self.ctx.sync_stream(), D.ptr(self.H), self.H.shape[1],
+                                              N.int_array(ms), order, S, N.dbl_array([scale] * S),
+                                              D.ptr(self.brk), D.ptr(self.beta_dev), D.ptr(Y),
+                                              self.m_cap + 1, D.ptr(res)), "phi_small_batch")
+        return Y, res
+
+    def truncate(self, m_keep):
+        """Drop speculative iterations beyond m_keep (they were never needed)."""
+        drop = self.m - m_keep
+        if drop <= 0:
+            return
+        self.applies -= drop
+        self.ctx.rhs_discount += drop          # each dropped iteration ran one stencil
+        self.m = m_keep
+        self._settled = min(self._settled, m_keep)
+        self.breakdown = bool(self.brk_host_flag(m_keep - 1))
+
+    def brk_host_flag(self, j):
+        return self._brk_seen.get(j, 0.0) != 0.0
+
+    def resolve_status(self, m_keep):
+        """Raise for device errors of iterations the reference performs (< m_keep); forget
+        the ones raised only by discarded speculative iterations."""
+        st = self.last_status
+        bad = st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE)
+        if bad and st.fail_iter < m_keep and self.eng.fused:
+            self.check_status(st)
+        elif st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE | N.ST_DENSE):
+            self.ctx.reset_status()
 
     def _brk(self):
         if not hasattr(self, "_brk_t"):
@@ -553,19 +610,44 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
     while proc.m < m_target and proc.extend(sync=False):
         pass
     proc.settle()
+    check_current = True
     while True:
-        _, res_raw = proc.phi_coeffs(order, [c_big * h])
-        r = float(proc.settle(res_raw)[0])          # the iteration's only host sync
-        res = r * c_big * h
-        if res <= tol or proc.breakdown or proc.m >= proc.n:
+        # speculative batch: the residual at the current m plus up to B-1 further iterations,
+        # all checked in one phi launch and one host sync; the reference's decision sequence
+        # (stop at the first m with res <= tol, breakdown or m >= n) is replayed on the host
+        B = proc.batch_size()
+        ms = [proc.m] if check_current else []
+        while len(ms) < B and not proc.breakdown and proc.m < proc.m_cap:
+            proc.extend(sync=False)
+            ms.append(proc.m)
+        _, res_raw = proc.phi_batch(order, c_big * h, ms)
+        raw = proc.settle(res_raw, check=False)
+        chosen, res = None, None
+        for k, mk in enumerate(ms):
+            if mk > proc.m:                       # beyond a breakdown found by settle
+                break
+            res = float(raw[k]) * c_big * h
+            if math.isinf(raw[k]):
+                proc.truncate(mk)
+                proc.resolve_status(mk)
+                proc.ctx.reset_status()
+                raise FloatingPointError("overflow in augmented-matrix exponential")
+            if res <= tol or proc.brk_host_flag(mk - 1) or mk >= proc.n:
+                chosen = mk
+                break
+            if mk >= proc.m_cap:                  # extend() would leave m unchanged
+                proc.truncate(mk)
+                proc.resolve_status(mk)
+                stats.operator_applies += proc.applies
+                raise KrylovConvergenceError(
+                    f"Krylov basis cap {cfg.m_max} reached in multi-scale "
+                    f"evaluation (residual {res:.3e} > {tol:.3e})", residual=res)
+        if chosen is not None:
+            proc.truncate(chosen)
+            proc.resolve_status(chosen)
             break
-        m_before = proc.m
-        proc.extend(sync=False)
-        if proc.m == m_before:
-            stats.operator_applies += proc.applies
-            raise KrylovConvergenceError(
-                f"Krylov basis cap {cfg.m_max} reached in multi-scale "
-                f"evaluation (residual {res:.3e} > {tol:.3e})", residual=res)
+        proc.resolve_status(proc.m)
+        check_current = False                     # proc.m was just checked and failed
     stats.operator_applies += proc.applies
     stats.max_basis_size = proc.m
     stats.substeps = 1
