@@ -714,26 +714,56 @@ def phi_comb(req, cfg=None, _zero=None):
         while proc.m < m_target and proc.extend(sync=False):
             pass
         proc.settle()
+        check_current = True
         while True:
-            Y, res_raw = proc.phi_coeffs(0, [delta])
-            r = float(proc.settle(res_raw)[0])      # the iteration's only host sync
-            res = r * delta
+            # speculative batch of residual checks (see multi_scale_eval); extensions stop
+            # where the reference could change delta instead of extending (soft cap)
+            limit = proc.m_cap if delta <= cfg.min_substep else min(cfg.soft_cap, proc.m_cap)
+            B = proc.batch_size()
+            ms = [proc.m] if check_current else []
+            while (len(ms) < B or not ms) and not proc.breakdown and proc.m < limit:
+                proc.extend(sync=False)
+                ms.append(proc.m)
+            if not ms:
+                ms = [proc.m]
+            Yb, res_raw = proc.phi_batch(0, delta, ms)
+            raw = proc.settle(res_raw, check=False)
             tol_sub = req.tol * max(delta, 1e-2)
-            if res <= tol_sub or proc.breakdown or proc.m >= proc.n:
-                break
-            if proc.m >= cfg.soft_cap and delta > cfg.min_substep:
-                delta = delta / 2.0
+            action, res = None, None
+            for k, mk in enumerate(ms):
+                if mk > proc.m:                       # beyond a breakdown found by settle
+                    break
+                if math.isinf(raw[k]):
+                    proc.truncate(mk)
+                    proc.resolve_status(mk)
+                    proc.ctx.reset_status()
+                    raise FloatingPointError("overflow in augmented-matrix exponential")
+                res = float(raw[k]) * delta
+                if res <= tol_sub or proc.brk_host_flag(mk - 1) or mk >= proc.n:
+                    action = ("done", k, mk)
+                elif mk >= cfg.soft_cap and delta > cfg.min_substep:
+                    action = ("halve", k, mk)
+                elif mk >= proc.m_cap:
+                    action = ("cap", k, mk)
+                if action is not None:
+                    break
+            if action is None:
+                proc.resolve_status(proc.m)
+                check_current = False
                 continue
-            m_before = proc.m
-            proc.extend(sync=False)
-            if proc.m == m_before:
-                if delta > cfg.min_substep:
-                    delta = delta / 2.0
-                    continue
+            kind, k, mk = action
+            proc.truncate(mk)
+            proc.resolve_status(mk)
+            if kind == "done":
+                Y = Yb[k:k + 1, :mk].contiguous()
+                break
+            if kind == "cap" and delta <= cfg.min_substep:
                 stats.operator_applies += proc.applies
                 raise KrylovConvergenceError(
                     f"Krylov basis cap {cfg.m_max} reached at substep "
                     f"{delta:.3e} (residual {res:.3e} > {tol_sub:.3e})", residual=res)
+            delta = delta / 2.0                       # soft cap, or hard cap above min_substep
+            check_current = True
         stats.operator_applies += proc.applies
         u_new = torch.empty(n_top, dtype=D.F64, device=D.device())
         proc.combine(Y, [u_new])
