@@ -192,6 +192,7 @@ class _Process:
         self._settled = 0
         self._pending = False
         self._brk_seen = {}
+        self._depth = 2
         self.Ybuf = torch.empty(8 * (self.m_cap + 1), dtype=D.F64, device=D.device())
         self.resbuf = torch.empty(8, dtype=D.F64, device=D.device())
         self.host_rb = torch.zeros(self.m_cap + 16, dtype=D.F64, pin_memory=True)
@@ -470,14 +471,22 @@ class _Process:
         return Y, res
 
     def batch_size(self):
-        """Speculation depth of the residual checks: deep when an iteration is cheap relative
-        to a small dense exponential (small grids), none on very large grids."""
+        """Speculation depth of the next batch of residual checks.
+
+        The cap is deep when an iteration is cheap relative to a small dense exponential
+        (small grids) and 1 on very large grids; within a projection the depth starts at 2
+        and doubles after every failed batch, so a projection that converges right after
+        m_init wastes at most one iteration while a long one needs O(log m) host syncs."""
         if not self.fast or SPEC_DEPTH_OVERRIDE == 1:
             return 1
         if SPEC_DEPTH_OVERRIDE:
-            return SPEC_DEPTH_OVERRIDE
-        n = self.n_top
-        return 8 if n <= (1 << 21) else (4 if n <= (1 << 23) else (2 if n <= (1 << 25) else 1))
+            cap = SPEC_DEPTH_OVERRIDE
+        else:
+            n = self.n_top
+            cap = 8 if n <= (1 << 21) else (4 if n <= (1 << 23) else (2 if n <= (1 << 25) else 1))
+        depth = min(cap, self._depth)
+        self._depth = min(2 * self._depth, 8)
+        return depth
 
     def phi_batch(self, order, scale, ms):
         """Residuals (device) of phi_order(scale H_m) e1 for every m in ms, one launch."""
