@@ -201,6 +201,8 @@ int emhd_current_j(emhd_ctx* ctx, const double* U, const double* U_halo, double*
  * (krylov.py:144-168) — (normalise +) Jv, multi-dot, update + re-dot, update + norms +
  * column bookkeeping — as one stream-ordered call. */
 int emhd_arnoldi_iter(emhd_ctx* ctx, const void* args, int j);
+/* emhd_arnoldi_iter for j = j_begin .. j_end-1 (one call for a burst of iterations) */
+int emhd_arnoldi_run(emhd_ctx* ctx, const void* args, int j_begin, int j_end);
 /* Copy brk[0:nbrk] and res[0:nres] into host_out (pinned), then read the status word: the one
  * host synchronisation of a residual check. */
 int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res, int nres,

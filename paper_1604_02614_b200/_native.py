@@ -73,6 +73,7 @@ _SIGS = {
     "emhd_expm": (c_int, [c_vp, P, c_int, P, P]),
     "emhd_phi_small_h": (c_int, [c_vp, P, c_ll, c_int, c_int, c_int, DP, P, P, P, P]),
     "emhd_arnoldi_iter": (c_int, [c_vp, c_vp, c_int]),
+    "emhd_arnoldi_run": (c_int, [c_vp, c_vp, c_int, c_int]),
     "emhd_phi_small_batch": (c_int, [c_vp, P, c_ll, IP, c_int, c_int, DP, P, P, P, c_ll, P]),
     "emhd_readback": (c_int, [c_vp, P, c_int, P, c_int, P, ctypes.POINTER(Status)]),
     "emhd_combine": (c_int, [c_vp, P, c_ll, c_int, P, c_int, PP, DP, PP, c_ll]),

@@ -548,3 +548,12 @@ extern "C" int emhd_current_j(emhd_ctx* c, const double* U, const double* U_halo
   P.a = U; P.a_halo = U_halo;
   return cerr(launch_diag(P, 1, J, nullptr, c->stream));
 }
+
+// Iterations j_begin .. j_end-1 back to back (the m_init burst / a speculative batch)
+extern "C" int emhd_arnoldi_run(emhd_ctx* c, const void* args, int j_begin, int j_end) {
+  for (int j = j_begin; j < j_end; ++j) {
+    const int rc = emhd_arnoldi_iter(c, args, j);
+    if (rc) return rc;
+  }
+  return EMHD_OK;
+}

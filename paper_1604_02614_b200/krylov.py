@@ -361,6 +361,27 @@ class _Process:
             return True
         return self.settle()
 
+    def extend_many(self, k):
+        """Queue up to k iterations without syncing; one C call on the single-rank fast path."""
+        k = min(k, self.m_cap - self.m)
+        if k <= 0 or self.breakdown:
+            return 0
+        if not self.fast:
+            done = 0
+            while done < k and self.extend(sync=False):
+                done += 1
+            return done
+        j0 = self.m
+        N.check(self.lib.emhd_arnoldi_run(self.ctx.sync_stream(), self._args_ref, j0, j0 + k),
+                "arnoldi_run")
+        self.applies += k
+        self.m = j0 + k
+        self.cur = (self.m - 1) % 2
+        if self.m - 1 > 0:
+            self._vm_ready = self.m
+        self._pending = True
+        return k
+
     def settle(self, res_dev=None, check=True):
         """One host sync: breakdown position, device status of queued iterations and (when
         given) the residual estimates just computed on the device; returns them.  With
@@ -561,8 +582,7 @@ def arnoldi(op, v, m, reorthogonalize=True):
     if m > n_glob:
         raise ValueError(f"basis size {m} exceeds operator dimension {op.n}")
     proc = _Process(eng, vd, m, vd.numel(), 0, layout, comm)
-    while proc.m < m and proc.extend(sync=False):
-        pass
+    proc.extend_many(m)
     proc.settle()
     return proc.basis(host=host)
 
@@ -616,8 +636,7 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
     c_big = max(scales)
     proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm)
     m_target = min(cfg.m_init, proc.n)
-    while proc.m < m_target and proc.extend(sync=False):
-        pass
+    proc.extend_many(m_target)
     proc.settle()
     check_current = True
     while True:
@@ -626,9 +645,9 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
         # (stop at the first m with res <= tol, breakdown or m >= n) is replayed on the host
         B = proc.batch_size()
         ms = [proc.m] if check_current else []
-        while len(ms) < B and not proc.breakdown and proc.m < proc.m_cap:
-            proc.extend(sync=False)
-            ms.append(proc.m)
+        m0 = proc.m
+        proc.extend_many(B - len(ms))
+        ms += list(range(m0 + 1, proc.m + 1))
         _, res_raw = proc.phi_batch(order, c_big * h, ms)
         raw = proc.settle(res_raw, check=False)
         chosen, res = None, None
@@ -720,8 +739,7 @@ def phi_comb(req, cfg=None, _zero=None):
         seed[n_top:n_top + p].copy_(torch.from_numpy(q))
         proc = _Process(eng, seed[:n_top + p], min(cfg.m_max, naug_glob), n_top, p, layout, comm)
         m_target = min(cfg.m_init, naug_glob)
-        while proc.m < m_target and proc.extend(sync=False):
-            pass
+        proc.extend_many(m_target)
         proc.settle()
         check_current = True
         while True:
@@ -730,9 +748,9 @@ def phi_comb(req, cfg=None, _zero=None):
             limit = proc.m_cap if delta <= cfg.min_substep else min(cfg.soft_cap, proc.m_cap)
             B = proc.batch_size()
             ms = [proc.m] if check_current else []
-            while (len(ms) < B or not ms) and not proc.breakdown and proc.m < limit:
-                proc.extend(sync=False)
-                ms.append(proc.m)
+            m0 = proc.m
+            proc.extend_many(min(max(B - len(ms), 0 if ms else 1), limit - proc.m))
+            ms += list(range(m0 + 1, proc.m + 1))
             if not ms:
                 ms = [proc.m]
             Yb, res_raw = proc.phi_batch(0, delta, ms)
