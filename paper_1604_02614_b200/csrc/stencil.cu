@@ -275,11 +275,12 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
   extern __shared__ double smem[];
-  double* qring = smem;                             // [3][NQ][QW]
-  double* gxring = qring + 3 * NQ * QW;             // [3][NF][TY]
-  double* gyring = gxring + 3 * NF * TY;            // [2][NF][GYW]
+  // rings sized so ONE barrier per row step suffices (see the loop): primitives 4 rows,
+  // y-fluxes 3 rows; x-fluxes live in registers of the column's own thread
+  double* qring = smem;                             // [4][NQ][QW]
+  double* gyring = qring + 4 * NQ * QW;             // [3][NF][GYW]
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  double* rawring = gyring + 2 * NF * GYW;          // [2][NARR*NF][QW] raw rows in flight
+  double* rawring = gyring + 3 * NF * GYW;          // [2][NARR*NF][QW] raw rows in flight
 
   const int t = threadIdx.x;
   const int j0 = blockIdx.x * TY;
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
     // prologue: primitives of rows i0-2 and i0-1
     for (int r = i0 - 2; r < i0; ++r) {
       const RowRef R = row_ref(P, r);
-      double* q = qring + ((r + 3) % 3) * NQ * QW;
+      double* q = qring + ((r + 4) % 4) * NQ * QW;
       double u[NF];
       if (okm) {
         load_cell<MODE>(P, R, jm, fm, sigma, hnext, rh, u);
@@ -386,6 +387,9 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
       for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o + (long long)f * P.nx * P.ny);
     }
     constexpr int SLOT = NARR * NF * QW;
+    double gxA[NF], gxB[NF], gxC[NF];        // x-fluxes of rows r-3, r-2, r-1 (own column)
+#pragma unroll
+    for (int f = 0; f < NF; ++f) { gxA[f] = 0.0; gxB[f] = 0.0; gxC[f] = 0.0; }
     for (int k = 0; k < 2; ++k) {
       const int rr = i0 + k;
       if (rr <= i1 + 1) {
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
       // ---- primitives of row r
       {
         const RowRef Rr = row_ref(P, r);
-        double* q = qring + ((r + 3) % 3) * NQ * QW;
+        double* q = qring + ((r + 4) % 4) * NQ * QW;
         double u[NF];
         if (okm) {
           RawCell<MODE> xm;
@@ -432,21 +436,23 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
         if (oke) fetch_async<MODE, QW>(P, R2, je, cextra, sraw);
       }
       cp_commit();
+      // The only barrier of the step.  RAW: fluxes of row r-1 read primitives of row r
+      // (just written) and outputs of row r-2 read y-fluxes of row r-2 (previous step).
+      // WAR is covered by ring depth: primitives of row r+1 overwrite row r-3 (last read by
+      // the fluxes of row r-2, previous step); y-fluxes of row r overwrite row r-3 (last
+      // read by the outputs of row r-3, previous step).
       __syncthreads();
       // ---- fluxes of row rf = r - 1
       const int rf = r - 1;
       if (rf >= i0 - 1) {
-        const double* qm = qring + ((rf + 2) % 3) * NQ * QW;
-        const double* q0 = qring + ((rf + 3) % 3) * NQ * QW;
-        const double* qp = qring + ((rf + 4) % 3) * NQ * QW;
-        double* gxr = gxring + ((rf + 3) % 3) * NF * TY;
-        double* gyr = gyring + ((rf + 2) % 2) * NF * GYW;
+        const double* qm = qring + ((rf + 3) % 4) * NQ * QW;
+        const double* q0 = qring + ((rf + 4) % 4) * NQ * QW;
+        const double* qp = qring + ((rf + 5) % 4) * NQ * QW;
+        double* gyr = gyring + ((rf + 3) % 3) * NF * GYW;
         const bool out_row = (rf >= i0 && rf < i1);
-        double gx[NF], gy[NF];
+        double gy[NF];
         if (t < ncols_out) {
-          flux_cell<FXY>(P, qm, q0, qp, cmain, QW, true, out_row, gx, gy);
-#pragma unroll
-          for (int f = 0; f < NF; ++f) gxr[f * TY + t] = gx[f];
+          flux_cell<FXY>(P, qm, q0, qp, cmain, QW, true, out_row, gxC, gy);
           if (out_row) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) gyr[f * GYW + t + 1] = gy[f];
@@ -458,23 +464,22 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
           if (t == 0) { cs = 1; gslot = 0; }
           if (t == TY - 1) { cs = ncols_out + 2; gslot = ncols_out + 1; }
           if (cs >= 0) {
-            flux_cell<FXY>(P, qm, q0, qp, cs, QW, false, true, gx, gy);
+            double gdummy[NF];
+            flux_cell<FXY>(P, qm, q0, qp, cs, QW, false, true, gdummy, gy);
 #pragma unroll
             for (int f = 0; f < NF; ++f) gyr[f * GYW + gslot] = gy[f];
           }
         }
       }
-      __syncthreads();
-      // ---- output row ro = r - 2
+      // ---- output row ro = r - 2: x-fluxes of rows ro+1 (gxC) and ro-1 (gxA) are this
+      // thread's own registers; y-fluxes of row ro come from the ring (previous step)
       const int ro = r - 2;
       if (ro >= i0 && t < ncols_out) {
-        const double* gxp = gxring + ((ro + 4) % 3) * NF * TY;
-        const double* gxm = gxring + ((ro + 2) % 3) * NF * TY;
-        const double* gyr = gyring + ((ro + 2) % 2) * NF * GYW;
+        const double* gyr = gyring + ((ro + 3) % 3) * NF * GYW;
         const long long o = (long long)ro * P.ny + j0 + t;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-          const double ddx = div_c<FXY>(__dsub_rn(gxp[f * TY + t], gxm[f * TY + t]), P.two_hx, P.r_two_hx);
+          const double ddx = div_c<FXY>(__dsub_rn(gxC[f], gxA[f]), P.two_hx, P.r_two_hx);
           const double ddy = div_c<FXY>(__dsub_rn(gyr[f * GYW + t + 2], gyr[f * GYW + t]), P.two_hy, P.r_two_hy);
           double F = __dsub_rn(-ddx, ddy);                    // -ddx(gx) - ddy(gy) (mhd.py:277)
           const long long idx = o + (long long)f * P.nx * P.ny;
@@ -502,6 +507,8 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
           for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o2 + (long long)f * P.nx * P.ny);
         }
       }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) { gxA[f] = gxB[f]; gxB[f] = gxC[f]; }
     }
   }
 
@@ -660,7 +667,7 @@ template <int TY, int MODE, bool AUG, bool FXY>
 static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  const size_t sm = sizeof(double) * (3 * NQ * QW + 3 * NF * TY + 2 * NF * GYW + 2 * NARR * NF * QW);
+  const size_t sm = sizeof(double) * (4 * NQ * QW + 3 * NF * GYW + 2 * NARR * NF * QW);
   auto k = stencil_kernel<TY, MODE, AUG, FXY>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
@@ -670,7 +677,8 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, TY, sm);
     const int strips = (P.ny + TY - 1) / TY;
     const int target = (occ < 1 ? 1 : occ) * num_sms;
-    const int chunks = (target + strips - 1) / strips;
+    // floor: strips x chunks must not exceed one wave of resident CTAs
+    const int chunks = target / strips > 0 ? target / strips : 1;
     const int rows = (P.nx + chunks - 1) / chunks;
     static int min_rows = -1;
     if (min_rows < 0) {
