@@ -120,6 +120,18 @@ def _ld(n):
     return (n + 31) // 32 * 32
 
 
+def _persistent_basis(ctx, rows, ld):
+    """A (rows, ld) view of the context's reusable Krylov basis buffer (grown on demand)."""
+    buf = getattr(ctx, "_basis", None)
+    need = rows * ld
+    if buf is None or buf.numel() < need:
+        ctx._basis = None
+        del buf
+        torch.cuda.empty_cache()
+        ctx._basis = torch.empty(need, dtype=D.F64, device=D.device())
+    return ctx._basis[:need].view(rows, ld)
+
+
 class _Engine:
     """How one Arnoldi iteration obtains w = A v_j."""
 
@@ -153,7 +165,7 @@ class _Generic(_Engine):
 class _Process:
     """Device Arnoldi factorisation (reference _ArnoldiProcess, krylov.py:127-188)."""
 
-    def __init__(self, engine, seed, m_cap, n_top, p=0, layout=None, comm=None):
+    def __init__(self, engine, seed, m_cap, n_top, p=0, layout=None, comm=None, persistent=False):
         self.eng = engine
         self.ctx = engine.ctx
         self.lib = self.ctx.lib
@@ -169,9 +181,16 @@ class _Process:
         self.m_cap = min(m_cap, self.n)
         if self.m_cap + 1 > self.ctx.max_vectors - 4:
             raise ValueError(f"basis cap {self.m_cap} exceeds the context limit")
-        self.ld = _ld(self.naug)
-        # V and w are never read beyond their written lengths: no zero-fill of 2.7 GB
-        self.V = torch.empty((self.m_cap + 1, self.ld), dtype=D.F64, device=D.device())
+        # V and w are never read beyond their written lengths: no zero-fill of 2.7 GB.
+        # Projections inside a step (multi-scale, phi-comb) share one persistent basis per
+        # context, sized for any tail p <= 5, so a 129 GiB basis (4096^2, m_max 128) is
+        # allocated once instead of once per projection.
+        if persistent:
+            self.ld = _ld(n_top + MAX_COMB_ORDER)
+            self.V = _persistent_basis(self.ctx, self.m_cap + 1, self.ld)
+        else:
+            self.ld = _ld(self.naug)
+            self.V = torch.empty((self.m_cap + 1, self.ld), dtype=D.F64, device=D.device())
         self.w = [torch.empty(self.ld, dtype=D.F64, device=D.device()) for _ in range(2)]
         k = self.m_cap + 4
         hw = max(self.m_cap, 1)
@@ -634,7 +653,7 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
             outs = [t[2] for t in _into]
         return ([D.to_host(o) for o in outs] if host else outs), stats
     c_big = max(scales)
-    proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm)
+    proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm, persistent=True)
     m_target = min(cfg.m_init, proc.n)
     proc.extend_many(m_target)
     proc.settle()
@@ -737,7 +756,8 @@ def phi_comb(req, cfg=None, _zero=None):
         q = np.array([t ** (p - 1 - i) / math.factorial(p - 1 - i) for i in range(p)])
         seed[:n_top].copy_(u)
         seed[n_top:n_top + p].copy_(torch.from_numpy(q))
-        proc = _Process(eng, seed[:n_top + p], min(cfg.m_max, naug_glob), n_top, p, layout, comm)
+        proc = _Process(eng, seed[:n_top + p], min(cfg.m_max, naug_glob), n_top, p, layout, comm,
+                        persistent=True)
         m_target = min(cfg.m_init, naug_glob)
         proc.extend_many(m_target)
         proc.settle()
