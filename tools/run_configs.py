@@ -115,6 +115,7 @@ def main():
         import pstats
         pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(25)
     out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
+           "speculative_discarded_total": f.ctx.rhs_discount,
            "iterations_per_s": st.operator_applies / T,
            "cell_steps_per_s": g.nx * g.ny * st.steps_accepted / T}
     if a.check:
