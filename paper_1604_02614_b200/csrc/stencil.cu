@@ -16,6 +16,7 @@
 // identical bits), the derivatives of a flux cell are shared by its x- and
 // y-flux, and halo recomputation only happens at strip edges (4 columns) and
 // chunk edges (4 rows).
+#include <cstdint>
 #include <cstdlib>
 #include "emhd_common.cuh"
 #include "stencil.cuh"
@@ -135,6 +136,54 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// --- bulk async copies (TMA engine, cp.async.bulk) tracked by an mbarrier ----------
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred done;\n"
+      "MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra MBAR_WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, unsigned bytes,
+                                              unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+
+// one raw row of an interior strip (columns j0-2 .. j0+TY+1, all inside the grid): 8 or 16
+// contiguous row segments, issued by one thread; completion lands on the slot's mbarrier
+template <int MODE, int QW>
+__device__ __forceinline__ void fetch_row_bulk(const StencilParams& P, const RowRef& R, int jfirst,
+                                               double* slot, unsigned long long* bar) {
+  constexpr int NA = MODE == MODE_RHS ? 1 : 2;
+  constexpr unsigned SEG = QW * sizeof(double);
+  mbar_expect_tx(bar, NA * NF * SEG);
+  const double* A = R.halo ? P.a_halo : P.a;
+  const long long o = R.off + jfirst;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) bulk_copy_g2s(slot + f * QW, A + o + f * R.fs, SEG, bar);
+  if (NA == 2) {
+    const double* Vv = R.halo ? P.v_halo : P.v;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) bulk_copy_g2s(slot + (NF + f) * QW, Vv + o + f * R.fs, SEG, bar);
+  }
+}
 
 // raw ring layout: [slot][array (a, v)][field][column slot]
 template <int MODE, int QW>
@@ -281,6 +330,7 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
   double* gyring = qring + 4 * NQ * QW;             // [3][NF][GYW]
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
   double* rawring = gyring + 3 * NF * GYW;          // [2][NARR*NF][QW] raw rows in flight
+  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + 2 * NARR * NF * QW);
 
   const int t = threadIdx.x;
   const int j0 = blockIdx.x * TY;
@@ -390,19 +440,35 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
     double gxA[NF], gxB[NF], gxC[NF];        // x-fluxes of rows r-3, r-2, r-1 (own column)
 #pragma unroll
     for (int f = 0; f < NF; ++f) { gxA[f] = 0.0; gxB[f] = 0.0; gxC[f] = 0.0; }
-    for (int k = 0; k < 2; ++k) {
-      const int rr = i0 + k;
-      if (rr <= i1 + 1) {
-        const RowRef R = row_ref(P, rr);
-        if (okm) fetch_async<MODE, QW>(P, R, jm, cmain, rawring + k * SLOT);
-        if (oke) fetch_async<MODE, QW>(P, R, je, cextra, rawring + k * SLOT);
+    // interior strips (no y-ghost columns) stream whole row segments with bulk async copies
+    // issued by thread 0 (one mbarrier per slot); edge strips keep per-thread cp.async
+    const bool bulk = P.tma && j0 >= 2 && j0 + TY + 2 <= P.ny;
+    if (bulk) {
+      if (t == 0) {
+        mbar_init(rbar, 1);
+        mbar_init(rbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (int k = 0; k < 2; ++k)
+          if (i0 + k <= i1 + 1)
+            fetch_row_bulk<MODE, QW>(P, row_ref(P, i0 + k), j0 - 2, rawring + k * SLOT, rbar + k);
       }
-      cp_commit();
+      __syncthreads();
+    } else {
+      for (int k = 0; k < 2; ++k) {
+        const int rr = i0 + k;
+        if (rr <= i1 + 1) {
+          const RowRef R = row_ref(P, rr);
+          if (okm) fetch_async<MODE, QW>(P, R, jm, cmain, rawring + k * SLOT);
+          if (oke) fetch_async<MODE, QW>(P, R, je, cextra, rawring + k * SLOT);
+        }
+        cp_commit();
+      }
     }
     for (int r = i0; r <= i1 + 1; ++r) {
       const int slot = (r - i0) & 1;
       double* sraw = rawring + slot * SLOT;
-      cp_wait<1>();                          // row r has landed (row r+1 may still be in flight)
+      if (bulk) mbar_wait(rbar + slot, ((r - i0) >> 1) & 1);
+      else cp_wait<1>();                     // row r has landed (row r+1 may still be in flight)
       // ---- primitives of row r
       {
         const RowRef Rr = row_ref(P, r);
@@ -429,19 +495,27 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
           cell_prims(P, u, q + cextra, QW, flag);
         }
       }
-      // refill the consumed slot with row r+2
-      if (r + 2 <= i1 + 1) {
-        const RowRef R2 = row_ref(P, r + 2);
-        if (okm) fetch_async<MODE, QW>(P, R2, jm, cmain, sraw);
-        if (oke) fetch_async<MODE, QW>(P, R2, je, cextra, sraw);
+      // refill the consumed slot with row r+2 (each thread its own cells; the bulk path
+      // refills after the barrier below, once every thread has consumed the slot)
+      if (!bulk) {
+        if (r + 2 <= i1 + 1) {
+          const RowRef R2 = row_ref(P, r + 2);
+          if (okm) fetch_async<MODE, QW>(P, R2, jm, cmain, sraw);
+          if (oke) fetch_async<MODE, QW>(P, R2, je, cextra, sraw);
+        }
+        cp_commit();
       }
-      cp_commit();
       // The only barrier of the step.  RAW: fluxes of row r-1 read primitives of row r
       // (just written) and outputs of row r-2 read y-fluxes of row r-2 (previous step).
       // WAR is covered by ring depth: primitives of row r+1 overwrite row r-3 (last read by
       // the fluxes of row r-2, previous step); y-fluxes of row r overwrite row r-3 (last
       // read by the outputs of row r-3, previous step).
       __syncthreads();
+      if (bulk && t == 0 && r + 2 <= i1 + 1) {
+        // generic-proxy reads of the slot (before the barrier) precede the async-proxy refill
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        fetch_row_bulk<MODE, QW>(P, row_ref(P, r + 2), j0 - 2, sraw, rbar + slot);
+      }
       // ---- fluxes of row rf = r - 1
       const int rf = r - 1;
       if (rf >= i0 - 1) {
@@ -667,8 +741,20 @@ template <int TY, int MODE, bool AUG, bool FXY>
 static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  const size_t sm = sizeof(double) * (4 * NQ * QW + 3 * NF * GYW + 2 * NARR * NF * QW);
+  const size_t sm = sizeof(double) * (4 * NQ * QW + 3 * NF * GYW + 2 * NARR * NF * QW) +
+                    2 * sizeof(unsigned long long);
   auto k = stencil_kernel<TY, MODE, AUG, FXY>;
+  {
+    // bulk copies need 16-byte aligned sources and sizes: even ny and aligned buffers
+    static int use_tma = -1;
+    if (use_tma < 0) {
+      const char* env = getenv("EMHD_STENCIL_TMA");
+      use_tma = env ? atoi(env) != 0 : 1;
+    }
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    P.tma = use_tma && (P.ny % 2 == 0) && al(P.a) && al(P.a_halo) &&
+            (MODE == MODE_RHS || (al(P.v) && al(P.v_halo)));
+  }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   if (P.rows_per_cta <= 0) {

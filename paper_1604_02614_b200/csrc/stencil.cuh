@@ -32,6 +32,7 @@ struct StencilParams {
   const double* qsrc;         // MODE_JV + tail: q (device, length p)
   DevStatus* st;
   int epoch;                  // caller-defined launch tag recorded on failure
+  int tma;                    // interior strips stage raw rows with bulk async copies (set by the launcher)
 };
 
 cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s);
