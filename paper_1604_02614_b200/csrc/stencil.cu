@@ -23,8 +23,10 @@
 
 namespace emhd {
 
-// primitive slots kept per cell in shared memory
-enum : int { Q_RHO = 0, Q_MX, Q_MY, Q_EN, Q_B0, Q_B1, Q_B2, Q_V0, Q_V1, Q_V2, Q_T, Q_PT, NQ };
+// primitives differentiated across rows/columns: shared by the CTA in the primitive ring
+enum : int { Q_V0 = 0, Q_V1, Q_V2, Q_B0, Q_B1, Q_B2, Q_T, NQ };
+// cell-centre-only quantities: written and read by the cell's own thread (no barrier)
+enum : int { C_RHO = 0, C_MX, C_MY, C_EN, C_PT, NC };
 
 struct RowRef {
   long long off;     // element offset of (field 0, row, col 0) in the chosen buffer
@@ -213,7 +215,7 @@ __device__ __forceinline__ void consume_raw(const double* slot, int c, RawCell<M
 
 // pressure / admissibility / primitives (mhd.py:106-131, 176-181, 217-221)
 __device__ __forceinline__ void cell_prims(const StencilParams& P, const double u[NF],
-                                           double* q, int qs, int& flag) {
+                                           double* q, double* cq, int qs, int& flag) {
   const double rho = u[0], mx = u[1], my = u[2], mz = u[3];
   const double b0 = u[4], b1 = u[5], b2 = u[6], en = u[7];
   if (P.check && rho <= 0.0) flag |= ST_RHO;
@@ -224,10 +226,10 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
   const double mag = __dmul_rn(P.bfac, bb);
   const double p = __dmul_rn(P.gm1, __dsub_rn(__dsub_rn(en, kin), mag));
   if (P.check && p <= 0.0) flag |= ST_PRESSURE;
-  q[Q_RHO * qs] = rho;
-  q[Q_MX * qs] = mx;
-  q[Q_MY * qs] = my;
-  q[Q_EN * qs] = en;
+  cq[C_RHO * qs] = rho;
+  cq[C_MX * qs] = mx;
+  cq[C_MY * qs] = my;
+  cq[C_EN * qs] = en;
   q[Q_B0 * qs] = b0;
   q[Q_B1 * qs] = b1;
   q[Q_B2 * qs] = b2;
@@ -235,14 +237,15 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
   q[Q_V1 * qs] = div_const(my, rho, rr);
   q[Q_V2 * qs] = div_const(mz, rho, rr);
   q[Q_T * qs] = div_const(p, rho, rr);
-  q[Q_PT * qs] = __dadd_rn(p, __dmul_rn(0.5, bb));
+  cq[C_PT * qs] = __dadd_rn(p, __dmul_rn(0.5, bb));
 }
 
 // x- and y-flux G = F_hyp - F_diff at one cell (mhd.py:174-197, 209-266, 275-276).
-// c: prim column slot of the cell; qm/q0/qp: prim rows i-1, i, i+1.
+// c: prim column slot of the cell; qm/q0/qp: prim rows i-1, i, i+1; c0: centre row i.
 template <bool FXY>
 __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* qm,
-                                          const double* q0, const double* qp, int c, int qs,
+                                          const double* q0, const double* qp, const double* c0,
+                                          int c, int qs,
                                           bool need_x, bool need_y, double gx[NF], double gy[NF]) {
 #define QV(row, k, col) row[(k) * qs + (col)]
   const double thx = P.two_hx, rhx = P.r_two_hx, thy = P.two_hy, rhy = P.r_two_hy;
@@ -254,7 +257,7 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
   const double dBx1 = div_c<FXY>(__dsub_rn(QV(qp, Q_B1, c), QV(qm, Q_B1, c)), thx, rhx);
   const double dBy0 = div_c<FXY>(__dsub_rn(QV(q0, Q_B0, c + 1), QV(q0, Q_B0, c - 1)), thy, rhy);
 
-  const double rho = QV(q0, Q_RHO, c), en = QV(q0, Q_EN, c), pt = QV(q0, Q_PT, c);
+  const double rho = QV(c0, C_RHO, c), en = QV(c0, C_EN, c), pt = QV(c0, C_PT, c);
   const double v0 = QV(q0, Q_V0, c), v1 = QV(q0, Q_V1, c), v2 = QV(q0, Q_V2, c);
   const double b0 = QV(q0, Q_B0, c), b1 = QV(q0, Q_B1, c), b2 = QV(q0, Q_B2, c);
   const double mu = P.mu, eta = P.eta, heat = P.heat;
@@ -283,7 +286,7 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
     const double res = __dmul_rn(eta, __dadd_rn(__dmul_rn(b1, curl), __dmul_rn(b2, dBx2)));
     const double fen = __dadd_rn(__dadd_rn(visc, __dmul_rn(heat, dTx)), res);
     // hyperbolic x-flux (mhd.py:185-196) minus diffusive
-    gx[0] = QV(q0, Q_MX, c);
+    gx[0] = QV(c0, C_MX, c);
     gx[1] = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(r0, v0), __dmul_rn(b0, b0)), pt), fmx);
     gx[2] = __dsub_rn(__dsub_rn(__dmul_rn(r1, v0), __dmul_rn(b1, b0)), fmy);
     gx[3] = __dsub_rn(__dsub_rn(__dmul_rn(r2, v0), __dmul_rn(b2, b0)), fmz);
@@ -307,7 +310,7 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
                                                 __dmul_rn(dvy2, v2)));
     const double res = __dmul_rn(eta, __dadd_rn(__dmul_rn(b0, __dsub_rn(dBy0, dBx1)), __dmul_rn(b2, dBy2)));
     const double fen = __dadd_rn(__dadd_rn(visc, __dmul_rn(heat, dTy)), res);
-    gy[0] = QV(q0, Q_MY, c);
+    gy[0] = QV(c0, C_MY, c);
     gy[1] = __dsub_rn(__dsub_rn(__dmul_rn(r0, v1), __dmul_rn(b0, b1)), fmx);
     gy[2] = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(r1, v1), __dmul_rn(b1, b1)), pt), fmy);
     gy[3] = __dsub_rn(__dsub_rn(__dmul_rn(r2, v1), __dmul_rn(b2, b1)), fmz);
@@ -320,17 +323,19 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
 }
 
 template <int TY, int MODE, bool AUG, bool FXY>
-__global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
+__global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilParams P) {
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
   extern __shared__ double smem[];
   // rings sized so ONE barrier per row step suffices (see the loop): primitives 4 rows,
-  // y-fluxes 3 rows; x-fluxes live in registers of the column's own thread
+  // y-fluxes 2 rows, thread-private centre quantities 2 rows, one raw row in flight;
+  // x-fluxes live in registers of the column's own thread.  ~72 KB at TY=128: 3 CTAs/SM
   double* qring = smem;                             // [4][NQ][QW]
-  double* gyring = qring + 4 * NQ * QW;             // [3][NF][GYW]
+  double* gyring = qring + 4 * NQ * QW;             // [2][NF][GYW]
+  double* cring = gyring + 2 * NF * GYW;            // [2][NC][QW]
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  double* rawring = gyring + 3 * NF * GYW;          // [2][NARR*NF][QW] raw rows in flight
-  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + 2 * NARR * NF * QW);
+  double* rawring = cring + 2 * NC * QW;            // [NARR*NF][QW] raw row in flight
+  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NARR * NF * QW);
 
   const int t = threadIdx.x;
   const int j0 = blockIdx.x * TY;
@@ -403,10 +408,11 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
       }
     }
   } else {
-    // column slots handled by this thread: main slot c = t + 2 (column j0 + t),
-    // extra halo slots 0,1 (threads 0,1) and TY+2, TY+3 (threads TY-2, TY-1)
+    // column slots handled by this thread: main slot c = t + 2 (column j0 + t), extra
+    // halo slots 1,0 (threads 0,1) and TY+3, TY+2 (threads TY-2, TY-1): the threads that
+    // compute the halo y-fluxes (slots 1 and TY+2) own those columns' centre quantities
     const int cmain = t + 2;
-    const int cextra = (t < 2) ? t : ((t >= TY - 2) ? t + 4 : -1);
+    const int cextra = t == 0 ? 1 : t == 1 ? 0 : t == TY - 2 ? TY + 3 : t == TY - 1 ? TY + 2 : -1;
     auto col_ok = [&](int c) { int j = j0 - 2 + c; return j >= -2 && j <= P.ny + 1; };
     bool fm, fe;
     const int jm = map_ghost(j0 - 2 + cmain, P.ny, P.bcy, fm);
@@ -417,68 +423,60 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
     for (int r = i0 - 2; r < i0; ++r) {
       const RowRef R = row_ref(P, r);
       double* q = qring + ((r + 4) % 4) * NQ * QW;
+      double* cq = cring + ((r + 2) % 2) * NC * QW;
       double u[NF];
       if (okm) {
         load_cell<MODE>(P, R, jm, fm, sigma, hnext, rh, u);
-        cell_prims(P, u, q + cmain, QW, flag);
+        cell_prims(P, u, q + cmain, cq + cmain, QW, flag);
       }
       if (oke) {
         load_cell<MODE>(P, R, je, fe, sigma, hnext, rh, u);
-        cell_prims(P, u, q + cextra, QW, flag);
+        cell_prims(P, u, q + cextra, cq + cextra, QW, flag);
       }
     }
-    // software pipeline: raw inputs of rows r+1 and r+2 stream into a 2-slot shared
-    // ring by cp.async while the fluxes of row r-1 and outputs of row r-2 are computed;
-    // every thread consumes only the cells it copied itself, so no barrier guards the ring
+    // software pipeline: the raw inputs of row r+1 stream into the shared raw row while the
+    // fluxes of row r-1 and outputs of row r-2 are computed
     double fa_pre[NF];                       // F(a) of the next output row, one step ahead
     if (MODE != MODE_RHS && t < ncols_out) {
       const long long o = (long long)i0 * P.ny + j0 + t;
 #pragma unroll
       for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o + (long long)f * P.nx * P.ny);
     }
-    constexpr int SLOT = NARR * NF * QW;
     double gxA[NF], gxB[NF], gxC[NF];        // x-fluxes of rows r-3, r-2, r-1 (own column)
 #pragma unroll
     for (int f = 0; f < NF; ++f) { gxA[f] = 0.0; gxB[f] = 0.0; gxC[f] = 0.0; }
     // interior strips (no y-ghost columns) stream whole row segments with bulk async copies
-    // issued by thread 0 (one mbarrier per slot); edge strips keep per-thread cp.async
+    // issued by thread 0 (tracked by one mbarrier); edge strips keep per-thread cp.async
     const bool bulk = P.tma && j0 >= 2 && j0 + TY + 2 <= P.ny;
     if (bulk) {
       if (t == 0) {
         mbar_init(rbar, 1);
-        mbar_init(rbar + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        for (int k = 0; k < 2; ++k)
-          if (i0 + k <= i1 + 1)
-            fetch_row_bulk<MODE, QW>(P, row_ref(P, i0 + k), j0 - 2, rawring + k * SLOT, rbar + k);
+        fetch_row_bulk<MODE, QW>(P, row_ref(P, i0), j0 - 2, rawring, rbar);
       }
       __syncthreads();
     } else {
-      for (int k = 0; k < 2; ++k) {
-        const int rr = i0 + k;
-        if (rr <= i1 + 1) {
-          const RowRef R = row_ref(P, rr);
-          if (okm) fetch_async<MODE, QW>(P, R, jm, cmain, rawring + k * SLOT);
-          if (oke) fetch_async<MODE, QW>(P, R, je, cextra, rawring + k * SLOT);
-        }
-        cp_commit();
-      }
+      // per-thread cp.async: every thread consumes only the cells it copied itself
+      const RowRef R = row_ref(P, i0);
+      if (okm) fetch_async<MODE, QW>(P, R, jm, cmain, rawring);
+      if (oke) fetch_async<MODE, QW>(P, R, je, cextra, rawring);
+      cp_commit();
     }
     for (int r = i0; r <= i1 + 1; ++r) {
-      const int slot = (r - i0) & 1;
-      double* sraw = rawring + slot * SLOT;
-      if (bulk) mbar_wait(rbar + slot, ((r - i0) >> 1) & 1);
-      else cp_wait<1>();                     // row r has landed (row r+1 may still be in flight)
+      double* sraw = rawring;
+      if (bulk) mbar_wait(rbar, (r - i0) & 1);
+      else cp_wait<0>();                     // row r has landed
       // ---- primitives of row r
       {
         const RowRef Rr = row_ref(P, r);
         double* q = qring + ((r + 4) % 4) * NQ * QW;
+        double* cq = cring + ((r + 2) % 2) * NC * QW;
         double u[NF];
         if (okm) {
           RawCell<MODE> xm;
           consume_raw<MODE, QW>(sraw, cmain, xm);
           combine_cell<MODE>(xm, Rr.flip, fm, sigma, hnext, rh, fh, u);
-          cell_prims(P, u, q + cmain, QW, flag);
+          cell_prims(P, u, q + cmain, cq + cmain, QW, flag);
           if (MODE == MODE_JVN && r >= i0 && r < i1 && t < ncols_out) {
             // v_j = w / h_next of an owned cell (krylov.py:167), from the fetched w
             const long long o = (long long)r * P.ny + j0 + t;
@@ -492,29 +490,30 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
           RawCell<MODE> xe;
           consume_raw<MODE, QW>(sraw, cextra, xe);
           combine_cell<MODE>(xe, Rr.flip, fe, sigma, hnext, rh, fh, u);
-          cell_prims(P, u, q + cextra, QW, flag);
+          cell_prims(P, u, q + cextra, cq + cextra, QW, flag);
         }
       }
-      // refill the consumed slot with row r+2 (each thread its own cells; the bulk path
-      // refills after the barrier below, once every thread has consumed the slot)
+      // refill the consumed raw row with row r+1 (each thread its own cells; the bulk path
+      // refills after the barrier below, once every thread has consumed the row)
       if (!bulk) {
-        if (r + 2 <= i1 + 1) {
-          const RowRef R2 = row_ref(P, r + 2);
-          if (okm) fetch_async<MODE, QW>(P, R2, jm, cmain, sraw);
-          if (oke) fetch_async<MODE, QW>(P, R2, je, cextra, sraw);
+        if (r + 1 <= i1 + 1) {
+          const RowRef R1 = row_ref(P, r + 1);
+          if (okm) fetch_async<MODE, QW>(P, R1, jm, cmain, sraw);
+          if (oke) fetch_async<MODE, QW>(P, R1, je, cextra, sraw);
         }
         cp_commit();
       }
       // The only barrier of the step.  RAW: fluxes of row r-1 read primitives of row r
       // (just written) and outputs of row r-2 read y-fluxes of row r-2 (previous step).
       // WAR is covered by ring depth: primitives of row r+1 overwrite row r-3 (last read by
-      // the fluxes of row r-2, previous step); y-fluxes of row r overwrite row r-3 (last
-      // read by the outputs of row r-3, previous step).
+      // the fluxes of row r-2, previous step); y-fluxes of row r-1 (this step) overwrite
+      // row r-3 (last read by the outputs of row r-3, previous step); centre quantities
+      // are private to their thread.
       __syncthreads();
-      if (bulk && t == 0 && r + 2 <= i1 + 1) {
-        // generic-proxy reads of the slot (before the barrier) precede the async-proxy refill
+      if (bulk && t == 0 && r + 1 <= i1 + 1) {
+        // generic-proxy reads of the row (before the barrier) precede the async-proxy refill
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        fetch_row_bulk<MODE, QW>(P, row_ref(P, r + 2), j0 - 2, sraw, rbar + slot);
+        fetch_row_bulk<MODE, QW>(P, row_ref(P, r + 1), j0 - 2, sraw, rbar);
       }
       // ---- fluxes of row rf = r - 1
       const int rf = r - 1;
@@ -522,24 +521,27 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
         const double* qm = qring + ((rf + 3) % 4) * NQ * QW;
         const double* q0 = qring + ((rf + 4) % 4) * NQ * QW;
         const double* qp = qring + ((rf + 5) % 4) * NQ * QW;
-        double* gyr = gyring + ((rf + 3) % 3) * NF * GYW;
+        const double* c0 = cring + ((rf + 2) % 2) * NC * QW;
+        double* gyr = gyring + ((rf + 2) % 2) * NF * GYW;
         const bool out_row = (rf >= i0 && rf < i1);
         double gy[NF];
         if (t < ncols_out) {
-          flux_cell<FXY>(P, qm, q0, qp, cmain, QW, true, out_row, gxC, gy);
+          flux_cell<FXY>(P, qm, q0, qp, c0, cmain, QW, true, out_row, gxC, gy);
           if (out_row) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) gyr[f * GYW + t + 1] = gy[f];
           }
         }
         if (out_row) {
-          // y-fluxes at the strip's halo columns j0-1 (thread 0) and j0+ncols (last thread)
+          // y-fluxes at the strip's halo columns j0-1 (thread 0, extra slot 1) and
+          // j0+ncols (thread TY-1's extra slot TY+2 on a full strip, else the main slot of
+          // thread ncols): each computed by the owner of that column's centre quantities
           int cs = -1, gslot = 0;
           if (t == 0) { cs = 1; gslot = 0; }
-          if (t == TY - 1) { cs = ncols_out + 2; gslot = ncols_out + 1; }
+          if (t == (ncols_out == TY ? TY - 1 : ncols_out)) { cs = ncols_out + 2; gslot = ncols_out + 1; }
           if (cs >= 0) {
             double gdummy[NF];
-            flux_cell<FXY>(P, qm, q0, qp, cs, QW, false, true, gdummy, gy);
+            flux_cell<FXY>(P, qm, q0, qp, c0, cs, QW, false, true, gdummy, gy);
 #pragma unroll
             for (int f = 0; f < NF; ++f) gyr[f * GYW + gslot] = gy[f];
           }
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(TY) stencil_kernel(const StencilParams P) {
       // thread's own registers; y-fluxes of row ro come from the ring (previous step)
       const int ro = r - 2;
       if (ro >= i0 && t < ncols_out) {
-        const double* gyr = gyring + ((ro + 3) % 3) * NF * GYW;
+        const double* gyr = gyring + ((ro + 2) % 2) * NF * GYW;
         const long long o = (long long)ro * P.ny + j0 + t;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
@@ -741,8 +743,8 @@ template <int TY, int MODE, bool AUG, bool FXY>
 static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  const size_t sm = sizeof(double) * (4 * NQ * QW + 3 * NF * GYW + 2 * NARR * NF * QW) +
-                    2 * sizeof(unsigned long long);
+  const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NARR * NF * QW) +
+                    sizeof(unsigned long long);
   auto k = stencil_kernel<TY, MODE, AUG, FXY>;
   {
     // bulk copies need 16-byte aligned sources and sizes: even ny and aligned buffers
