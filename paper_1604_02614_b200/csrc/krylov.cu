@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     else if (e < len_upd) w[e] = wv.x;
     const double dx = (e < len_dot) ? wv.x : 0.0, dy = (e + 1 < len_dot) ? wv.y : 0.0;
     if (MODE == 0) {
-      for (int i = 0; i < nvec; i += U) {
+      // re-read the basis newest-first: the vectors just streamed by the update are the
+      // likeliest to still sit in L1/L2 (halves the mean reuse distance of the tile)
+      for (int i = (nvec - 1) / U * U; i >= 0; i -= U) {
         double2 x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u)
