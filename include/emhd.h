@@ -212,6 +212,23 @@ int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res,
 /* sendbuf[2][8][2][ny] = rows {0,1} and {nx-2, nx-1} of every field of x */
 int emhd_pack_edges(emhd_ctx* ctx, const double* x, double* sendbuf);
 
+/* ---- output side: snapshots and the explicit-RK4 harness ---- */
+/* cells[(c * 8) + f] = U[f * ncell + c]: the cell-major data block of a .mhd25 snapshot
+ * (replaces np.moveaxis(U, 0, -1) in write_snapshot, snapshot.py:53-57); a slab's block is a
+ * contiguous byte range of the file at offset 96 + 64 * x_offset * ny. */
+int emhd_cells_pack(emhd_ctx* ctx, const double* U, long long ncell, double* cells);
+/* inverse of emhd_cells_pack (read_snapshot, snapshot.py:77) */
+int emhd_cells_unpack(emhd_ctx* ctx, const double* cells, long long ncell, double* U);
+/* *cmax (device) = max over this rank's cells of sqrt((gamma p + |B|^2)/rho) + sqrt(|m|^2/rho^2),
+ * bitwise the reference's (harness.py:166-174, pressure mhd.py:116-131); non-positive density or
+ * pressure raises the status flags. */
+int emhd_max_signal_speed(emhd_ctx* ctx, const double* U, double* cmax);
+/* out[f] (device, 8) = sum over this rank's cells of (U_f - R_f)^2 (error_norm, harness.py:153-163) */
+int emhd_field_sqdiff(emhd_ctx* ctx, const double* U, const double* R, double* out);
+/* out = base + post (x) (t_0 + ...) with lincomb's term rules (harness.py:194, RK4 update) */
+int emhd_lincomb_onto(emhd_ctx* ctx, const double* base, int nterms, const double* const* x, const double* c,
+                      const int* has_c, double post, int has_post, double* out, long long n);
+
 #ifdef __cplusplus
 }
 #endif

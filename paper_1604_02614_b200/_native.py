@@ -83,6 +83,11 @@ _SIGS = {
     "emhd_div_b": (c_int, [c_vp, P, P, P, P]),
     "emhd_current_j": (c_int, [c_vp, P, P, P]),
     "emhd_admissibility_report": (c_int, [c_vp, c_int, P, P, P, P, P, ctypes.POINTER(Report)]),
+    "emhd_cells_pack": (c_int, [c_vp, P, c_ll, P]),
+    "emhd_cells_unpack": (c_int, [c_vp, P, c_ll, P]),
+    "emhd_max_signal_speed": (c_int, [c_vp, P, P]),
+    "emhd_field_sqdiff": (c_int, [c_vp, P, P, P]),
+    "emhd_lincomb_onto": (c_int, [c_vp, P, c_int, PP, DP, IP, c_dbl, c_int, P, c_ll]),
 }
 
 _lib = None

@@ -3,7 +3,7 @@
     python -m paper_1604_02614_b200.build        # or __graft_entry__.build()
 
 Translation units whose arithmetic must be bit-identical to the NumPy
-reference (stencil.cu, vecops.cu) are compiled with ``-fmad=false``; the
+reference (stencil.cu, vecops.cu, harness.cu) are compiled with ``-fmad=false``; the
 reduction / dense kernels keep FMA contraction.  cudart is linked statically
 so the library only needs the driver at run time.
 """
@@ -21,6 +21,7 @@ LIB = os.path.join(HERE, "libemhd.so")
 SOURCES = {
     "stencil.cu": ["-fmad=false"],
     "vecops.cu": ["-fmad=false"],
+    "harness.cu": ["-fmad=false"],
     "krylov.cu": [],
     "dense.cu": [],
     "capi.cu": [],

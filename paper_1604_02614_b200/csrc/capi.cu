@@ -8,6 +8,7 @@
 #include "krylov.cuh"
 #include "dense.cuh"
 #include "vecops.cuh"
+#include "harness.cuh"
 
 using namespace emhd;
 
@@ -392,6 +393,28 @@ extern "C" int emhd_lincomb(emhd_ctx* c, int nterms, const double* const* x, con
   return cerr(launch_lincomb(L, n, len_max, c->partials, max_out, c->ticket, c->num_sms, c->stream));
 }
 
+// out = base + post (x) (t_0 + t_1 + ...): the final stage update of explicit RK4
+// (harness.py:194: y + (step / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4))
+extern "C" int emhd_lincomb_onto(emhd_ctx* c, const double* base, int nterms, const double* const* x,
+                                 const double* cc, const int* has_c, double post, int has_post,
+                                 double* out, long long n) {
+  if (!c || !base || nterms < 1 || nterms > 6 || !x || !out) return EMHD_ERR_ARG;
+  LinComb L;
+  std::memset(&L, 0, sizeof(L));
+  for (int k = 0; k < nterms; ++k) {
+    if (!x[k]) return EMHD_ERR_ARG;
+    L.x[k] = x[k];
+    L.has_c[k] = has_c ? has_c[k] : 0;
+    L.c[k] = cc ? cc[k] : 1.0;
+  }
+  L.nterms = nterms;
+  L.post = post;
+  L.has_post = has_post;
+  L.base = base;
+  L.out = out;
+  return cerr(launch_lincomb(L, n, 0, c->partials, nullptr, c->ticket, c->num_sms, c->stream));
+}
+
 extern "C" int emhd_wrms(emhd_ctx* c, const double* err, const double* y, double tol, long long n,
                          double* out) {
   if (!c || !err || !y || !out) return EMHD_ERR_ARG;
@@ -419,6 +442,32 @@ extern "C" int emhd_pack_edges(emhd_ctx* c, const double* x, double* sendbuf) {
   int G = (int)((total + 255) / 256);
   pack_edges_kernel<<<G, 256, 0, c->stream>>>(x, sendbuf, c->g.nx, c->g.ny);
   return cerr(cudaGetLastError());
+}
+
+// ---- snapshot layout / RK4 harness ----
+extern "C" int emhd_cells_pack(emhd_ctx* c, const double* U, long long ncell, double* cells) {
+  if (!c || !U || !cells || ncell < 0) return EMHD_ERR_ARG;
+  return cerr(launch_cells_pack(U, ncell, cells, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_cells_unpack(emhd_ctx* c, const double* cells, long long ncell, double* U) {
+  if (!c || !U || !cells || ncell < 0) return EMHD_ERR_ARG;
+  return cerr(launch_cells_unpack(cells, ncell, U, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_max_signal_speed(emhd_ctx* c, const double* U, double* cmax) {
+  if (!c || !U || !cmax) return EMHD_ERR_ARG;
+  const long long ncell = (long long)c->g.nx * c->g.ny;
+  const double gm1 = c->p.gamma - 1.0;
+  const double bfac = c->p.b_half ? 0.5 : 1.0;
+  return cerr(launch_signal_speed(U, ncell, c->p.gamma, gm1, bfac, cmax, c->st, c->num_sms, c->stream));
+}
+
+extern "C" int emhd_field_sqdiff(emhd_ctx* c, const double* U, const double* R, double* out) {
+  if (!c || !U || !R || !out) return EMHD_ERR_ARG;
+  const long long ncell = (long long)c->g.nx * c->g.ny;
+  return cerr(launch_field_sqdiff(U, R, ncell, c->partials, (int)(c->partials_len / NF), out, c->num_sms,
+                                  c->stream));
 }
 
 struct emhd_report_s { int which, i, j, pad; double value; };

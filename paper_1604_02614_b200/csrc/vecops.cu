@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(VT) lincomb_kernel(const LinComb L, long long 
     }
     if (L.has_post == 1) acc = __dmul_rn(L.post, acc);
     else if (L.has_post == 2) acc = acc / L.post;      // IEEE division (fdjac.py:49)
+    if (L.base) acc = __dadd_rn(L.base[e], acc);
     L.out[e] = acc;
     if (e < len_max) mx = fmax(mx, fabs(acc));
   }

@@ -11,6 +11,7 @@ struct LinComb {
   int nterms;
   double post;
   int has_post;
+  const double* base;       // optional: out = base + (post-applied sum)
   double* out;
 };
 

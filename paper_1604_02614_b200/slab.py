@@ -119,6 +119,10 @@ class Comm:
             dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
         return t
 
+    def barrier(self):
+        if self.layout.distributed:
+            dist.barrier(group=self.group)
+
 
 def halo_shape(ny):
     return (2, NF, 2, ny)

@@ -203,11 +203,41 @@ def errors():
         json.dump(out, fh)
 
 
+def harness_fixtures():
+    """Output side: .mhd25 / CSV snapshots written by the reference's
+    own writer, and a short explicit-RK4 run with the reference's stable step."""
+    from expmhd import harness as Rh
+    from expmhd import snapshot as Rs
+    from expmhd.problems import ReconnectionSpec, reconnection_ic
+    P = R.MhdParams(mu=1e-3, eta=2e-3, kappa=3e-3)
+    g = ReconnectionSpec().grid(16, 12)
+    U = reconnection_ic(g, params=P)
+    U = U + 1e-3 * np.random.default_rng(11).standard_normal(U.shape)
+    Rs.write_snapshot(os.path.join(OUT, "snapshot_recon16x12.mhd25"), U, g, 0.75, P)
+    Rs.write_snapshot_csv(os.path.join(OUT, "snapshot_recon16x12.csv"), U, g, 0.75, P)
+    np.save(os.path.join(OUT, "snapshot_recon16x12_U.npy"), U)
+
+    g = ReconnectionSpec().grid(32, 16)
+    P = R.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    U0 = reconnection_ic(g, params=P)
+    dt = Rh._rk4_stable_dt(U0, g, P)
+    f = Rm.make_rhs(P, g, R.default_bc("reconnection"))
+    y, st = Rh.integrate_rk4(f, Rm.state_to_vector(U0), 0.0, 7.3 * dt, dt)
+    err = Rh.error_norm(Rm.vector_to_state(y, g), U0, g)
+    np.savez_compressed(os.path.join(OUT, "rk4_recon32x16.npz"), U0=U0, y=y,
+                        scal=np.array([dt, 7.3 * dt, err]),
+                        counts=np.array([st.steps_accepted, st.rhs_evals]))
+
+
 if __name__ == "__main__":
-    rhs_cases()
-    config0()
-    krylov_dense()
-    krylov_mhd()
-    epirk_small()
-    errors()
+    if sys.argv[1:] == ["harness"]:
+        harness_fixtures()
+    else:
+        rhs_cases()
+        config0()
+        krylov_dense()
+        krylov_mhd()
+        epirk_small()
+        errors()
+        harness_fixtures()
     print("fixtures written to", OUT)

@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _worker(rank, size, port):
+def _worker(rank, size, port, tmpdir):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -114,10 +114,41 @@ def _worker(rank, size, port):
         assert np.linalg.norm(y1 - want) <= 1e-8 * np.linalg.norm(z0["y1"]) / np.sqrt(size)
         for key, v in s1.items():
             assert getattr(S, key) == v, key
+
+        # (e): output side across slabs: every rank writes its own byte range of the .mhd25
+        # file and reads its rows back; RK4 (+ stable step, error norm) across slabs
+        U = np.load(os.path.join(GOLDEN, "snapshot_recon16x12_U.npy"))
+        g = P.ReconnectionSpec().grid(16, 12)
+        prm = P.MhdParams(mu=1e-3, eta=2e-3, kappa=3e-3)
+        L = make_layout(g.nx, g.ny, "periodic", rank, size)
+        cm = StagingComm(L)
+        path = os.path.join(tmpdir, f"slabs{size}.mhd25")
+        mine = local_rows(U.reshape(-1), g, L).reshape(8, L.nx_local, g.ny)
+        P.write_snapshot(path, torch.from_numpy(mine).cuda(), g, 0.75, prm, layout=L, comm=cm)
+        with open(path, "rb") as fh, open(os.path.join(GOLDEN, "snapshot_recon16x12.mhd25"), "rb") as gh:
+            assert fh.read() == gh.read()
+        R, _, t, _ = P.read_snapshot(path, layout=L, comm=cm)
+        assert t == 0.75 and np.array_equal(R.cpu().numpy(), mine)
+
+        zr = golden("rk4_recon32x16.npz")
+        g = P.ReconnectionSpec().grid(32, 16)
+        prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+        bc = P.default_bc("reconnection")
+        L = make_layout(g.nx, g.ny, bc.x, rank, size)
+        cm = StagingComm(L)
+        U0 = local_rows(zr["U0"].reshape(-1), g, L)
+        dt = P.rk4_stable_dt(U0.reshape(8, L.nx_local, g.ny), g, prm, layout=L, comm=cm)
+        assert dt == zr["scal"][0]
+        f = P.make_rhs(prm, g, bc, layout=L, comm=cm)
+        y, st = P.integrate_rk4(f, U0, 0.0, zr["scal"][1], dt)
+        assert np.array_equal(y, local_rows(zr["y"], g, L))
+        err = P.error_norm(y.reshape(8, L.nx_local, g.ny), U0.reshape(8, L.nx_local, g.ny), g,
+                           layout=L, comm=cm)
+        assert abs(err - zr["scal"][2]) <= 1e-13 * zr["scal"][2]
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("size", [2, 3])
-def test_slab_ranks_on_one_gpu_match_reference(size):
-    mp.spawn(_worker, args=(size, _port()), nprocs=size, join=True)
+def test_slab_ranks_on_one_gpu_match_reference(size, tmp_path):
+    mp.spawn(_worker, args=(size, _port(), str(tmp_path)), nprocs=size, join=True)

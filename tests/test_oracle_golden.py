@@ -167,3 +167,40 @@ def test_divergence_oracle_bitwise():
         g, P, bc = case_objects(z, k)
         d, peak = stencil.divergence_B(z[f"c{k}_U"], g, bc)
         assert np.array_equal(d, z[f"c{k}_divB"]) and peak == z[f"c{k}_divBmax"][0]
+
+
+def test_harness_oracle_matches_reference_outputs():
+    """oracle/harness_cpu.py against the reference's own snapshot files and RK4 run."""
+    from oracle import harness_cpu as H
+    from paper_1604_02614_b200.mhd import MhdParams
+    from paper_1604_02614_b200.problems import ReconnectionSpec, default_bc
+    U = np.load(os.path.join(GOLDEN, "snapshot_recon16x12_U.npy"))
+    g = ReconnectionSpec().grid(16, 12)
+    P = MhdParams(mu=1e-3, eta=2e-3, kappa=3e-3)
+    with open(os.path.join(GOLDEN, "snapshot_recon16x12.mhd25"), "rb") as fh:
+        assert H.snapshot_bytes(U, g, 0.75, P) == fh.read()
+    with open(os.path.join(GOLDEN, "snapshot_recon16x12.csv")) as fh:
+        assert H.snapshot_csv(U, g, 0.75, P) == fh.read()
+    z = golden("rk4_recon32x16.npz")
+    g = ReconnectionSpec().grid(32, 16)
+    P = MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    dt = H.rk4_stable_dt(z["U0"], g, P)
+    assert dt == z["scal"][0]
+    f = stencil.rhs_closure(P, g, default_bc("reconnection"))
+    y, steps, evals = H.rk4(f, z["U0"].reshape(-1), 0.0, z["scal"][1], dt)
+    assert np.array_equal(y, z["y"]) and [steps, evals] == list(z["counts"])
+    assert H.error_norm(y.reshape(8, 32, 16), z["U0"], g) == z["scal"][2]
+
+
+def test_snapshot_header_parsing_host_logic():
+    """The product's header parser (host logic, no GPU) on the reference file and broken ones."""
+    from paper_1604_02614_b200.snapshot import HEADER_SIZE, SnapshotFormatError, _parse_header
+    with open(os.path.join(GOLDEN, "snapshot_recon16x12.mhd25"), "rb") as fh:
+        raw = fh.read()
+    grid, t, P = _parse_header("f", raw[:HEADER_SIZE])
+    assert (grid.nx, grid.ny, t, P.mu, P.eta, P.kappa) == (16, 12, 0.75, 1e-3, 2e-3, 3e-3)
+    assert (grid.x_lo, grid.x_hi, grid.y_lo, grid.y_hi) == (-12.8, 12.8, -6.4, 6.4)
+    for blob, msg in ((raw[:95], "truncated header"), (b"MHD26\x00" + raw[6:96], "bad magic"),
+                      (raw[:6] + b"\x07\x00" + raw[8:96], "unsupported version 7")):
+        with pytest.raises(SnapshotFormatError, match=msg):
+            _parse_header("f", blob)
