@@ -1,5 +1,6 @@
 // Shared device helpers for the expmhd B200 hot path.
 #pragma once
+#include <cmath>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,9 +44,18 @@ __device__ __forceinline__ double div_const1(double x, double d, double r) {
   return __fma_rn(e, r, q);
 }
 
-template <bool FAST>
+// division by a grid constant: DV 2 = d is a power of two (1/d exact, so x / d == RN(x r)
+// for every x, overflow and underflow included), 1 = one correction suffices, 0 = general
+enum : int { DIV_GENERAL = 0, DIV_TIGHT = 1, DIV_POW2 = 2 };
+template <int DV>
 __device__ __forceinline__ double div_c(double x, double d, double r) {
-  return FAST ? div_const1(x, d, r) : div_const(x, d, r);
+  if (DV == DIV_POW2) return __dmul_rn(x, r);
+  return DV == DIV_TIGHT ? div_const1(x, d, r) : div_const(x, d, r);
+}
+
+__host__ __forceinline__ bool is_pow2(double d) {
+  int e;
+  return d > 0.0 && std::frexp(d, &e) == 0.5;
 }
 
 // exact test of the one-correction condition (1 - r d is exactly representable)

@@ -112,17 +112,19 @@ __device__ __forceinline__ void fetch_cell(const StencilParams& P, const RowRef&
   }
 }
 
+// vj (MODE_JVN, optional): the normalised basis entries w / h_next, kept for the v_j store
 template <int MODE>
 __device__ __forceinline__ void combine_cell(const RawCell<MODE>& x, bool xflip, bool yflip,
                                              double sigma, double hnext, double rh, bool fh,
-                                             double u[NF]) {
+                                             double u[NF], double* vj = nullptr) {
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     double val = x.a[f];
     if (MODE == MODE_JV) val = __dadd_rn(val, __dmul_rn(sigma, x.v[f]));
     if (MODE == MODE_JVN) {
-      const double vj = fh ? div_const1(x.v[f], hnext, rh) : div_const(x.v[f], hnext, rh);
-      val = __dadd_rn(val, __dmul_rn(sigma, vj));
+      const double q = fh ? div_const1(x.v[f], hnext, rh) : div_const(x.v[f], hnext, rh);
+      if (vj) vj[f] = q;
+      val = __dadd_rn(val, __dmul_rn(sigma, q));
     }
     u[f] = val;
   }
@@ -242,7 +244,7 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
 
 // x- and y-flux G = F_hyp - F_diff at one cell (mhd.py:174-197, 209-266, 275-276).
 // c: prim column slot of the cell; qm/q0/qp: prim rows i-1, i, i+1; c0: centre row i.
-template <bool FXY>
+template <int FXY>
 __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* qm,
                                           const double* q0, const double* qp, const double* c0,
                                           int c, int qs,
@@ -322,7 +324,7 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
 #undef QV
 }
 
-template <int TY, int MODE, bool AUG, bool FXY>
+template <int TY, int MODE, bool AUG, int FXY>
 __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilParams P) {
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
@@ -475,15 +477,15 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
         if (okm) {
           RawCell<MODE> xm;
           consume_raw<MODE, QW>(sraw, cmain, xm);
-          combine_cell<MODE>(xm, Rr.flip, fm, sigma, hnext, rh, fh, u);
+          double vj[MODE == MODE_JVN ? NF : 1];
+          combine_cell<MODE>(xm, Rr.flip, fm, sigma, hnext, rh, fh, u, MODE == MODE_JVN ? vj : nullptr);
           cell_prims(P, u, q + cmain, cq + cmain, QW, flag);
           if (MODE == MODE_JVN && r >= i0 && r < i1 && t < ncols_out) {
-            // v_j = w / h_next of an owned cell (krylov.py:167), from the fetched w
+            // v_j = w / h_next of an owned cell (krylov.py:167), computed once for the stencil
+            // input above (the ghost flips apply to u only, never to the stored basis entry)
             const long long o = (long long)r * P.ny + j0 + t;
 #pragma unroll
-            for (int f = 0; f < NF; ++f)
-              P.vout[o + (long long)f * P.nx * P.ny] =
-                  fh ? div_const1(xm.v[f], hnext, rh) : div_const(xm.v[f], hnext, rh);
+            for (int f = 0; f < NF; ++f) P.vout[o + (long long)f * P.nx * P.ny] = vj[f];
           }
         }
         if (oke) {
@@ -739,7 +741,7 @@ cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* 
   return cudaGetLastError();
 }
 
-template <int TY, int MODE, bool AUG, bool FXY>
+template <int TY, int MODE, bool AUG, int FXY>
 static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
@@ -781,7 +783,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int TY, bool FXY>
+template <int TY, int FXY>
 static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s) {
   if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false, FXY>(P, ns, s);
   if (mode == MODE_JV)
@@ -791,8 +793,13 @@ static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, int ns, 
 
 template <int TY>
 static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s) {
+  // 2h constants: powers of two (e.g. [0,1]^2 on 2^k cells) make the 28 centred-difference
+  // divisions per cell single multiplications; otherwise one or two FMA corrections
+  if (is_pow2(P.two_hx) && is_pow2(P.two_hy) && P.r_two_hx == 1.0 / P.two_hx &&
+      P.r_two_hy == 1.0 / P.two_hy)
+    return launch_f<TY, DIV_POW2>(P, mode, aug, ns, s);
   const bool fxy = recip_tight(P.two_hx, P.r_two_hx) && recip_tight(P.two_hy, P.r_two_hy);
-  return fxy ? launch_f<TY, true>(P, mode, aug, ns, s) : launch_f<TY, false>(P, mode, aug, ns, s);
+  return fxy ? launch_f<TY, DIV_TIGHT>(P, mode, aug, ns, s) : launch_f<TY, DIV_GENERAL>(P, mode, aug, ns, s);
 }
 
 int stencil_tile_width(int ny) {

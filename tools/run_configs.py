@@ -106,16 +106,21 @@ def main():
         import cProfile
         prof = cProfile.Profile()
         prof.enable()
+    ms0 = torch.cuda.memory_stats()
     t0 = time.perf_counter()
     y, st = go(f, yd)
     torch.cuda.synchronize()
     T = time.perf_counter() - t0
+    ms1 = torch.cuda.memory_stats()
+    alloc = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries")}
     if prof is not None:
         prof.disable()
         import pstats
-        pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(25)
+        ps = pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime")
+        ps.print_stats(25)
+        ps.print_callers("torch.empty|settle")
     out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
-           "speculative_discarded_total": f.ctx.rhs_discount,
+           "speculative_discarded_total": f.ctx.rhs_discount, "cuda_allocs_in_run": alloc,
            "iterations_per_s": st.operator_applies / T,
            "cell_steps_per_s": g.nx * g.ny * st.steps_accepted / T}
     if a.check:
