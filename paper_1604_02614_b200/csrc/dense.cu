@@ -17,48 +17,71 @@ namespace emhd {
 
 constexpr int DT = 512;   // threads per CTA
 
-// C = alpha * A * B (+ beta * C0 when C0 given); n x n row-major, ld = n.
-__device__ void mm(double* C, const double* A, const double* B, int n, double* sA, double* sB) {
-  // 64x64 output tiles, 16-wide k steps; thread owns a 4 x 2 micro-tile
+// C = A * B, n x n row-major (ld = n).  The CTA's 16 x 32 thread grid owns one output tile
+// of (16 RM) x (32 RN) elements, RM x RN per thread, sized to n (n = 85 -> 96 x 96 instead of
+// four padded 64 x 64 tiles); k runs in 16-wide shared-memory chunks, so every element is
+// one fma chain over k = 0 .. n-1 in order, whatever the tiling.
+constexpr int MM_MAXR = 128;                 // largest single-tile extent (8 x 16, 4 x 32)
+template <int RM, int RN>
+__device__ void mm_tile(double* C, const double* A, const double* B, int n, double* sA, double* sB) {
+  constexpr int TR = 16 * RM, TC = 32 * RN;
   const int t = threadIdx.x;
-  const int tr = (t / 32) * 4;      // 16 row-groups of 4
-  const int tc = (t % 32) * 2;      // 32 col-groups of 2
-  for (int bi = 0; bi < n; bi += 64) {
-    for (int bj = 0; bj < n; bj += 64) {
-      double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  const int tr = (t / 32) * RM;
+  const int tc = (t % 32) * RN;
+  for (int bi = 0; bi < n; bi += TR) {
+    for (int bj = 0; bj < n; bj += TC) {
+      double acc[RM][RN];
+#pragma unroll
+      for (int u = 0; u < RM; ++u)
+#pragma unroll
+        for (int v = 0; v < RN; ++v) acc[u][v] = 0.0;
       for (int bk = 0; bk < n; bk += 16) {
-        // load A[bi:bi+64, bk:bk+16] and B[bk:bk+16, bj:bj+64]
-        for (int q = t; q < 64 * 16; q += DT) {
-          int r = q / 16, c = q % 16;
-          int gr = bi + r, gc = bk + c;
+        for (int q = t; q < TR * 16; q += DT) {
+          const int r = q / 16, c = q % 16;
+          const int gr = bi + r, gc = bk + c;
           sA[r * 17 + c] = (gr < n && gc < n) ? A[gr * n + gc] : 0.0;
-          int r2 = q / 64, c2 = q % 64;
-          int gr2 = bk + r2, gc2 = bj + c2;
-          sB[r2 * 64 + c2] = (gr2 < n && gc2 < n) ? B[gr2 * n + gc2] : 0.0;
+        }
+        for (int q = t; q < 16 * TC; q += DT) {
+          const int r2 = q / TC, c2 = q % TC;
+          const int gr2 = bk + r2, gc2 = bj + c2;
+          sB[r2 * TC + c2] = (gr2 < n && gc2 < n) ? B[gr2 * n + gc2] : 0.0;
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const double b0 = sB[k * 64 + tc], b1 = sB[k * 64 + tc + 1];
+          double bv[RN];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double a = sA[(tr + u) * 17 + k];
-            acc[u][0] = fma(a, b0, acc[u][0]);
-            acc[u][1] = fma(a, b1, acc[u][1]);
+          for (int v = 0; v < RN; ++v) bv[v] = sB[k * TC + tc + v];
+#pragma unroll
+          for (int u = 0; u < RM; ++u) {
+            const double av = sA[(tr + u) * 17 + k];
+#pragma unroll
+            for (int v = 0; v < RN; ++v) acc[u][v] = fma(av, bv[v], acc[u][v]);
           }
         }
         __syncthreads();
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < RM; ++u)
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
+        for (int v = 0; v < RN; ++v) {
           const int gr = bi + tr + u, gc = bj + tc + v;
           if (gr < n && gc < n) C[gr * n + gc] = acc[u][v];
         }
     }
   }
   __syncthreads();
+}
+
+__device__ void mm(double* C, const double* A, const double* B, int n, double* sA, double* sB) {
+  if (n <= 16) mm_tile<1, 1>(C, A, B, n, sA, sB);
+  else if (n <= 32) mm_tile<2, 1>(C, A, B, n, sA, sB);
+  else if (n <= 48) mm_tile<3, 2>(C, A, B, n, sA, sB);
+  else if (n <= 64) mm_tile<4, 2>(C, A, B, n, sA, sB);
+  else if (n <= 80) mm_tile<5, 3>(C, A, B, n, sA, sB);
+  else if (n <= 96) mm_tile<6, 3>(C, A, B, n, sA, sB);
+  else if (n <= 112) mm_tile<7, 4>(C, A, B, n, sA, sB);
+  else mm_tile<8, 4>(C, A, B, n, sA, sB);    // n > 128 loops over 128 x 128 tiles
 }
 
 // 1-norm (max column sum) of an n x n matrix
@@ -194,8 +217,9 @@ __device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac, 
 
 // E = exp(A), A overwritten by scaling; returns false on failure.
 // E = exp(A) (vcol < 0), or only vout = exp(A) e_vcol (vcol >= 0; E then holds a scaled factor)
+// sM: shared-memory home of the n x 2n Gauss-Jordan system when it fits (else null: global)
 __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA, double* sB, double* red,
-                          int* ired, double* prow, int vcol, double* vout) {
+                          int* ired, double* prow, int vcol, double* vout, double* sM) {
   double* A2 = W.m[0];
   double* A4 = W.m[1];
   double* A6 = W.m[2];
@@ -203,7 +227,7 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
   double* U = W.m[4];
   double* Vm = W.m[5];
   double* T = W.m[6];
-  double* M = W.m[7];      // n x 2n
+  double* M = sM ? sM : W.m[7];      // n x 2n: n dependent elimination steps, keep on chip
   double* x = W.vec;
   double* y = W.vec + n;
   double* fac = W.vec + 2 * n;
@@ -337,11 +361,11 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
 // One CTA per scale s: A = (scale_s * post) * augmented(H_m, order); E = expm(A);
 // y_s = beta * E[0:m, order*m]; res_s = |h_next| |y_m| / ||y|| * res_scale_s.
 __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
-  __shared__ double sA[64 * 17];
-  __shared__ double sB[16 * 64];
+  __shared__ double sA[MM_MAXR * 17];
+  __shared__ double sB[16 * MM_MAXR];
   __shared__ double red[DT / 32 + 1];
   __shared__ int ired[DT / 32 + 1];
-  extern __shared__ double prow[];                 // [2n] staged pivot row
+  extern __shared__ double prow[];                 // [2n] staged pivot row (+ [n][2n] M)
   const int sidx = blockIdx.x;
   // phi_order(X) e1 from the (m + order)-dimensional augmentation
   //   [[X, e1, 0 ..], [0, 0, 1 ..], .., [0 .. 0]]   (exp top-right column = phi_order(X) e1),
@@ -380,7 +404,8 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   for (int e = threadIdx.x; e < m * m; e += DT) if (!isfinite(A[(e / m) * n + e % m])) finite = false;
   finite = __syncthreads_and(finite);
   double* ycol = W.vec + 3 * n;                    // [2n] column result / ping-pong
-  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol);
+  double* sM = (n <= P.smem_n) ? prow + 2 * n : nullptr;
+  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol, sM);
   if (ok) {
     bool fin2 = true;
     if (P.E_out) {
@@ -417,9 +442,32 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   }
 }
 
-cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s) {
+cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t s) {
+  PhiSmallArgs P = Pin;
   const int n = P.m + P.order;              // the largest m of a batch
-  phi_small_kernel<<<nscales, DT, sizeof(double) * 2 * n, s>>>(P);
+  // the Gauss-Jordan system [n][2n] joins the pivot row in dynamic shared memory when it
+  // fits next to the static matmul tiles (n <= ~110)
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, phi_small_kernel);
+    max_dyn = optin - (int)fa.sharedSizeBytes;
+    if (cudaFuncSetAttribute(phi_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      max_dyn = 48 * 1024 - (int)fa.sharedSizeBytes;
+    }
+  }
+  size_t dyn = sizeof(double) * 2 * n;
+  P.smem_n = 0;
+  if (sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
+    dyn = sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n);
+    P.smem_n = n;
+  }
+  phi_small_kernel<<<nscales, DT, dyn, s>>>(P);
   return cudaGetLastError();
 }
 

@@ -32,7 +32,8 @@ struct PhiSmallArgs {
   const double* brk_hist;
   long long ldy;            // row stride of Y in batch mode
   double sv[DENSE_MAX_SCALES];
-  double rv[DENSE_MAX_SCALES];            // optional: full n x n exponential of scale_0 * A (S = 1)
+  double rv[DENSE_MAX_SCALES];
+  int smem_n;               // set by the launcher: largest n whose [n][2n] system is on chip            // optional: full n x n exponential of scale_0 * A (S = 1)
 };
 
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s);
