@@ -10,6 +10,7 @@
 // Gauss–Jordan solve with partial pivoting and the squarings all stay on the
 // device, so a residual check costs one launch and one 8-byte read.
 #include <math.h>
+#include <stdlib.h>
 #include "emhd_common.cuh"
 #include "dense.cuh"
 
@@ -84,64 +85,68 @@ __device__ void mm(double* C, const double* A, const double* B, int n, double* s
   else mm_tile<8, 4>(C, A, B, n, sA, sB);    // n > 128 loops over 128 x 128 tiles
 }
 
-// 1-norm (max column sum) of an n x n matrix
-__device__ double norm1(const double* A, int n, double* red) {
-  double best = 0.0;
-  for (int c = threadIdx.x; c < n; c += DT) {
+// Column sums y[c] = sum_r w(r) |A[r][c]| (w = 1 or x[r]) with all threads: 16 row groups x
+// 32 column lanes (coalesced rows), per-lane partials combined in a fixed order.
+__device__ void abs_colsums(const double* A, int n, const double* x, double* y, double* part) {
+  const int l = threadIdx.x & 31, g = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int c = c0 + l;
     double s = 0.0;
-    for (int r = 0; r < n; ++r) s += fabs(A[r * n + c]);
-    best = fmax(best, s);
+    if (c < n) {
+      if (x) for (int r = g; r < n; r += DT / 32) s += x[r] * fabs(A[r * n + c]);
+      else for (int r = g; r < n; r += DT / 32) s += fabs(A[r * n + c]);
+    }
+    part[g * 32 + l] = s;
+    __syncthreads();
+    if (g == 0 && c < n) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < DT / 32; ++q) t += part[q * 32 + l];
+      y[c] = t;
+    }
+    __syncthreads();
   }
-  best = warp_max(best);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+}
+
+__device__ double max_of(const double* y, int n, double* red) {
+  if (threadIdx.x < 32) {
     double b = 0.0;
-    for (int w = 0; w < DT / 32; ++w) b = fmax(b, red[w]);
-    red[DT / 32] = b;
+    for (int i = threadIdx.x; i < n; i += 32) b = fmax(b, y[i]);
+    b = warp_max(b);
+    if (threadIdx.x == 0) red[DT / 32] = b;
   }
   __syncthreads();
   const double r = red[DT / 32];
   __syncthreads();
   return r;
+}
+
+// 1-norm (max column sum) of an n x n matrix; y: n scratch, part: 512 scratch
+__device__ double norm1(const double* A, int n, double* red, double* y, double* part) {
+  abs_colsums(A, n, nullptr, y, part);
+  return max_of(y, n, red);
 }
 
 // || |A|^p ||_1 via p row-vector products 1^T |A| ... |A|
-__device__ double norm1_abs_power(const double* A, int n, int p, double* x, double* y, double* red) {
+__device__ double norm1_abs_power(const double* A, int n, int p, double* x, double* y, double* red,
+                                  double* part) {
   for (int i = threadIdx.x; i < n; i += DT) x[i] = 1.0;
   __syncthreads();
   for (int k = 0; k < p; ++k) {
-    for (int c = threadIdx.x; c < n; c += DT) {
-      double s = 0.0;
-      for (int r = 0; r < n; ++r) s += x[r] * fabs(A[r * n + c]);
-      y[c] = s;
-    }
-    __syncthreads();
+    abs_colsums(A, n, x, y, part);
     for (int i = threadIdx.x; i < n; i += DT) x[i] = y[i];
     __syncthreads();
   }
-  double best = 0.0;
-  for (int i = threadIdx.x; i < n; i += DT) best = fmax(best, x[i]);
-  best = warp_max(best);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = 0.0;
-    for (int w = 0; w < DT / 32; ++w) b = fmax(b, red[w]);
-    red[DT / 32] = b;
-  }
-  __syncthreads();
-  const double r = red[DT / 32];
-  __syncthreads();
-  return r;
+  return max_of(x, n, red);
 }
 
 // Al-Mohy & Higham backward-error estimate ell(A, m) (exact norms)
-__device__ int ell(const double* A, int n, int m, double a1, double* x, double* y, double* red) {
+__device__ int ell(const double* A, int n, int m, double a1, double* x, double* y, double* red,
+                   double* part) {
   // |c_{2m+1}|^{-1} = C(4m+2, 2m+1) * (4m+3)!
   const int p = 2 * m + 1;
   double lg = lgamma(2.0 * p + 1.0) - 2.0 * lgamma((double)p + 1.0) + lgamma(2.0 * p + 2.0);
-  const double nap = norm1_abs_power(A, n, p, x, y, red);
+  const double nap = norm1_abs_power(A, n, p, x, y, red, part);
   if (nap == 0.0 || a1 == 0.0) return 0;
   // alpha = nap / (a1 * abs_c_recip); value = ceil(log2(alpha / u) / (2m))
   const double log2_alpha = log2(nap) - log2(a1) - lg / log(2.0);
@@ -228,31 +233,39 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
   double* Vm = W.m[5];
   double* T = W.m[6];
   double* M = sM ? sM : W.m[7];      // n x 2n: n dependent elimination steps, keep on chip
-  double* x = W.vec;
-  double* y = W.vec + n;
+  double* x = prow;        // norm scratch on chip (prow is free until the solve)
+  double* y = prow + n;
   double* fac = W.vec + 2 * n;
 
+  // ell() runs 2m+1 dependent |A|-matvecs: read A from shared memory when the (not yet
+  // used) Gauss-Jordan area is on chip
+  auto onchip = [&](const double* src) -> const double* {
+    if (!sM) return src;
+    for (int e = threadIdx.x; e < n * n; e += DT) sM[e] = src[e];
+    __syncthreads();
+    return sM;
+  };
   mm(A2, A, A, n, sA, sB);
   mm(A4, A2, A2, n, sA, sB);
   mm(A6, A4, A2, n, sA, sB);
-  const double a1 = norm1(A, n, red);
-  const double d4 = pow(norm1(A4, n, red), 0.25);
-  const double d6 = pow(norm1(A6, n, red), 1.0 / 6.0);
+  const double a1 = norm1(A, n, red, y, sA);
+  const double d4 = pow(norm1(A4, n, red, y, sA), 0.25);
+  const double d6 = pow(norm1(A6, n, red, y, sA), 1.0 / 6.0);
   const double eta1 = fmax(d4, d6);
   int mdeg = 0, s = 0;
-  if (eta1 <= 1.495585217958292e-002 && ell(A, n, 3, a1, x, y, red) == 0) mdeg = 3;
-  else if (eta1 <= 2.539398330063230e-001 && ell(A, n, 5, a1, x, y, red) == 0) mdeg = 5;
+  if (eta1 <= 1.495585217958292e-002 && ell(onchip(A), n, 3, a1, x, y, red, sA) == 0) mdeg = 3;
+  else if (eta1 <= 2.539398330063230e-001 && ell(onchip(A), n, 5, a1, x, y, red, sA) == 0) mdeg = 5;
   double d8 = 0.0, eta3 = 0.0;
   if (mdeg == 0) {
     mm(A8, A4, A4, n, sA, sB);
-    d8 = pow(norm1(A8, n, red), 0.125);
+    d8 = pow(norm1(A8, n, red, y, sA), 0.125);
     eta3 = fmax(d6, d8);
-    if (eta3 <= 9.504178996162932e-001 && ell(A, n, 7, a1, x, y, red) == 0) mdeg = 7;
-    else if (eta3 <= 2.097847961257068e+000 && ell(A, n, 9, a1, x, y, red) == 0) mdeg = 9;
+    if (eta3 <= 9.504178996162932e-001 && ell(onchip(A), n, 7, a1, x, y, red, sA) == 0) mdeg = 7;
+    else if (eta3 <= 2.097847961257068e+000 && ell(onchip(A), n, 9, a1, x, y, red, sA) == 0) mdeg = 9;
   }
   if (mdeg == 0) {
     mm(T, A4, A6, n, sA, sB);           // A^10
-    const double d10 = pow(norm1(T, n, red), 0.1);
+    const double d10 = pow(norm1(T, n, red, y, sA), 0.1);
     const double eta4 = fmax(d8, d10);
     const double eta5 = fmin(eta3, eta4);
     s = (eta5 == 0.0) ? 0 : (int)fmax(ceil(log2(eta5 / 4.25)), 0.0);
@@ -260,8 +273,8 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
     const double sc = ldexp(1.0, -s);
     for (int e = threadIdx.x; e < n * n; e += DT) A[e] *= sc;
     __syncthreads();
-    const double a1s = norm1(A, n, red);
-    s += ell(A, n, 13, a1s, x, y, red);
+    const double a1s = norm1(A, n, red, y, sA);
+    s += ell(onchip(A), n, 13, a1s, x, y, red, sA);
     const double sc2 = ldexp(1.0, -s);
     // rescale from the already-applied 2^-s0 to 2^-s (A), then rebuild powers
     const double extra = sc2 / sc;
@@ -331,12 +344,22 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
     double* xa = vout;
     double* xb = vout + n;
     for (int i = threadIdx.x; i < n; i += DT) xa[i] = E[(size_t)i * n + vcol];
+    // E^T on chip (thread i walks column i: consecutive threads, consecutive words)
+    double* Et = nullptr;
+    if (sM && s > 0) {
+      Et = sM;
+      for (int e = threadIdx.x; e < n * n; e += DT) Et[(e % n) * n + e / n] = E[e];
+    }
     __syncthreads();
     for (int k = 1; k < (1 << s); ++k) {
       for (int i = threadIdx.x; i < n; i += DT) {
         double acc = 0.0;
-        const double* row = E + (size_t)i * n;
-        for (int c = 0; c < n; ++c) acc = fma(row[c], xa[c], acc);
+        if (Et) {
+          for (int c = 0; c < n; ++c) acc = fma(Et[(size_t)c * n + i], xa[c], acc);
+        } else {
+          const double* row = E + (size_t)i * n;
+          for (int c = 0; c < n; ++c) acc = fma(row[c], xa[c], acc);
+        }
         xb[i] = acc;
       }
       __syncthreads();
@@ -461,9 +484,14 @@ cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t 
       max_dyn = 48 * 1024 - (int)fa.sharedSizeBytes;
     }
   }
+  static int use_smem = -1;
+  if (use_smem < 0) {
+    const char* env = getenv("EMHD_DENSE_SMEM");
+    use_smem = env ? atoi(env) != 0 : 1;
+  }
   size_t dyn = sizeof(double) * 2 * n;
   P.smem_n = 0;
-  if (sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
+  if (use_smem && sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
     dyn = sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n);
     P.smem_n = n;
   }
