@@ -211,6 +211,11 @@ int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res,
 /* ---- slab halos ------------------------------------------------------ */
 /* sendbuf[2][8][2][ny] = rows {0,1} and {nx-2, nx-1} of every field of x */
 int emhd_pack_edges(emhd_ctx* ctx, const double* x, double* sendbuf);
+/* Arnoldi norms across slabs with ONE sum all-reduce (krylov.py:151,161 and the next sigma):
+ * slots[0] = nrm[0], slots[1 + rank] = nrm[1], other slots 0; after the SUM all-reduce of the
+ * 1 + nranks slots, emhd_unslot_norms gives nrm = {global sum, max over ranks}. */
+int emhd_slot_norms(emhd_ctx* ctx, const double* nrm, int rank, int nranks, double* slots);
+int emhd_unslot_norms(emhd_ctx* ctx, const double* slots, int nranks, double* nrm);
 
 /* ---- output side: snapshots and the explicit-RK4 harness ---- */
 /* cells[(c * 8) + f] = U[f * ncell + c]: the cell-major data block of a .mhd25 snapshot

@@ -421,6 +421,35 @@ extern "C" int emhd_wrms(emhd_ctx* c, const double* err, const double* y, double
   return cerr(launch_wrms(err, y, tol, n, c->partials, out, c->ticket, c->num_sms, c->stream));
 }
 
+// {sum w^2, max|w|} of one rank -> slots {sum, 0.., max at 1 + rank, ..0}: ONE all-reduce SUM
+// of 1 + P doubles then carries both the global sum and every rank's maximum (adding zeros
+// is exact), instead of a SUM and a MAX collective per Arnoldi iteration
+__global__ void slot_norms_kernel(const double* nrm, int rank, int nranks, double* slots) {
+  for (int i = threadIdx.x; i <= nranks; i += blockDim.x)
+    slots[i] = i == 0 ? nrm[0] : (i == 1 + rank ? nrm[1] : 0.0);
+}
+
+__global__ void unslot_norms_kernel(const double* slots, int nranks, double* nrm) {
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int r = 0; r < nranks; ++r) mx = fmax(mx, slots[1 + r]);
+    nrm[0] = slots[0];
+    nrm[1] = mx;
+  }
+}
+
+extern "C" int emhd_slot_norms(emhd_ctx* c, const double* nrm, int rank, int nranks, double* slots) {
+  if (!c || !nrm || !slots || nranks < 1 || rank < 0 || rank >= nranks) return EMHD_ERR_ARG;
+  slot_norms_kernel<<<1, 32, 0, c->stream>>>(nrm, rank, nranks, slots);
+  return cerr(cudaGetLastError());
+}
+
+extern "C" int emhd_unslot_norms(emhd_ctx* c, const double* slots, int nranks, double* nrm) {
+  if (!c || !nrm || !slots || nranks < 1) return EMHD_ERR_ARG;
+  unslot_norms_kernel<<<1, 32, 0, c->stream>>>(slots, nranks, nrm);
+  return cerr(cudaGetLastError());
+}
+
 __global__ void pack_edges_kernel(const double* x, double* buf, int nx, int ny) {
   // buf[side][f][r][j]: side 0 = rows {0,1}, side 1 = rows {nx-2, nx-1}
   const long long total = 2LL * NF * 2 * ny;

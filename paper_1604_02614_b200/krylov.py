@@ -258,9 +258,17 @@ class _Process:
             self.comm.allreduce_sum(t)
 
     def _allreduce_norms(self, t2):
+        """{sum, max} across slabs with one SUM all-reduce of 1 + P slots (emhd_slot_norms)."""
         if self.comm is not None and self.layout.distributed:
-            self.comm.allreduce_sum(t2[0:1])
-            self.comm.allreduce_max(t2[1:2])
+            L = self.layout
+            slots = getattr(self, "_slots", None)
+            if slots is None:
+                slots = self._slots = torch.zeros(L.size + 1, dtype=D.F64, device=D.device())
+            h = self.ctx.sync_stream()
+            N.check(self.lib.emhd_slot_norms(h, D.ptr(t2), L.rank, L.size, D.ptr(slots)), "slot_norms")
+            self.comm.allreduce_sum(slots)
+            N.check(self.lib.emhd_unslot_norms(self.ctx.sync_stream(), D.ptr(slots), L.size, D.ptr(t2)),
+                    "unslot_norms")
 
     # -- one iteration ----------------------------------------------------------
     def _apply(self, j):
