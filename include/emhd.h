@@ -211,6 +211,14 @@ int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res,
 /* ---- slab halos ------------------------------------------------------ */
 /* sendbuf[2][8][2][ny] = rows {0,1} and {nx-2, nx-1} of every field of x */
 int emhd_pack_edges(emhd_ctx* ctx, const double* x, double* sendbuf);
+/* emhd_update mode 1 (w -= V h; out = {sum w^2, max|w_top|}) that also stores the final w's
+ * rows {0,1} into lo_halo side 1 and rows {nx-2,nx-1} into hi_halo side 0 (the neighbours'
+ * [2][8][2][ny] halo buffers, peer pointers; NULL = no neighbour): the halo exchange of the next
+ * normalised Jv (krylov.py:167,149) fused into the producing pass; the norm all-reduce that
+ * follows orders the stores before the neighbours' stencil. */
+int emhd_update_push(emhd_ctx* ctx, double* w, const double* V, long long ldv, int nvec, const double* h,
+                     long long len_upd, long long len_dot, long long len_max, double* out,
+                     double* lo_halo, double* hi_halo);
 /* Arnoldi norms across slabs with ONE sum all-reduce (krylov.py:151,161 and the next sigma):
  * slots[0] = nrm[0], slots[1 + rank] = nrm[1], other slots 0; after the SUM all-reduce of the
  * 1 + nranks slots, emhd_unslot_norms gives nrm = {global sum, max over ranks}. */

@@ -81,6 +81,7 @@ _SIGS = {
     "emhd_wrms": (c_int, [c_vp, P, P, c_dbl, c_ll, P]),
     "emhd_pack_edges": (c_int, [c_vp, P, P]),
     "emhd_slot_norms": (c_int, [c_vp, P, c_int, c_int, P]),
+    "emhd_update_push": (c_int, [c_vp, P, P, c_ll, c_int, P, c_ll, c_ll, c_ll, P, P, P]),
     "emhd_unslot_norms": (c_int, [c_vp, P, c_int, P]),
     "emhd_div_b": (c_int, [c_vp, P, P, P, P]),
     "emhd_current_j": (c_int, [c_vp, P, P, P]),

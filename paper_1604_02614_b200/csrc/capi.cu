@@ -222,6 +222,25 @@ extern "C" int emhd_update(emhd_ctx* c, double* w, const double* V, long long ld
   return cerr(launch_update(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode, k, out, c->stream));
 }
 
+// emhd_update mode 1 whose final w also lands, rows {0,1} and {nx-2,nx-1} of every field, in
+// the neighbours' halo buffers (peer pointers from symmetric memory; null side: no neighbour).
+// Ordered before the neighbours' next stencil by the norm all-reduce that follows.
+extern "C" int emhd_update_push(emhd_ctx* c, double* w, const double* V, long long ldv, int nvec,
+                                const double* h, long long len_upd, long long len_dot, long long len_max,
+                                double* out, double* lo_halo, double* hi_halo) {
+  if (!c || !w || !out || nvec < 0 || nvec > c->max_vectors || (nvec > 0 && (!V || !h))) return EMHD_ERR_ARG;
+  KWork k = kwork(c);
+  HaloPush P;
+  P.lo = lo_halo;
+  P.hi = hi_halo;
+  P.n_top = 8LL * c->g.nx * c->g.ny;
+  P.plane = (unsigned)((long long)c->g.nx * c->g.ny);
+  P.nx = (unsigned)c->g.nx;
+  P.ny = (unsigned)c->g.ny;
+  if (P.n_top >= (1LL << 32)) return EMHD_ERR_ARG;
+  return cerr(launch_update_push(w, V, ldv, nvec, h, len_upd, len_dot, len_max, k, out, P, c->stream));
+}
+
 extern "C" int emhd_update_finish(emhd_ctx* c, double* w, const double* V, long long ldv, int nvec,
                                   const double* h2, long long len_upd, long long len_dot,
                                   long long len_max, double* nrm, const double* h1,

@@ -148,11 +148,27 @@ __device__ __forceinline__ void finish_column(const FinishArgs& F, const double*
   }
 }
 
-template <int MODE, int U>
+// Halo push (slab ranks): store a final w element that lies in rows {0,1} / {nx-2,nx-1} of
+// its field straight into the lo / hi neighbour's halo buffer (peer memory over NVLink);
+// layout [2 sides][8][2 rows][ny], our low rows land in the lo neighbour's side 1, our high
+// rows in the hi neighbour's side 0 (what Comm.exchange delivers).
+__device__ __forceinline__ void push_edge(const HaloPush& H, long long e, double val) {
+  if (e >= H.n_top) return;
+  const unsigned eu = (unsigned)e;
+  const unsigned f = eu / H.plane;
+  const unsigned q = eu - f * H.plane;
+  const unsigned row = q / H.ny;
+  const unsigned col = q - row * H.ny;
+  if (H.lo && row < 2) H.lo[((size_t)(NF + f) * 2 + row) * H.ny + col] = val;
+  if (H.hi && row + 2 >= H.nx) H.hi[((size_t)f * 2 + (row + 2 - H.nx)) * H.ny + col] = val;
+}
+
+template <int MODE, int U, bool PUSH = false>
 __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, const double* __restrict__ h,
     long long len_upd, long long len_dot, long long len_max,
-    double* partials, double* out, unsigned int* ticket, const FinishArgs fin) {
+    double* partials, double* out, unsigned int* ticket, const FinishArgs fin,
+    const HaloPush push = HaloPush{}) {
   extern __shared__ double sm[];
   constexpr int TL = KT * 2;
   double* s_h = sm;                              // [nvec]
@@ -184,6 +200,10 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     }
     if (full) *reinterpret_cast<double2*>(w + e) = wv;
     else if (e < len_upd) w[e] = wv.x;
+    if (PUSH) {
+      push_edge(push, e, wv.x);
+      if (full) push_edge(push, e + 1, wv.y);
+    }
     const double dx = (e < len_dot) ? wv.x : 0.0, dy = (e + 1 < len_dot) ? wv.y : 0.0;
     if (MODE == 0) {
       // re-read the basis newest-first: the vectors just streamed by the update are the
@@ -209,6 +229,7 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
       mx = fmax(mx, fmax(mxx, mxy));
     }
   }
+  if (PUSH) __threadfence_system();   // peer stores visible before the ordering collective
   if (MODE == 1) {
     ss = warp_sum(ss);
     mx = warp_max(mx);
@@ -342,6 +363,16 @@ cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, c
   else
     update_kernel<1, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
                                            wk.partials, out, wk.ticket, fin);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_push(double* w, const double* V, long long ldv, int nvec, const double* h,
+                               long long len_upd, long long len_dot, long long len_max, KWork& wk,
+                               double* out, const HaloPush& push, cudaStream_t s) {
+  const int G = grid_for(len_upd, KT * 2, wk.num_sms);
+  const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + 2 * NWARP);
+  update_kernel<1, 8, true><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
+                                               wk.partials, out, wk.ticket, FinishArgs{}, push);
   return cudaGetLastError();
 }
 

@@ -23,6 +23,13 @@ struct FinishArgs {         // optional Arnoldi column bookkeeping fused into up
   double rtol;
 };
 
+struct HaloPush {            // peer halo destinations of a slab's edge rows (null: none)
+  double* lo;                // lo neighbour's halo buffer [2][8][2][ny]
+  double* hi;                // hi neighbour's halo buffer
+  long long n_top;           // 8 * nx * ny
+  unsigned plane, nx, ny;    // nx * ny, local rows, columns
+};
+
 struct CombineOut {
   const double* base[4];     // optional base vector per output (null: plain V y)
   double coef[4];            // out = base + coef * (V y)
@@ -34,6 +41,9 @@ cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
                           KWork& wk, double* out, cudaStream_t s, FinishArgs fin = FinishArgs{});
+cudaError_t launch_update_push(double* w, const double* V, long long ldv, int nvec, const double* h,
+                               long long len_upd, long long len_dot, long long len_max, KWork& wk,
+                               double* out, const HaloPush& push, cudaStream_t s);
 cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, KWork& wk, double* out,
                          cudaStream_t s);
 cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,

@@ -29,6 +29,7 @@ from . import _native as N
 from . import device as D
 from .fdjac import FdJacobianOperator, LinearOperator, _generic_ctx, _lincomb
 from .mhd import raise_status
+from .slab import PushHalo
 
 MAX_COMB_ORDER = 5
 # speculation depth of the batched residual checks (0: automatic from the vector size,
@@ -216,6 +217,14 @@ class _Process:
         self.resbuf = torch.empty(8, dtype=D.F64, device=D.device())
         self.host_rb = torch.zeros(self.m_cap + 16, dtype=D.F64, pin_memory=True)
         self.beta_dev = self.nb[2:3]
+        # slab ranks with symmetric memory: w's edge rows are pushed into the neighbours'
+        # halo buffers by the update pass itself (emhd_update_push), no P2P exchange per Jv
+        self.push = None
+        if engine.fused and layout is not None and layout.distributed:
+            g = engine.gpu
+            if "_push_halo" not in g.__dict__:
+                g._push_halo = PushHalo.create(g.layout, g.comm)
+            self.push = g._push_halo
         self.m = 0
         self.breakdown = False
         self.applies = 0
@@ -296,7 +305,7 @@ class _Process:
                 self._last = (1, v, vh, E._vn)
             else:
                 wp = self.w[self.cur]
-                wh = E.gpu.halo(wp[:self.n_top])
+                wh = self.push.buf if self.push is not None else E.gpu.halo(wp[:self.n_top])
                 N.check(self.lib.emhd_jv_normalized(h, D.ptr(a), D.ptr(ah), D.ptr(fa), D.ptr(wp),
                                                     D.ptr(wh), D.ptr(self.scal.dev), D.ptr(self.V[j]),
                                                     self.p, E.ch, len(E.bcols), E._bptr, E._bidx,
@@ -373,6 +382,16 @@ class _Process:
                 h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2), self.len_upd, self.len_dot,
                 self.n_top, D.ptr(self.nrm), D.ptr(self.d1), D.ptr(self.d1[nv:]), j, D.ptr(self.H),
                 self.H.shape[1], D.ptr(self.scal.dev), D.ptr(self.brk)), "update_finish")
+        elif self.push is not None:
+            P = self.push
+            N.check(self.lib.emhd_update_push(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2),
+                                              self.len_upd, self.len_dot, self.n_top, D.ptr(self.nrm),
+                                              P.lo_ptr, P.hi_ptr), "update_push")
+            self._allreduce_norms(self.nrm)          # also orders the pushed halo rows
+            N.check(self.lib.emhd_arnoldi_finish(h, D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm),
+                                                 D.ptr(self.d1[nv:]), j, D.ptr(self.H),
+                                                 self.H.shape[1], D.ptr(self.scal.dev), D.ptr(self.brk)),
+                    "arnoldi_finish")
         else:
             N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2),
                                          self.len_upd, self.len_dot, self.n_top, 1, D.ptr(self.nrm)),

@@ -135,3 +135,66 @@ def pack_edges_torch(x_local, nx_local, ny):
     out[0] = U[:, 0:2, :]
     out[1] = U[:, nx_local - 2:nx_local, :]
     return out
+
+
+class PushHalo:
+    """Symmetric-memory halo buffer of one slab rank plus its neighbours' peer pointers.
+
+    The producer of the Arnoldi vector w (``emhd_update_push``) stores its edge rows straight
+    into the neighbours' buffers over NVLink, replacing the per-iteration P2P halo exchange;
+    the norm all-reduce that follows orders those stores before the neighbours' next stencil,
+    and the dot-product all-reduces of the next iteration order the neighbours' reads before
+    the following overwrite (one buffer suffices).  ``PushHalo.create`` returns None (callers
+    keep the NCCL exchange) unless every rank of the group set it up.
+    """
+
+    def __init__(self, buf, lo_ptr, hi_ptr, handle):
+        self.buf, self.lo_ptr, self.hi_ptr, self._handle = buf, lo_ptr, hi_ptr, handle
+
+    @staticmethod
+    def create(layout, comm):
+        import os
+        if not layout.distributed or os.environ.get("EMHD_PUSH_HALO", "1") == "0":
+            return None
+        if not dist.is_initialized() or dist.get_backend(comm.group) != "nccl":
+            return None
+        group = comm.group if comm.group is not None else dist.group.WORLD
+        n = 2 * NF * 2 * layout.ny
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+        def agree(ok):
+            t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=comm.group)
+            return t.item() == 1.0
+
+        buf = None
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(n, dtype=torch.float64, device=dev)
+            buf.zero_()
+            ok = True
+        except Exception:
+            ok = False
+        if not agree(ok):
+            return None
+        try:
+            if hasattr(symm_mem, "enable_symm_mem_for_group"):
+                try:
+                    symm_mem.enable_symm_mem_for_group(group.group_name)
+                except Exception:
+                    pass
+            hdl = symm_mem.rendezvous(buf, group)
+            lo = hi = None
+            if layout.lo_neighbor >= 0:
+                lo = hdl.get_buffer(layout.lo_neighbor, (n,), torch.float64, 0)
+            if layout.hi_neighbor >= 0:
+                hi = hdl.get_buffer(layout.hi_neighbor, (n,), torch.float64, 0)
+            ok = True
+        except Exception:
+            ok = False
+        if not agree(ok):
+            return None
+        torch.cuda.synchronize()
+        dist.barrier(group=comm.group)
+        return PushHalo(buf.view(halo_shape(layout.ny)), None if lo is None else lo.data_ptr(),
+                        None if hi is None else hi.data_ptr(), (hdl, lo, hi))

@@ -180,6 +180,41 @@ def test_virtual_slabs_match_single_domain(P):
                 assert np.array_equal(out.cpu().numpy(), want), (k, nslab, r)
 
 
+def test_update_push_delivers_exchange_halos(P):
+    """emhd_update_push (the update pass that also stores w's edge rows into the neighbours'
+    halo buffers over peer memory) on one GPU with local buffers standing in for the peers':
+    w and the norms are bitwise emhd_update mode 1's, and the two destination sides hold
+    exactly what Comm.exchange would deliver (emhd_pack_edges of the final w)."""
+    from paper_1604_02614_b200 import _native as N
+    from paper_1604_02614_b200 import device as D
+    from paper_1604_02614_b200.mhd import GpuRhs
+    from paper_1604_02614_b200.slab import make_layout
+    rng = np.random.default_rng(5)
+    g = P.Grid2D(37, 70, 0.0, 1.0, 0.0, 1.0)
+    for nslab, r in ((2, 0), (3, 1), (3, 2)):
+        L = make_layout(g.nx, g.ny, "periodic", r, nslab)
+        f = GpuRhs(P.MhdParams(), g, P.BoundaryPolicy("periodic", "reflect"), layout=L)
+        n = L.n_local
+        ld = (n + 31) // 32 * 32
+        nv = 5
+        V = dev(rng.standard_normal((nv, ld)))
+        hcoef = dev(rng.standard_normal(nv))
+        w0 = rng.standard_normal(n)
+        h = f.ctx.sync_stream()
+        wa, wb = dev(w0), dev(w0)
+        na, nb = D.zeros(2), D.zeros(2)
+        N.check(f.ctx.lib.emhd_update(h, D.ptr(wa), D.ptr(V), ld, nv, D.ptr(hcoef), n, n, n, 1, D.ptr(na)))
+        lo = torch.full((2, 8, 2, g.ny), -7.0, dtype=torch.float64, device="cuda")
+        hi = torch.full((2, 8, 2, g.ny), -7.0, dtype=torch.float64, device="cuda")
+        N.check(f.ctx.lib.emhd_update_push(h, D.ptr(wb), D.ptr(V), ld, nv, D.ptr(hcoef), n, n, n,
+                                           D.ptr(nb), D.ptr(lo), D.ptr(hi)))
+        assert torch.equal(wa, wb) and torch.equal(na, nb)
+        send = torch.empty((2, 8, 2, g.ny), dtype=torch.float64, device="cuda")
+        N.check(f.ctx.lib.emhd_pack_edges(h, D.ptr(wb), D.ptr(send)))
+        assert torch.equal(lo[1], send[0]) and torch.equal(hi[0], send[1])
+        assert bool((lo[0] == -7.0).all()) and bool((hi[1] == -7.0).all())
+
+
 # -------------------------------------------------------------- (c) Arnoldi / phi
 
 def test_arnoldi_dense_operator(P):

@@ -102,6 +102,16 @@ def _slab_worker(rank, size, port, bcx, nx, ny):
         c.allreduce_max(part[1:2])
         assert abs(part[0].item() - float(np.sum(w * U))) <= 1e-12 * abs(float(np.sum(w * U)))
         assert part[1].item() == float(np.max(np.abs(U)))
+        # one-collective norms (emhd_slot_norms layout): {sum, max of rank r at 1 + r}
+        slots = torch.zeros(size + 1, dtype=torch.float64)
+        slots[0] = float(np.sum(Ul * Ul))
+        slots[1 + rank] = float(np.max(np.abs(Ul)))
+        c.allreduce_sum(slots)
+        assert abs(slots[0].item() - float(np.sum(U * U))) <= 1e-12 * float(np.sum(U * U))
+        assert slots[1:].max().item() == float(np.max(np.abs(U)))
+        # peer-memory halo push needs NCCL + symmetric memory: gloo keeps the exchange
+        from paper_1604_02614_b200.slab import PushHalo
+        assert PushHalo.create(L, c) is None
     finally:
         dist.destroy_process_group()
 
