@@ -21,7 +21,7 @@ import torch
 from . import _native as N
 from . import device as D
 from .epirk import StepController, StepStats, integrate_adaptive, integrate_fixed
-from .fdjac import _lincomb, unwrap_gpu_rhs
+from .fdjac import _generic_ctx, _lincomb, host_rhs, unwrap_gpu_rhs
 from .mhd import AdmissibilityError, BoundaryPolicy, _diag_ctx, agree_status, make_rhs, raise_status
 
 
@@ -78,21 +78,29 @@ def rk4_stable_dt(U, grid, params, layout=None, comm=None):
 
 
 class _Rk4Stages:
-    """Device buffers and launches of one RK4 step (k1..k4, the stage input, the next y)."""
+    """Device buffers and launches of one RK4 step (k1..k4, the stage input, the next y).
 
-    def __init__(self, rhs, n):
+    ``rhs`` is the fused stencil (GpuRhs) or, for a user callable (the reference accepts
+    any rhs), ``call`` evaluates it on the device vector; the stage algebra is on the device
+    either way."""
+
+    def __init__(self, rhs, n, call=None, ctx=None):
         self.rhs = rhs
-        self.ctx = rhs.ctx
+        self.call = call
+        self.ctx = ctx if ctx is not None else rhs.ctx
         mk = lambda: torch.empty(n, dtype=D.F64, device=D.device())   # noqa: E731
         self.k = [mk() for _ in range(4)]
         self.stage = mk()
         self.ynew = mk()
         self.halo = None
-        if rhs.layout.distributed:
+        if call is None and rhs.layout.distributed:
             from .slab import halo_shape
             self.halo = torch.zeros(halo_shape(rhs.grid.ny), dtype=D.F64, device=D.device())
 
     def f(self, x, out):
+        if self.call is not None:
+            out.copy_(D.to_device(self.call(x)).reshape(-1))
+            return
         xh = self.rhs.halo(x, self.halo) if self.halo is not None else None
         self.rhs.launch(x, out, xh)
 
@@ -127,26 +135,36 @@ class _Rk4Stages:
 def integrate_rk4(rhs, y0, t0, t_end, h):
     """Classical explicit RK4 with the last step clipped (harness.py:182-199).
 
-    ``rhs`` is a ``make_rhs`` closure; ``y0`` a host or device vector (a host input returns a
-    host result).  With admissibility checks on, the status word is read once per step (one
+    ``rhs`` is a ``make_rhs`` closure (the fused stencil) or any other callable, as in the
+    reference; ``y0`` a host or device vector (a host input returns a host result).  The
+    stage algebra runs on the device in the reference's operation order.  With admissibility
+    checks on, the status word is read once per step (one
     device sync); a flagged step is replayed stage by stage from the state before it (still
     resident: the three step buffers rotate) to raise the reference's exception.
     """
     g = unwrap_gpu_rhs(rhs)
-    if g is None:
-        raise TypeError("integrate_rk4 needs a make_rhs closure (GPU stencil)")
     host = D.is_host(y0)
     y = D.to_device(y0).reshape(-1).clone()
     stats = StepStats()
     start = _time.perf_counter()
+    if g is None:
+        # any other callable (the reference takes one): evaluated as given, on device vectors
+        # for torch-aware callables or through the host for NumPy ones
+        S = _Rk4Stages(None, y.numel(), call=host_rhs(rhs), ctx=_generic_ctx())
+        return _rk4_loop(S, None, y, t0, t_end, h, stats, start, host)
     S = _Rk4Stages(g, y.numel())
+    return _rk4_loop(S, g, y, t0, t_end, h, stats, start, host)
+
+
+def _rk4_loop(S, g, y, t0, t_end, h, stats, start, host):
     prev = torch.empty_like(y)
     t = t0
+    check = g is not None and g.check
     while t < t_end - 1e-14 * max(1.0, abs(t_end)):
         step = min(h, t_end - t)
         ynew = S.step(y, step)
         y, prev, S.ynew = ynew, y, prev          # prev: the state this step started from
-        if g.check:
+        if check:
             st = agree_status(g.ctx.status(), g.comm)
             if st.flags & (N.ST_RHO | N.ST_PRESSURE):
                 g.ctx.reset_status()

@@ -96,3 +96,55 @@ def test_rk4_inadmissible_raises_reference_error():
     assert str(got.value) == str(want.value)
     with pytest.raises(P.AdmissibilityError):
         P.rk4_stable_dt(U, g, prm)
+
+
+def test_error_norm_reference_properties():
+    """harness.py:153-163 behaviour: zero on identical states, closed form for one cell,
+    invariance under a permutation of the components, grid mismatch rejected."""
+    import math
+    import paper_1604_02614_b200 as P
+    g = P.Grid2D(8, 8, 0.0, 1.0, 0.0, 1.0)
+    U = np.random.default_rng(0).standard_normal((8, 8, 8))
+    assert P.error_norm(U, U, g) == 0.0
+    g = P.Grid2D(10, 5, 0.0, 2.0, 0.0, 1.0)
+    U = np.zeros((8, 10, 5))
+    V = U.copy()
+    V[3, 4, 2] += 0.37
+    assert abs(P.error_norm(U, V, g) - 0.37 * math.sqrt(g.hx * g.hy)) <= 1e-14 * 0.37
+    g = P.Grid2D(6, 6, 0.0, 1.0, 0.0, 1.0)
+    rng = np.random.default_rng(1)
+    U, V = rng.standard_normal((8, 6, 6)), rng.standard_normal((8, 6, 6))
+    perm = rng.permutation(8)
+    a, b = P.error_norm(U, V, g), P.error_norm(U[perm], V[perm], g)
+    assert abs(a - b) <= 1e-14 * a
+    g = P.Grid2D(8, 8, 0.0, 1.0, 0.0, 1.0)
+    with pytest.raises(ValueError, match="grid"):
+        P.error_norm(np.zeros((8, 8, 8)), np.zeros((8, 8, 4)), g)
+
+
+def test_rk4_generic_rhs_is_fourth_order():
+    """Any callable rhs, as the reference accepts (harness.py:182-199): y' = -2y."""
+    import math
+    import paper_1604_02614_b200 as P
+    errs = []
+    for h in (0.1, 0.05, 0.025):
+        y, st = P.integrate_rk4(lambda y: -2.0 * y, np.array([1.0]), 0.0, 1.0, h)
+        errs.append(abs(y[0] - math.exp(-2.0)))
+        assert st.rhs_evals == 4 * st.steps_accepted
+    assert abs(math.log2(errs[0] / errs[1]) - 4.0) <= 0.3
+    # same arithmetic as the oracle restatement, step for step
+    yo, steps, _ = harness_cpu.rk4(lambda y: -2.0 * y, np.array([1.0]), 0.0, 1.0, 0.3)
+    y, st = P.integrate_rk4(lambda y: -2.0 * y, np.array([1.0]), 0.0, 1.0, 0.3)
+    assert np.array_equal(y, yo) and st.steps_accepted == steps
+
+
+def test_snapshot_layout_details(tmp_path):
+    """Header fields at their byte offsets; the data block starts with cell (0, 0)'s 8 values."""
+    P, U, g, prm = _snap_case()
+    path = tmp_path / "s.mhd25"
+    P.write_snapshot(str(path), torch.from_numpy(U).cuda(), g, 0.0, prm)
+    raw = path.read_bytes()
+    assert raw[:6] == b"MHD25\x00" and len(raw) == 96 + 16 * 12 * 64
+    assert int.from_bytes(raw[8:12], "little") == 16 and int.from_bytes(raw[12:16], "little") == 12
+    assert np.frombuffer(raw[16:48], dtype="<f8").tolist() == [g.x_lo, g.x_hi, g.y_lo, g.y_hi]
+    assert np.array_equal(np.frombuffer(raw[96:96 + 64], dtype="<f8"), U[:, 0, 0])
