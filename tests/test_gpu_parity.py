@@ -57,6 +57,44 @@ def test_rhs_bitwise_full_config2_grid_vs_oracle(P):
     assert np.array_equal(F, stencil.mhd_rhs(U, prm, g, bc).reshape(-1))
 
 
+def test_rhs_jv_minimum_and_ragged_grids_vs_oracle(P):
+    """Edge sizes: the reference's minimum 4-cell grids, one-strip and ragged strips (TY=32/64/128
+    paths), every boundary combination, RHS and Jv bit-identical to the oracle."""
+    from oracle import jvp, stencil
+    rng = np.random.default_rng(44)
+    bcs = ["periodic", "reflect", "zero-gradient"]
+    for (nx, ny) in ((4, 4), (4, 7), (9, 4), (5, 33), (6, 65), (7, 129), (3 * 2 + 4, 130)):
+        g = P.Grid2D(nx, ny, -0.3, 1.1, 0.2, 0.9)
+        prm = P.MhdParams(mu=2e-2, eta=1e-2, kappa=3e-2, b_half=bool(nx % 2))
+        U = np.zeros((8, nx, ny))
+        U[0] = 1.0 + 0.3 * rng.random((nx, ny))
+        U[1:4] = 0.3 * rng.standard_normal((3, nx, ny))
+        U[4:7] = rng.standard_normal((3, nx, ny))
+        U[7] = 40.0 + rng.random((nx, ny))
+        v = rng.standard_normal(U.size)
+        for bx in bcs:
+            for by in bcs:
+                bc = P.BoundaryPolicy(bx, by)
+                f = P.make_rhs(prm, g, bc)
+                F = f(U.reshape(-1))
+                assert np.array_equal(F, stencil.mhd_rhs(U, prm, g, bc).reshape(-1)), (nx, ny, bx, by)
+                ref = jvp.FdJv(stencil.rhs_closure(prm, g, bc), U.reshape(-1))
+                assert np.array_equal(P.FdJacobianOperator(f, U.reshape(-1))(v), ref(v)), (nx, ny, bx, by)
+
+
+def test_rhs_bitwise_large_ragged_grid_vs_oracle(P):
+    """2048 x 1000 (non power-of-two spacing: corrected-reciprocal divisions; a ragged last
+    strip; 8 M cells) against the oracle."""
+    from oracle import stencil
+    from paper_1604_02614_b200.problems import fourier_state
+    g = P.Grid2D(2048, 1000, 0.0, 1.0, 0.0, 0.7)
+    prm = P.MhdParams(mu=1e-3, eta=2e-3, kappa=1e-3)
+    bc = P.BoundaryPolicy("periodic", "reflect")
+    U, _ = fourier_state(g, prm)
+    F = P.make_rhs(prm, g, bc)(dev(U.reshape(-1))).cpu().numpy()
+    assert np.array_equal(F, stencil.mhd_rhs(U, prm, g, bc).reshape(-1))
+
+
 def test_rhs_is_pure_and_reconnection_bitwise(P):
     z = golden("config0_recon64.npz")
     g = P.ReconnectionSpec().grid(64, 64)
