@@ -8,7 +8,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libemhd.so")
+# EMHD_LIB: an alternative in-tree build of the same ABI (A/B kernel experiments)
+LIB_PATH = os.environ.get("EMHD_LIB") or os.path.join(HERE, "libemhd.so")
 
 c_int, c_ll, c_dbl, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p
 P = ctypes.c_void_p          # device pointers travel as integers

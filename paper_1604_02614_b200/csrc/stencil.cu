@@ -28,12 +28,19 @@ enum : int { Q_V0 = 0, Q_V1, Q_V2, Q_B0, Q_B1, Q_B2, Q_T, NQ };
 // cell-centre-only quantities: written and read by the cell's own thread (no barrier)
 enum : int { C_RHO = 0, C_MX, C_MY, C_EN, C_PT, NC };
 
+// Element offsets are 32-bit: the launcher requires 8 * nx * ny < 2^32 (a 4096^2 slab is
+// 2^27), so every address is one 32 x 32 -> 64 IMAD.WIDE from the array base.
 struct RowRef {
-  long long off;     // element offset of (field 0, row, col 0) in the chosen buffer
-  long long fs;      // field stride in that buffer
+  unsigned off;      // element offset of (field 0, row, col 0) in the chosen buffer
+  unsigned fs;       // field stride in that buffer
   bool halo;         // read from the halo buffer instead of the interior
   bool flip;         // mirrored ghost row: MX, BX change sign
 };
+
+// ghost-row / ghost-column sign flips as a mask on the high word (-x flips the sign bit)
+__device__ __forceinline__ double flip_sign(double x, unsigned m) {
+  return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
 
 __device__ __forceinline__ int map_ghost(int k, int n, int bc, bool& flip) {
   flip = false;
@@ -46,21 +53,21 @@ __device__ __forceinline__ int map_ghost(int k, int n, int bc, bool& flip) {
 
 __device__ __forceinline__ RowRef row_ref(const StencilParams& P, int r) {
   RowRef R;
-  const long long ny = P.ny;
+  const unsigned ny = (unsigned)P.ny;
   R.halo = false;
-  R.fs = (long long)P.nx * ny;
+  R.fs = (unsigned)P.nx * ny;
   if (r < 0 && P.bcx_lo == BC_EXTERNAL) {
-    R.halo = true; R.fs = 2 * ny; R.off = (long long)(r + 2) * ny; R.flip = false;
+    R.halo = true; R.fs = 2 * ny; R.off = (unsigned)(r + 2) * ny; R.flip = false;
     return R;
   }
   if (r >= P.nx && P.bcx_hi == BC_EXTERNAL) {
-    R.halo = true; R.fs = 2 * ny; R.off = (long long)NF * 2 * ny + (long long)(r - P.nx) * ny;
+    R.halo = true; R.fs = 2 * ny; R.off = (unsigned)NF * 2 * ny + (unsigned)(r - P.nx) * ny;
     R.flip = false;
     return R;
   }
   bool fl;
   int src = map_ghost(r, P.nx, r < 0 ? P.bcx_lo : P.bcx_hi, fl);
-  R.off = (long long)src * ny;
+  R.off = (unsigned)src * ny;
   R.flip = fl;
   return R;
 }
@@ -74,15 +81,15 @@ __device__ __forceinline__ void load_cell(const StencilParams& P, const RowRef& 
   const double* A = R.halo ? P.a_halo : P.a;
   const double* Vv = nullptr;
   if (MODE != MODE_RHS) Vv = R.halo ? P.v_halo : P.v;
-  const long long o = R.off + jsrc;
+  const unsigned o = R.off + jsrc;
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    double x = __ldg(A + o + f * R.fs);
+    double x = __ldg(A + (o + f * R.fs));
     if (MODE == MODE_JV) {
-      double d = __ldg(Vv + o + f * R.fs);
+      double d = __ldg(Vv + (o + f * R.fs));
       x = __dadd_rn(x, __dmul_rn(sigma, d));          // a + sigma * v   (fdjac.py:44)
     } else if (MODE == MODE_JVN) {
-      double d = div_const(__ldg(Vv + o + f * R.fs), hnext, rh);   // v_j = w / h (krylov.py:167)
+      double d = div_const(__ldg(Vv + (o + f * R.fs)), hnext, rh);   // v_j = w / h (krylov.py:167)
       x = __dadd_rn(x, __dmul_rn(sigma, d));
     }
     u[f] = x;
@@ -102,19 +109,19 @@ template <int MODE>
 __device__ __forceinline__ void fetch_cell(const StencilParams& P, const RowRef& R, int jsrc,
                                            RawCell<MODE>& x) {
   const double* A = R.halo ? P.a_halo : P.a;
-  const long long o = R.off + jsrc;
+  const unsigned o = R.off + jsrc;
 #pragma unroll
-  for (int f = 0; f < NF; ++f) x.a[f] = __ldg(A + o + f * R.fs);
+  for (int f = 0; f < NF; ++f) x.a[f] = __ldg(A + (o + f * R.fs));
   if (MODE != MODE_RHS) {
     const double* Vv = R.halo ? P.v_halo : P.v;
 #pragma unroll
-    for (int f = 0; f < NF; ++f) x.v[f] = __ldg(Vv + o + f * R.fs);
+    for (int f = 0; f < NF; ++f) x.v[f] = __ldg(Vv + (o + f * R.fs));
   }
 }
 
 // vj (MODE_JVN, optional): the normalised basis entries w / h_next, kept for the v_j store
 template <int MODE>
-__device__ __forceinline__ void combine_cell(const RawCell<MODE>& x, bool xflip, bool yflip,
+__device__ __forceinline__ void combine_cell(const RawCell<MODE>& x, unsigned xflip, unsigned yflip,
                                              double sigma, double hnext, double rh, bool fh,
                                              double u[NF], double* vj = nullptr) {
 #pragma unroll
@@ -128,8 +135,8 @@ __device__ __forceinline__ void combine_cell(const RawCell<MODE>& x, bool xflip,
     }
     u[f] = val;
   }
-  if (xflip) { u[1] = -u[1]; u[4] = -u[4]; }
-  if (yflip) { u[2] = -u[2]; u[5] = -u[5]; }
+  u[1] = flip_sign(u[1], xflip); u[4] = flip_sign(u[4], xflip);
+  u[2] = flip_sign(u[2], yflip); u[5] = flip_sign(u[5], yflip);
 }
 
 // --- cp.async staging of raw rows (Ampere+ LDGSTS; no register cost) -------------
@@ -179,13 +186,13 @@ __device__ __forceinline__ void fetch_row_bulk(const StencilParams& P, const Row
   constexpr unsigned SEG = QW * sizeof(double);
   mbar_expect_tx(bar, NA * NF * SEG);
   const double* A = R.halo ? P.a_halo : P.a;
-  const long long o = R.off + jfirst;
+  const unsigned o = R.off + jfirst;
 #pragma unroll
-  for (int f = 0; f < NF; ++f) bulk_copy_g2s(slot + f * QW, A + o + f * R.fs, SEG, bar);
+  for (int f = 0; f < NF; ++f) bulk_copy_g2s(slot + f * QW, A + (o + f * R.fs), SEG, bar);
   if (NA == 2) {
     const double* Vv = R.halo ? P.v_halo : P.v;
 #pragma unroll
-    for (int f = 0; f < NF; ++f) bulk_copy_g2s(slot + (NF + f) * QW, Vv + o + f * R.fs, SEG, bar);
+    for (int f = 0; f < NF; ++f) bulk_copy_g2s(slot + (NF + f) * QW, Vv + (o + f * R.fs), SEG, bar);
   }
 }
 
@@ -195,13 +202,13 @@ __device__ __forceinline__ void fetch_async(const StencilParams& P, const RowRef
                                             double* slot) {
   constexpr int NA = MODE == MODE_RHS ? 1 : 2;
   const double* A = R.halo ? P.a_halo : P.a;
-  const long long o = R.off + jsrc;
+  const unsigned o = R.off + jsrc;
 #pragma unroll
-  for (int f = 0; f < NF; ++f) cp_async8(slot + f * QW + c, A + o + f * R.fs);
+  for (int f = 0; f < NF; ++f) cp_async8(slot + f * QW + c, A + (o + f * R.fs));
   if (NA == 2) {
     const double* Vv = R.halo ? P.v_halo : P.v;
 #pragma unroll
-    for (int f = 0; f < NF; ++f) cp_async8(slot + (NF + f) * QW + c, Vv + o + f * R.fs);
+    for (int f = 0; f < NF; ++f) cp_async8(slot + (NF + f) * QW + c, Vv + (o + f * R.fs));
   }
 }
 
@@ -387,6 +394,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
   }
 
   const int ncols_out = min(TY, P.ny - j0);
+  const unsigned plane = (unsigned)P.nx * (unsigned)P.ny;   // field stride of out / fa / vout
   int flag = 0;
   unsigned long long bad = ~0ull;
 
@@ -416,9 +424,10 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
     const int cmain = t + 2;
     const int cextra = t == 0 ? 1 : t == 1 ? 0 : t == TY - 2 ? TY + 3 : t == TY - 1 ? TY + 2 : -1;
     auto col_ok = [&](int c) { int j = j0 - 2 + c; return j >= -2 && j <= P.ny + 1; };
-    bool fm, fe;
+    bool fm, fe = false;
     const int jm = map_ghost(j0 - 2 + cmain, P.ny, P.bcy, fm);
     const int je = cextra >= 0 ? map_ghost(j0 - 2 + cextra, P.ny, P.bcy, fe) : 0;
+    const unsigned ymm = fm ? 0x80000000u : 0u, yme = fe ? 0x80000000u : 0u;
     const bool okm = col_ok(cmain), oke = cextra >= 0 && col_ok(cextra);
 
     // prologue: primitives of rows i0-2 and i0-1
@@ -440,9 +449,9 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
     // fluxes of row r-1 and outputs of row r-2 are computed
     double fa_pre[NF];                       // F(a) of the next output row, one step ahead
     if (MODE != MODE_RHS && t < ncols_out) {
-      const long long o = (long long)i0 * P.ny + j0 + t;
+      const unsigned o = (unsigned)i0 * P.ny + j0 + t;
 #pragma unroll
-      for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o + (long long)f * P.nx * P.ny);
+      for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + (o + f * plane));
     }
     double gxA[NF], gxB[NF], gxC[NF];        // x-fluxes of rows r-3, r-2, r-1 (own column)
 #pragma unroll
@@ -478,20 +487,21 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
           RawCell<MODE> xm;
           consume_raw<MODE, QW>(sraw, cmain, xm);
           double vj[MODE == MODE_JVN ? NF : 1];
-          combine_cell<MODE>(xm, Rr.flip, fm, sigma, hnext, rh, fh, u, MODE == MODE_JVN ? vj : nullptr);
+          combine_cell<MODE>(xm, Rr.flip ? 0x80000000u : 0u, ymm, sigma, hnext, rh, fh, u,
+                             MODE == MODE_JVN ? vj : nullptr);
           cell_prims(P, u, q + cmain, cq + cmain, QW, flag);
           if (MODE == MODE_JVN && r >= i0 && r < i1 && t < ncols_out) {
             // v_j = w / h_next of an owned cell (krylov.py:167), computed once for the stencil
             // input above (the ghost flips apply to u only, never to the stored basis entry)
-            const long long o = (long long)r * P.ny + j0 + t;
+            const unsigned o = (unsigned)r * P.ny + j0 + t;
 #pragma unroll
-            for (int f = 0; f < NF; ++f) P.vout[o + (long long)f * P.nx * P.ny] = vj[f];
+            for (int f = 0; f < NF; ++f) P.vout[o + f * plane] = vj[f];
           }
         }
         if (oke) {
           RawCell<MODE> xe;
           consume_raw<MODE, QW>(sraw, cextra, xe);
-          combine_cell<MODE>(xe, Rr.flip, fe, sigma, hnext, rh, fh, u);
+          combine_cell<MODE>(xe, Rr.flip ? 0x80000000u : 0u, yme, sigma, hnext, rh, fh, u);
           cell_prims(P, u, q + cextra, cq + cextra, QW, flag);
         }
       }
@@ -554,21 +564,19 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
       const int ro = r - 2;
       if (ro >= i0 && t < ncols_out) {
         const double* gyr = gyring + ((ro + 2) % 2) * NF * GYW;
-        const long long o = (long long)ro * P.ny + j0 + t;
+        const unsigned o = (unsigned)ro * P.ny + j0 + t;
+        unsigned nfmask = 0;                 // bit f: F of field f is inf / nan
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
           const double ddx = div_c<FXY>(__dsub_rn(gxC[f], gxA[f]), P.two_hx, P.r_two_hx);
           const double ddy = div_c<FXY>(__dsub_rn(gyr[f * GYW + t + 2], gyr[f * GYW + t]), P.two_hy, P.r_two_hy);
           double F = __dsub_rn(-ddx, ddy);                    // -ddx(gx) - ddy(gy) (mhd.py:277)
-          const long long idx = o + (long long)f * P.nx * P.ny;
+          const unsigned idx = o + f * plane;
           if (MODE == MODE_RHS) {
             P.out[idx] = F;
           } else {
-            if (!isfinite(F)) {
-              const unsigned long long gidx = (unsigned long long)f * P.nxg * P.ny +
-                  (unsigned long long)(P.x_off + ro) * P.ny + j0 + t;
-              bad = gidx < bad ? gidx : bad;
-            }
+            // exponent all ones <=> bit 31 of (hi & 0x7ff00000) + 2^20
+            nfmask |= (((unsigned)__double2hiint(F) & 0x7ff00000u) + 0x00100000u) >> (31 - f) & (1u << f);
             const double df = __dsub_rn(F, fa_pre[f]);
             double jv = fsig ? div_const1(df, sigma, rsig) : div_const(df, sigma, rsig);   // fdjac.py:49
             if (AUG) {
@@ -579,10 +587,16 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
             P.out[idx] = jv;
           }
         }
+        if (MODE != MODE_RHS && nfmask) {
+          // rare path: flat index (global (8, nxg, ny) order) of the first bad field
+          const unsigned long long gidx = (unsigned long long)(__ffs(nfmask) - 1) * P.nxg * P.ny +
+              (unsigned long long)(P.x_off + ro) * P.ny + j0 + t;
+          bad = gidx < bad ? gidx : bad;
+        }
         if (MODE != MODE_RHS && ro + 1 < i1) {
-          const long long o2 = o + P.ny;
+          const unsigned o2 = o + P.ny;
 #pragma unroll
-          for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + o2 + (long long)f * P.nx * P.ny);
+          for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + (o2 + f * plane));
         }
       }
 #pragma unroll
@@ -748,6 +762,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NARR * NF * QW) +
                     sizeof(unsigned long long);
   auto k = stencil_kernel<TY, MODE, AUG, FXY>;
+  if ((long long)NF * P.nx * P.ny >= (1LL << 32)) return cudaErrorInvalidValue;   // 32-bit offsets
   {
     // bulk copies need 16-byte aligned sources and sizes: even ny and aligned buffers
     static int use_tma = -1;
