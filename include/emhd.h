@@ -89,6 +89,9 @@ int emhd_set_epoch(emhd_ctx* ctx, int epoch);
 /* synchronous read of the device status word (stream-ordered) */
 int emhd_status_read(emhd_ctx* ctx, emhd_status* out);
 int emhd_status_reset(emhd_ctx* ctx);
+/* stream-ordered: clear RHO/PRESSURE/NONFINITE flags whose fail_iter >= epoch_min (discarded
+ * speculative Arnoldi iterations; no reference counterpart — they never run there) */
+int emhd_status_scrub(emhd_ctx* ctx, int epoch_min);
 
 /* ---- (a) right-hand side ------------------------------------------- */
 /* F = rhs(u)   — replaces make_rhs(...)(y) / rhs(U, params, grid, bc)  mhd.py:269-285 */
@@ -203,6 +206,16 @@ int emhd_current_j(emhd_ctx* ctx, const double* U, const double* U_halo, double*
 int emhd_arnoldi_iter(emhd_ctx* ctx, const void* args, int j);
 /* emhd_arnoldi_iter for j = j_begin .. j_end-1 (one call for a burst of iterations) */
 int emhd_arnoldi_run(emhd_ctx* ctx, const void* args, int j_begin, int j_end);
+/* emhd_arnoldi_run for look-ahead iterations queued while the residual checks of earlier ones
+ * run on another stream: each iteration is gated on the context's cancel word (j >= 1).
+ * No reference counterpart — the reference checks every residual before extending. */
+int emhd_arnoldi_lookahead(emhd_ctx* ctx, const void* args, int j_begin, int j_end);
+/* cancel the look-ahead iterations j >= epoch_min of process generation gen that have not
+ * started (async 8-byte copy on the context's stream) */
+int emhd_arnoldi_cancel(emhd_ctx* ctx, int gen, int epoch_min);
+/* status.rhs_evals -= sum(evals[0:count]): RHS evaluations of discarded speculative
+ * iterations (evals written per iteration by emhd_arnoldi_iter when args.evals is set) */
+int emhd_evals_discount(emhd_ctx* ctx, const double* evals, int count);
 /* Copy brk[0:nbrk] and res[0:nres] into host_out (pinned), then read the status word: the one
  * host synchronisation of a residual check. */
 int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res, int nres,

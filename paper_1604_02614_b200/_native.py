@@ -38,7 +38,8 @@ class ArnoldiArgs(ctypes.Structure):
     _fields_ = [("a", P), ("fa", P), ("V", P), ("ldv", c_ll), ("H", P), ("ldh", c_ll),
                 ("w0", P), ("w1", P), ("d1", P), ("d2", P), ("nrm", P), ("vn", P), ("scal", P),
                 ("brk", P), ("n_top", c_ll), ("len_dot", c_ll), ("len_upd", c_ll), ("p", c_int),
-                ("nb", c_int), ("ch", c_dbl), ("bcol", P * 5), ("bidx", c_int * 5)]
+                ("nb", c_int), ("ch", c_dbl), ("bcol", P * 5), ("bidx", c_int * 5),
+                ("gen", c_int), ("gate", P), ("evals", P)]
 
 
 class Report(ctypes.Structure):
@@ -58,6 +59,7 @@ _SIGS = {
     "emhd_num_sms": (c_int, [c_vp]),
     "emhd_status_read": (c_int, [c_vp, ctypes.POINTER(Status)]),
     "emhd_status_reset": (c_int, [c_vp]),
+    "emhd_status_scrub": (c_int, [c_vp, c_int]),
     "emhd_rhs": (c_int, [c_vp, P, P, P]),
     "emhd_jv": (c_int, [c_vp, P, P, P, P, P, P, P]),
     "emhd_jv_aug": (c_int, [c_vp, P, P, P, P, P, P, P, c_int, c_dbl, c_int, PP, IP, P]),
@@ -75,6 +77,9 @@ _SIGS = {
     "emhd_phi_small_h": (c_int, [c_vp, P, c_ll, c_int, c_int, c_int, DP, P, P, P, P]),
     "emhd_arnoldi_iter": (c_int, [c_vp, c_vp, c_int]),
     "emhd_arnoldi_run": (c_int, [c_vp, c_vp, c_int, c_int]),
+    "emhd_arnoldi_lookahead": (c_int, [c_vp, c_vp, c_int, c_int]),
+    "emhd_arnoldi_cancel": (c_int, [c_vp, c_int, c_int]),
+    "emhd_evals_discount": (c_int, [c_vp, P, c_int]),
     "emhd_phi_small_batch": (c_int, [c_vp, P, c_ll, IP, c_int, c_int, DP, P, P, P, c_ll, P]),
     "emhd_readback": (c_int, [c_vp, P, c_int, P, c_int, P, ctypes.POINTER(Status)]),
     "emhd_combine": (c_int, [c_vp, P, c_ll, c_int, P, c_int, PP, DP, PP, c_ll]),

@@ -28,6 +28,8 @@ struct emhd_ctx {
   size_t dense_len = 0;
   StencilParams base{};
   int epoch = 0;
+  unsigned long long* cancel = nullptr;       // look-ahead cancel word {generation, epoch}
+  unsigned long long* cancel_host = nullptr;  // pinned source of its async updates
 };
 
 static int cerr(cudaError_t e) {
@@ -88,6 +90,9 @@ extern "C" int emhd_ctx_create(emhd_ctx** out, const emhd_geometry* g, const emh
   if (!rc) rc = cerr(cudaMemset(c->ticket, 0, 16 * sizeof(unsigned int)));
   if (!rc) rc = cerr(cudaMalloc(&c->st, sizeof(DevStatus)));
   if (!rc) rc = cerr(cudaMallocHost(&c->st_host, sizeof(DevStatus)));
+  if (!rc) rc = cerr(cudaMalloc(&c->cancel, sizeof(unsigned long long)));
+  if (!rc) rc = cerr(cudaMallocHost(&c->cancel_host, sizeof(unsigned long long)));
+  if (!rc) rc = cerr(cudaMemset(c->cancel, 0xff, sizeof(unsigned long long)));   // matches nothing
   if (rc) { emhd_ctx_destroy(c); return rc; }
   fill_base(c);
   emhd_status_reset(c);
@@ -102,7 +107,9 @@ extern "C" int emhd_ctx_destroy(emhd_ctx* c) {
   cudaFree(c->ticket);
   cudaFree(c->st);
   cudaFree(c->dense);
+  cudaFree(c->cancel);
   if (c->st_host) cudaFreeHost(c->st_host);
+  if (c->cancel_host) cudaFreeHost(c->cancel_host);
   delete c;
   return EMHD_OK;
 }
@@ -131,6 +138,23 @@ extern "C" int emhd_status_reset(emhd_ctx* c) {
   int rc = cerr(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevStatus), cudaMemcpyHostToDevice, c->stream));
   if (!rc) rc = cerr(cudaStreamSynchronize(c->stream));
   return rc;
+}
+
+// Stream-ordered scrub of stencil error flags raised by iterations with epoch >= epoch_min
+// (speculative iterations that were discarded, possibly still running when the host decided):
+// the reference never performs them, so their flags must not reach a later status read.
+__global__ void status_scrub_kernel(DevStatus* st, int epoch_min) {
+  if ((st->flags & (ST_RHO | ST_PRESSURE | ST_NONFINITE)) && st->fail_iter >= epoch_min) {
+    st->flags &= ~(ST_RHO | ST_PRESSURE | ST_NONFINITE);
+    st->fail_iter = 0x7fffffff;
+    st->first_nonfinite = ~0ull;
+  }
+}
+
+extern "C" int emhd_status_scrub(emhd_ctx* c, int epoch_min) {
+  if (!c) return EMHD_ERR_ARG;
+  status_scrub_kernel<<<1, 1, 0, c->stream>>>(c->st, epoch_min);
+  return cerr(cudaGetLastError());
 }
 
 extern "C" int emhd_status_read(emhd_ctx* c, emhd_status* out) {
@@ -570,24 +594,36 @@ struct emhd_arnoldi_args_s {
   long long n_top; long long len_dot; long long len_upd;
   int p; int nb; double ch;
   const double* bcol[5]; int bidx[5];
+  int gen;             // process generation (look-ahead cancellation)
+  double* gate;        // [m_cap + 1] per-iteration gates (look-ahead launches)
+  double* evals;       // [m_cap + 1] 1 where iteration j evaluated the RHS (or null)
 };
 
 // Iteration j of krylov.py:144-168 on one rank: (normalise w_{j-1} +) Jv, pass-1 multi-dot with
 // the breakdown scale, update + re-projection, update + norms + column bookkeeping.  Writes
 // w_{j} into w0/w1 (j even/odd) and V[j] (j > 0), H[:, j], scal, brk[j].
-extern "C" int emhd_arnoldi_iter(emhd_ctx* c, const void* args, int j) {
+static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   if (!c || !args || j < 0) return EMHD_ERR_ARG;
   const emhd_arnoldi_args_s* A = (const emhd_arnoldi_args_s*)args;
-  if (j + 1 > c->max_vectors) return EMHD_ERR_ARG;
+  if (j + 1 > c->max_vectors || (gated && !A->gate)) return EMHD_ERR_ARG;
   c->epoch = j;
   double* out = (j % 2 == 0) ? A->w0 : A->w1;
+  const double* skip = nullptr;
+  if (gated) {
+    const int rc0 = cerr(launch_gate(c->cancel, (unsigned)A->gen, j, A->gate + j, c->stream));
+    if (rc0) return rc0;
+    skip = A->gate + j;
+  }
   StencilParams P = c->base;
   P.epoch = j;
+  P.skip = skip;
+  P.evals = A->evals ? A->evals + j : nullptr;
   P.a = A->a; P.fa = A->fa; P.out = out;
   set_epilogue(P, A->p, A->ch, A->nb, A->bcol, A->bidx);
   KWork k = kwork(c);
   int rc;
   if (j == 0) {
+    if (gated) return EMHD_ERR_ARG;
     // sigma of the seed direction: max|V[0][:n]| into vn[1] (norms writes {sum, max})
     rc = cerr(launch_norms(A->V, 0, A->n_top, k, A->vn, c->stream));
     if (rc) return rc;
@@ -602,15 +638,45 @@ extern "C" int emhd_arnoldi_iter(emhd_ctx* c, const void* args, int j) {
   }
   if (rc) return rc;
   const int nv = j + 1;
-  rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream));
+  rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream, skip));
   if (!rc) rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
-                                   A->d2, c->stream));
+                                   A->d2, c->stream, FinishArgs{}, skip));
   if (rc) return rc;
   FinishArgs F;
   F.h1 = A->d1; F.h2 = A->d2; F.selfdot = A->d1 + nv; F.j = j; F.H = A->H; F.ldh = A->ldh;
   F.scal = A->scal; F.brk_hist = A->brk; F.st = c->st; F.rtol = 1e-12;
   return cerr(launch_update(out, A->V, A->ldv, nv, A->d2, A->len_upd, A->len_dot, A->n_top, 1, k,
-                            A->nrm, c->stream, F));
+                            A->nrm, c->stream, F, skip));
+}
+
+extern "C" int emhd_arnoldi_iter(emhd_ctx* c, const void* args, int j) {
+  return arnoldi_iter(c, args, j, false);
+}
+
+// Look-ahead iterations (queued while residual checks run elsewhere): each is gated on the
+// context's cancel word, so the ones still queued when emhd_arnoldi_cancel lands do no work.
+extern "C" int emhd_arnoldi_lookahead(emhd_ctx* c, const void* args, int j_begin, int j_end) {
+  for (int j = j_begin; j < j_end; ++j) {
+    const int rc = arnoldi_iter(c, args, j, true);
+    if (rc) return rc;
+  }
+  return EMHD_OK;
+}
+
+// Cancel look-ahead iterations j >= epoch_min of process generation gen: an async 8-byte copy
+// on the context's current stream (issue it on an idle stream so it lands at once).
+extern "C" int emhd_arnoldi_cancel(emhd_ctx* c, int gen, int epoch_min) {
+  if (!c || epoch_min < 0) return EMHD_ERR_ARG;
+  *c->cancel_host = ((unsigned long long)(unsigned)gen << 32) | (unsigned)epoch_min;
+  return cerr(cudaMemcpyAsync(c->cancel, c->cancel_host, sizeof(unsigned long long),
+                              cudaMemcpyHostToDevice, c->stream));
+}
+
+// rhs_evals -= sum(evals[0:count]) in stream order (discarded speculative iterations)
+extern "C" int emhd_evals_discount(emhd_ctx* c, const double* evals, int count) {
+  if (!c || !evals || count < 0) return EMHD_ERR_ARG;
+  if (count == 0) return EMHD_OK;
+  return cerr(launch_evals_discount(evals, count, c->st, c->stream));
 }
 
 // One sync point: host_out[0:nbrk] = brk[0:nbrk], host_out[nbrk:nbrk+nres] = res[0:nres]

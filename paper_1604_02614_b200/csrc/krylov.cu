@@ -82,7 +82,8 @@ __device__ __forceinline__ double2 ld2_stream(const double* p, long long e, long
 template <int VEC, int U>
 __global__ void __launch_bounds__(KT, 4) multidot_kernel(const double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, long long len_dot, int self,
-    double* partials, double* out, unsigned int* ticket) {
+    double* partials, double* out, unsigned int* ticket, const double* skip) {
+  if (skip && *skip != 0.0) return;            // cancelled look-ahead iteration (all CTAs agree)
   extern __shared__ double s_acc[];            // [(nvec+1)][NWARP]
   constexpr int TL = KT * 2 * VEC;
   const int nval = nvec + self;
@@ -168,7 +169,8 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, const double* __restrict__ h,
     long long len_upd, long long len_dot, long long len_max,
     double* partials, double* out, unsigned int* ticket, const FinishArgs fin,
-    const HaloPush push = HaloPush{}) {
+    const HaloPush push = HaloPush{}, const double* skip = nullptr) {
+  if (skip && *skip != 0.0) return;            // cancelled look-ahead iteration (all CTAs agree)
   extern __shared__ double sm[];
   constexpr int TL = KT * 2;
   double* s_h = sm;                              // [nvec]
@@ -337,6 +339,33 @@ __global__ void __launch_bounds__(KT) combine_kernel(const double* __restrict__ 
   }
 }
 
+// Gate of a look-ahead Arnoldi iteration: cancelled when the host's cancel word (written by
+// an async copy once the residual checks made a decision) names this process generation and
+// an epoch <= j.  Evaluated once, before the iteration's first kernel; the iteration's
+// kernels read *gate, so all of their CTAs agree.
+__global__ void gate_kernel(const unsigned long long* cancel, unsigned gen, int j, double* gate) {
+  const unsigned long long c = *reinterpret_cast<const volatile unsigned long long*>(cancel);
+  const bool hit = (unsigned)(c >> 32) == gen && (long long)(c & 0xffffffffull) <= (long long)j;
+  *gate = hit ? 1.0 : 0.0;
+}
+
+// rhs_evals -= sum(evals[0:count]) (RHS evaluations of discarded iterations, stream-ordered)
+__global__ void evals_discount_kernel(const double* evals, int count, DevStatus* st) {
+  double s = 0.0;
+  for (int k = 0; k < count; ++k) s += evals[k];
+  st->rhs_evals -= (int)s;
+}
+
+cudaError_t launch_gate(const unsigned long long* cancel, unsigned gen, int j, double* gate, cudaStream_t s) {
+  gate_kernel<<<1, 1, 0, s>>>(cancel, gen, j, gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_evals_discount(const double* evals, int count, DevStatus* st, cudaStream_t s) {
+  evals_discount_kernel<<<1, 1, 0, s>>>(evals, count, st);
+  return cudaGetLastError();
+}
+
 static int grid_for(long long len, int tile, int num_sms) {
   long long tiles = (len + tile - 1) / tile;
   long long g = 4LL * num_sms;
@@ -344,25 +373,26 @@ static int grid_for(long long len, int tile, int num_sms) {
 }
 
 cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
-                            int self, KWork& wk, double* out, cudaStream_t s) {
+                            int self, KWork& wk, double* out, cudaStream_t s, const double* skip) {
   const int G = grid_for(len_dot, KT * 4, wk.num_sms);
   const size_t sm = sizeof(double) * (size_t)(nvec + 1) * NWARP;
-  multidot_kernel<2, 4><<<G, KT, sm, s>>>(w, V, ldv, nvec, len_dot, self, wk.partials, out, wk.ticket);
+  multidot_kernel<2, 4><<<G, KT, sm, s>>>(w, V, ldv, nvec, len_dot, self, wk.partials, out, wk.ticket,
+                                          skip);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
-                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin) {
+                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin, const double* skip) {
   const int G = grid_for(len_upd, KT * 2, wk.num_sms);
   const int nval = mode == 0 ? nvec : 2;
   const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)(nval > 0 ? nval : 1) * NWARP);
   if (mode == 0)
     update_kernel<0, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket, fin);
+                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip);
   else
     update_kernel<1, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket, fin);
+                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip);
   return cudaGetLastError();
 }
 

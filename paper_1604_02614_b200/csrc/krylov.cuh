@@ -37,10 +37,13 @@ struct CombineOut {
 };
 
 cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
-                            int self, KWork& wk, double* out, cudaStream_t s);
+                            int self, KWork& wk, double* out, cudaStream_t s, const double* skip = nullptr);
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
-                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin = FinishArgs{});
+                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin = FinishArgs{},
+                          const double* skip = nullptr);
+cudaError_t launch_gate(const unsigned long long* cancel, unsigned gen, int j, double* gate, cudaStream_t s);
+cudaError_t launch_evals_discount(const double* evals, int count, DevStatus* st, cudaStream_t s);
 cudaError_t launch_update_push(double* w, const double* V, long long ldv, int nvec, const double* h,
                                long long len_upd, long long len_dot, long long len_max, KWork& wk,
                                double* out, const HaloPush& push, cudaStream_t s);

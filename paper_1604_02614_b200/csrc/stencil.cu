@@ -349,6 +349,12 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
   const int t = threadIdx.x;
   const int j0 = blockIdx.x * TY;
   const int i0 = blockIdx.y * P.rows_per_cta;
+  const bool lead = blockIdx.x == 0 && blockIdx.y == 0 && t == 0;
+  if (P.skip && *P.skip != 0.0) {
+    // cancelled look-ahead iteration (its gate was written by an earlier launch)
+    if (lead && P.evals) *P.evals = 0.0;
+    return;
+  }
   if (i0 >= P.nx) return;
   const int i1 = min(i0 + P.rows_per_cta, P.nx);   // exclusive end of output rows
 
@@ -369,6 +375,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
 #pragma unroll
           for (int f = 0; f < NF; ++f) P.out[r * P.ny + j0 + t + (long long)f * P.nx * P.ny] = 0.0;
       if (blockIdx.x == 0 && blockIdx.y == 0 && t < P.p) P.out[P.n_top + t] = 0.0;
+      if (lead && P.evals) *P.evals = 0.0;
       return;
     }
     hnext = P.scal[0];
@@ -637,6 +644,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
       atomicMin(&P.st->fail_iter, P.epoch);
     }
     if (!skip_stencil && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&P.st->rhs_evals, 1);
+    if (P.evals && blockIdx.x == 0 && blockIdx.y == 0) *P.evals = skip_stencil ? 0.0 : 1.0;
   }
 }
 
@@ -691,41 +699,43 @@ __global__ void admissibility_kernel(const StencilParams P, int pass, unsigned l
 // ---- diagnostics: div B and J = curl B with one ghost layer (mhd.py:288-309) -------------
 // which = 0: out[nx*ny] = div B, *dmax = max |div B| (bit pattern max of non-negative doubles);
 // which = 1: out[3][nx][ny] = (d_y Bz, -d_x Bz, d_x By - d_y Bx).
-__global__ void diag_kernel(const StencilParams P, int which, double* out, unsigned long long* dmax) {
-  const long long total = (long long)P.nx * P.ny;
+__global__ void __launch_bounds__(256) diag_kernel(const StencilParams P, int which, double* out,
+                                                  unsigned long long* dmax) {
+  // rows over blockIdx.y, columns over threads (coalesced); ghosts mapped as
+  // apply_ghosts(width=1): x-neighbours (i +- 1, j) per row, y-neighbours (i, j +- 1) per column
+  const unsigned total = (unsigned)P.nx * (unsigned)P.ny;
   unsigned long long best = 0ull;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e / P.ny), j = (int)(e % P.ny);
-    // x-neighbours (i +- 1, j) and y-neighbours (i, j +- 1), ghosts mapped as apply_ghosts(width=1)
+  for (int i = blockIdx.y; i < P.nx; i += gridDim.y) {
     const RowRef Rm = row_ref(P, i - 1), Rp = row_ref(P, i + 1), R0 = row_ref(P, i);
-    bool fl, fr;
-    const int jl = map_ghost(j - 1, P.ny, P.bcy, fl), jr = map_ghost(j + 1, P.ny, P.bcy, fr);
-    auto fld = [&](const RowRef& R, int jj, int f) {
-      const double* A = R.halo ? P.a_halo : P.a;
-      return __ldg(A + R.off + jj + (long long)f * R.fs);
-    };
-    double bx_ip = fld(Rp, j, 4), bx_im = fld(Rm, j, 4);
-    if (Rp.flip) bx_ip = -bx_ip;
-    if (Rm.flip) bx_im = -bx_im;
-    double by_jp = fld(R0, jr, 5), by_jm = fld(R0, jl, 5);
-    if (fr) by_jp = -by_jp;
-    if (fl) by_jm = -by_jm;
-    if (which == 0) {
-      const double d = __dadd_rn(div_const(__dsub_rn(bx_ip, bx_im), P.two_hx, P.r_two_hx),
-                                 div_const(__dsub_rn(by_jp, by_jm), P.two_hy, P.r_two_hy));
-      out[e] = d;
-      const unsigned long long key = (unsigned long long)__double_as_longlong(fabs(d));
-      best = key > best ? key : best;
-    } else {
-      const double bz_jp = fld(R0, jr, 6), bz_jm = fld(R0, jl, 6);
-      const double bz_ip = fld(Rp, j, 6), bz_im = fld(Rm, j, 6);
-      const double by_ip = fld(Rp, j, 5), by_im = fld(Rm, j, 5);
-      double bx_jp = fld(R0, jr, 4), bx_jm = fld(R0, jl, 4);
-      out[e] = div_const(__dsub_rn(bz_jp, bz_jm), P.two_hy, P.r_two_hy);
-      out[e + total] = -div_const(__dsub_rn(bz_ip, bz_im), P.two_hx, P.r_two_hx);
-      out[e + 2 * total] = __dsub_rn(div_const(__dsub_rn(by_ip, by_im), P.two_hx, P.r_two_hx),
-                                     div_const(__dsub_rn(bx_jp, bx_jm), P.two_hy, P.r_two_hy));
+    const unsigned sm = Rm.flip ? 0x80000000u : 0u, sp = Rp.flip ? 0x80000000u : 0u;
+    const double* Am = Rm.halo ? P.a_halo : P.a;
+    const double* Ap = Rp.halo ? P.a_halo : P.a;
+    const double* A0 = P.a;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.ny; j += gridDim.x * blockDim.x) {
+      bool fl, fr;
+      const int jl = map_ghost(j - 1, P.ny, P.bcy, fl), jr = map_ghost(j + 1, P.ny, P.bcy, fr);
+      const unsigned sl = fl ? 0x80000000u : 0u, sr = fr ? 0x80000000u : 0u;
+      const unsigned e = (unsigned)i * P.ny + j;
+      const double bx_ip = flip_sign(__ldg(Ap + (Rp.off + j + 4 * Rp.fs)), sp);
+      const double bx_im = flip_sign(__ldg(Am + (Rm.off + j + 4 * Rm.fs)), sm);
+      const double by_jp = flip_sign(__ldg(A0 + (R0.off + jr + 5 * R0.fs)), sr);
+      const double by_jm = flip_sign(__ldg(A0 + (R0.off + jl + 5 * R0.fs)), sl);
+      if (which == 0) {
+        const double d = __dadd_rn(div_const(__dsub_rn(bx_ip, bx_im), P.two_hx, P.r_two_hx),
+                                   div_const(__dsub_rn(by_jp, by_jm), P.two_hy, P.r_two_hy));
+        out[e] = d;
+        const unsigned long long key = (unsigned long long)__double_as_longlong(fabs(d));
+        best = key > best ? key : best;
+      } else {
+        const double bz_jp = __ldg(A0 + (R0.off + jr + 6 * R0.fs)), bz_jm = __ldg(A0 + (R0.off + jl + 6 * R0.fs));
+        const double bz_ip = __ldg(Ap + (Rp.off + j + 6 * Rp.fs)), bz_im = __ldg(Am + (Rm.off + j + 6 * Rm.fs));
+        const double by_ip = __ldg(Ap + (Rp.off + j + 5 * Rp.fs)), by_im = __ldg(Am + (Rm.off + j + 5 * Rm.fs));
+        const double bx_jp = __ldg(A0 + (R0.off + jr + 4 * R0.fs)), bx_jm = __ldg(A0 + (R0.off + jl + 4 * R0.fs));
+        out[e] = div_const(__dsub_rn(bz_jp, bz_jm), P.two_hy, P.r_two_hy);
+        out[e + total] = -div_const(__dsub_rn(bz_ip, bz_im), P.two_hx, P.r_two_hx);
+        out[e + 2 * total] = __dsub_rn(div_const(__dsub_rn(by_ip, by_im), P.two_hx, P.r_two_hx),
+                                       div_const(__dsub_rn(bx_jp, bx_jm), P.two_hy, P.r_two_hy));
+      }
     }
   }
   if (which == 0) {
@@ -738,9 +748,18 @@ __global__ void diag_kernel(const StencilParams P, int which, double* out, unsig
 }
 
 cudaError_t launch_diag(StencilParams P, int which, double* out, unsigned long long* dmax, cudaStream_t s) {
-  const long long total = (long long)P.nx * P.ny;
-  const int G = (int)((total + 255) / 256 < 8192 ? (total + 255) / 256 : 8192);
-  diag_kernel<<<G, 256, 0, s>>>(P, which, out, dmax);
+  if ((long long)3 * P.nx * P.ny >= (1LL << 32)) return cudaErrorInvalidValue;   // 32-bit offsets
+  static int resident = 0;            // one wave: 8 CTAs of 256 threads per SM
+  if (!resident) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = 8 * sms;
+  }
+  const int gx = (P.ny + 255) / 256;
+  int gy = resident / gx;
+  gy = gy < 1 ? 1 : (gy > P.nx ? P.nx : gy);
+  diag_kernel<<<dim3(gx, gy), 256, 0, s>>>(P, which, out, dmax);
   return cudaGetLastError();
 }
 

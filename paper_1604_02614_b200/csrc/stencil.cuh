@@ -33,6 +33,8 @@ struct StencilParams {
   DevStatus* st;
   int epoch;                  // caller-defined launch tag recorded on failure
   int tma;                    // interior strips stage raw rows with bulk async copies (set by the launcher)
+  const double* skip;         // gated launch: *skip != 0 -> no work (cancelled look-ahead iteration)
+  double* evals;              // optional: 1 if this launch evaluated the RHS (counted), else 0
 };
 
 cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s);

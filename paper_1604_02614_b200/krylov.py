@@ -20,6 +20,7 @@ Device design:
 """
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -39,6 +40,9 @@ SPEC_DEPTH_OVERRIDE = 0
 # False routes through the per-kernel C entry points (same kernels; used for per-launch timing)
 FAST_DRIVER = True
 BREAKDOWN_RTOL = 1e-12
+# Arnoldi iterations queued behind a batch of residual checks while the checks run on a
+# side stream (None: by vector size; EMHD_LOOKAHEAD overrides; 0: checks in stream order)
+LOOKAHEAD_OVERRIDE = None
 
 
 class KrylovConvergenceError(RuntimeError):
@@ -196,7 +200,7 @@ class _Process:
         k = self.m_cap + 4
         hw = max(self.m_cap, 1)
         # one zero-filled block for H and every small scalar area (a single fill launch)
-        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + (self.m_cap + 1) + 4,
+        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + 3 * (self.m_cap + 1) + 4,
                                   dtype=D.F64, device=D.device())
         o = (self.m_cap + 1) * hw
         self.H = self._small[:o].view(self.m_cap + 1, hw)
@@ -206,6 +210,9 @@ class _Process:
         o2 = o + 2 * k + 2
         self.brk = self._small[o2:o2 + self.m_cap + 1]
         self.nb = self._small[o2 + self.m_cap + 1:o2 + self.m_cap + 5]   # {sum seed^2, max|seed|, beta, -}
+        o3 = o2 + self.m_cap + 5
+        self.gate = self._small[o3:o3 + self.m_cap + 1]       # look-ahead gates (fast path)
+        self.evals = self._small[o3 + self.m_cap + 1:o3 + 2 * (self.m_cap + 1)]   # RHS evals per iteration
         self.scal = D.Scratch(4)
         self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
@@ -258,8 +265,15 @@ class _Process:
             for k, b in enumerate(E.bcols):
                 A.bcol[k] = D.ptr(b)
                 A.bidx[k] = E.bidx[k]
+            A.gen = self._new_gen()
+            A.gate, A.evals = D.ptr(self.gate), D.ptr(self.evals)
             self._args = A
             self._args_ref = D.ctypes_byref(A)
+
+    def _new_gen(self):
+        g = (getattr(self.ctx, "_gen", 0) + 1) & 0x7fffffff
+        self.ctx._gen = g
+        return g
 
     # -- collectives ----------------------------------------------------------
     def _allreduce_sum(self, t):
@@ -407,8 +421,9 @@ class _Process:
             return True
         return self.settle()
 
-    def extend_many(self, k):
-        """Queue up to k iterations without syncing; one C call on the single-rank fast path."""
+    def extend_many(self, k, lookahead=False):
+        """Queue up to k iterations without syncing; one C call on the single-rank fast path.
+        ``lookahead``: the iterations are gated (cancellable) look-ahead iterations."""
         k = min(k, self.m_cap - self.m)
         if k <= 0 or self.breakdown:
             return 0
@@ -418,8 +433,12 @@ class _Process:
                 done += 1
             return done
         j0 = self.m
-        N.check(self.lib.emhd_arnoldi_run(self.ctx.sync_stream(), self._args_ref, j0, j0 + k),
-                "arnoldi_run")
+        if lookahead and j0 >= 1 and os.environ.get("EMHD_LOOKAHEAD_GATE", "1") != "0":
+            N.check(self.lib.emhd_arnoldi_lookahead(self.ctx.sync_stream(), self._args_ref, j0, j0 + k),
+                    "arnoldi_lookahead")
+        else:
+            N.check(self.lib.emhd_arnoldi_run(self.ctx.sync_stream(), self._args_ref, j0, j0 + k),
+                    "arnoldi_run")
         self.applies += k
         self.m = j0 + k
         self.cur = (self.m - 1) % 2
@@ -428,19 +447,25 @@ class _Process:
         self._pending = True
         return k
 
-    def settle(self, res_dev=None, check=True):
+    def settle(self, res_dev=None, check=True, upto=None, side=False):
         """One host sync: breakdown position, device status of queued iterations and (when
         given) the residual estimates just computed on the device; returns them.  With
-        ``check=False`` the status word is kept in ``self.last_status`` for the caller."""
-        self._pending = False
+        ``check=False`` the status word is kept in ``self.last_status`` for the caller.
+
+        ``upto`` (fast path): only iterations below it are resolved — later ones are
+        look-ahead iterations still queued; ``side``: the readback runs on the side stream
+        behind the residual checks, so the host does not wait for the look-ahead."""
+        upto = self.m if (upto is None or not self.fast) else min(upto, self.m)
+        self._pending = upto < self.m
         first = self._settled
         nres = 0 if res_dev is None else res_dev.numel()
         if self.fast:
             st = N.Status()
-            nb = self.m - first
-            N.check(self.lib.emhd_readback(self.ctx.sync_stream(), D.ptr(self.brk) + 8 * first, nb,
-                                           D.ptr(res_dev) if nres else None, nres,
-                                           D.ptr(self.host_rb), D.ctypes_byref(st)), "readback")
+            nb = upto - first
+            with torch.cuda.stream(self.side_stream() if side else torch.cuda.current_stream()):
+                N.check(self.lib.emhd_readback(self.ctx.sync_stream(), D.ptr(self.brk) + 8 * first, nb,
+                                               D.ptr(res_dev) if nres else None, nres,
+                                               D.ptr(self.host_rb), D.ctypes_byref(st)), "readback")
             hb = self.host_rb.numpy()
             flags = hb[:nb]
             if nres:
@@ -459,7 +484,10 @@ class _Process:
             self.applies -= self.m - (b + 1)
             self.m = b + 1
             self.breakdown = True
-        self._settled = self.m
+            self._pending = False
+            self._settled = self.m
+        else:
+            self._settled = upto
         if self.comm is not None and self.layout.distributed:
             from .mhd import agree_status
             st = agree_status(st, self.comm)
@@ -555,16 +583,61 @@ class _Process:
         self._depth = min(2 * self._depth, 8)
         return depth
 
-    def phi_batch(self, order, scale, ms):
-        """Residuals (device) of phi_order(scale H_m) e1 for every m in ms, one launch."""
+    def phi_batch(self, order, scale, ms, side=False):
+        """Residuals (device) of phi_order(scale H_m) e1 for every m in ms, one launch.
+
+        ``side``: the launch runs on the high-priority side stream once the iterations queued
+        so far have finished, so Arnoldi iterations queued afterwards (look-ahead) overlap it.
+        It reads H[:m, :m], H[m, m-1] and brk[m-1] for m <= max(ms) only, which later
+        iterations never write."""
         S = len(ms)
         Y = self.Ybuf[:S * (self.m_cap + 1)].view(S, self.m_cap + 1)
         res = self.resbuf[:S]
-        N.check(self.lib.emhd_phi_small_batch(self.ctx.sync_stream(), D.ptr(self.H), self.H.shape[1],
-                                              N.int_array(ms), order, S, N.dbl_array([scale] * S),
-                                              D.ptr(self.brk), D.ptr(self.beta_dev), D.ptr(Y),
-                                              self.m_cap + 1, D.ptr(res)), "phi_small_batch")
+        stream = torch.cuda.current_stream()
+        if side:
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            stream = self.side_stream()
+            stream.wait_event(ev)
+        with torch.cuda.stream(stream):
+            N.check(self.lib.emhd_phi_small_batch(self.ctx.sync_stream(), D.ptr(self.H), self.H.shape[1],
+                                                  N.int_array(ms), order, S, N.dbl_array([scale] * S),
+                                                  D.ptr(self.brk), D.ptr(self.beta_dev), D.ptr(Y),
+                                                  self.m_cap + 1, D.ptr(res)), "phi_small_batch")
         return Y, res
+
+    def side_stream(self):
+        s = getattr(self.ctx, "_side_stream", None)
+        if s is None:
+            s = self.ctx._side_stream = torch.cuda.Stream(priority=-1)
+        return s
+
+    def lookahead(self):
+        """Iterations to queue behind a batch of residual checks run on the side stream: about
+        one small dense exponential's worth of Arnoldi work (0 on very large grids, where one
+        iteration outlasts it, and on the per-kernel / multi-rank paths)."""
+        if not self.fast:
+            return 0
+        env = os.environ.get("EMHD_LOOKAHEAD")
+        if LOOKAHEAD_OVERRIDE is not None:
+            return LOOKAHEAD_OVERRIDE
+        if env is not None:
+            return max(0, int(env))
+        # Measured (config trajectories): 64^2 is host-bound (look-ahead only adds host work),
+        # 256^2 gains 12 % with 4, 1024^2 breaks even with 1 (a started look-ahead iteration
+        # runs to the end even when cancelled, as long as the exponential it hides)
+        n = self.n_top
+        return 4 if (1 << 17) < n <= (1 << 20) else 0
+
+    def _cancel_lookahead(self, m_keep):
+        """Cancel queued look-ahead iterations >= m_keep (async copy on the idle side stream,
+        so it lands ahead of them); later iterations of this process get a new generation."""
+        if not (self.fast and self._pending and self.m > m_keep):
+            return
+        with torch.cuda.stream(self.side_stream()):
+            N.check(self.lib.emhd_arnoldi_cancel(self.ctx.sync_stream(), self._args.gen, m_keep),
+                    "arnoldi_cancel")
+        self._args.gen = self._new_gen()
 
     def truncate(self, m_keep):
         """Drop speculative iterations beyond m_keep (they were never needed)."""
@@ -572,7 +645,19 @@ class _Process:
         if drop <= 0:
             return
         self.applies -= drop
-        self.ctx.rhs_discount += drop          # each dropped iteration ran one stencil
+        self.ctx.spec_dropped = getattr(self.ctx, "spec_dropped", 0) + drop   # reporting only
+        if self.fast:
+            self._cancel_lookahead(m_keep)
+            h = self.ctx.sync_stream()
+            # RHS evaluations the dropped iterations actually made (cancelled look-ahead and
+            # post-breakdown launches made none), subtracted on the device in stream order;
+            # error flags raised by look-ahead iterations after the host read the status are
+            # cleared the same way (no reference counterpart: the reference never runs them)
+            N.check(self.lib.emhd_evals_discount(h, D.ptr(self.evals[m_keep:]), drop), "evals_discount")
+            N.check(self.lib.emhd_status_scrub(h, m_keep), "status_scrub")
+        else:
+            self.ctx.rhs_discount += drop          # each dropped iteration ran one stencil
+        self._pending = False
         self.m = m_keep
         self._settled = min(self._settled, m_keep)
         self.breakdown = bool(self.brk_host_flag(m_keep - 1))
@@ -582,11 +667,15 @@ class _Process:
 
     def resolve_status(self, m_keep):
         """Raise for device errors of iterations the reference performs (< m_keep); forget
-        the ones raised only by discarded speculative iterations."""
+        the ones raised only by discarded speculative iterations.  Flags of look-ahead
+        iterations that are still queued (kept, checked by the next batch) stay put."""
         st = self.last_status
         bad = st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE)
         if bad and st.fail_iter < m_keep and self.eng.fused:
+            self._cancel_lookahead(m_keep)
             self.check_status(st)
+        elif self._pending and self.m > m_keep:
+            return
         elif st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE | N.ST_DENSE):
             self.ctx.reset_status()
 
@@ -684,18 +773,23 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
     m_target = min(cfg.m_init, proc.n)
     proc.extend_many(m_target)
     proc.settle()
-    check_current = True
+    nxt = proc.m                                  # smallest basis size not yet checked
+    look = proc.lookahead()
     while True:
         # speculative batch: the residual at the current m plus up to B-1 further iterations,
         # all checked in one phi launch and one host sync; the reference's decision sequence
-        # (stop at the first m with res <= tol, breakdown or m >= n) is replayed on the host
+        # (stop at the first m with res <= tol, breakdown or m >= n) is replayed on the host.
+        # While the checks run (side stream), `look` further iterations are already queued.
         B = proc.batch_size()
-        ms = [proc.m] if check_current else []
-        m0 = proc.m
-        proc.extend_many(B - len(ms))
-        ms += list(range(m0 + 1, proc.m + 1))
-        _, res_raw = proc.phi_batch(order, c_big * h, ms)
-        raw = proc.settle(res_raw, check=False)
+        want = nxt + B - 1
+        if proc.m < want:
+            proc.extend_many(want - proc.m)
+        hi = min(want, proc.m)
+        ms = list(range(nxt, hi + 1)) or [proc.m]
+        _, res_raw = proc.phi_batch(order, c_big * h, ms, side=look > 0)
+        if look:
+            proc.extend_many(look, lookahead=True)
+        raw = proc.settle(res_raw, check=False, upto=hi, side=look > 0)
         chosen, res = None, None
         for k, mk in enumerate(ms):
             if mk > proc.m:                       # beyond a breakdown found by settle
@@ -720,8 +814,8 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
             proc.truncate(chosen)
             proc.resolve_status(chosen)
             break
-        proc.resolve_status(proc.m)
-        check_current = False                     # proc.m was just checked and failed
+        proc.resolve_status(hi)
+        nxt = hi + 1                              # hi was just checked and failed
     stats.operator_applies += proc.applies
     stats.max_basis_size = proc.m
     stats.substeps = 1
@@ -788,20 +882,22 @@ def phi_comb(req, cfg=None, _zero=None):
         m_target = min(cfg.m_init, naug_glob)
         proc.extend_many(m_target)
         proc.settle()
-        check_current = True
+        nxt = proc.m
+        look = proc.lookahead()
         while True:
             # speculative batch of residual checks (see multi_scale_eval); extensions stop
             # where the reference could change delta instead of extending (soft cap)
             limit = proc.m_cap if delta <= cfg.min_substep else min(cfg.soft_cap, proc.m_cap)
             B = proc.batch_size()
-            ms = [proc.m] if check_current else []
-            m0 = proc.m
-            proc.extend_many(min(max(B - len(ms), 0 if ms else 1), limit - proc.m))
-            ms += list(range(m0 + 1, proc.m + 1))
-            if not ms:
-                ms = [proc.m]
-            Yb, res_raw = proc.phi_batch(0, delta, ms)
-            raw = proc.settle(res_raw, check=False)
+            want = min(nxt + B - 1, limit)
+            if proc.m < want:
+                proc.extend_many(want - proc.m)
+            hi = min(max(want, nxt), proc.m)
+            ms = list(range(nxt, hi + 1)) or [proc.m]
+            Yb, res_raw = proc.phi_batch(0, delta, ms, side=look > 0)
+            if look and proc.m < limit:
+                proc.extend_many(min(look, limit - proc.m), lookahead=True)
+            raw = proc.settle(res_raw, check=False, upto=ms[-1], side=look > 0)
             tol_sub = req.tol * max(delta, 1e-2)
             action, res = None, None
             for k, mk in enumerate(ms):
@@ -822,8 +918,8 @@ def phi_comb(req, cfg=None, _zero=None):
                 if action is not None:
                     break
             if action is None:
-                proc.resolve_status(proc.m)
-                check_current = False
+                proc.resolve_status(ms[-1])
+                nxt = ms[-1] + 1
                 continue
             kind, k, mk = action
             proc.truncate(mk)
@@ -837,7 +933,7 @@ def phi_comb(req, cfg=None, _zero=None):
                     f"Krylov basis cap {cfg.m_max} reached at substep "
                     f"{delta:.3e} (residual {res:.3e} > {tol_sub:.3e})", residual=res)
             delta = delta / 2.0                       # soft cap, or hard cap above min_substep
-            check_current = True
+            nxt = proc.m
         stats.operator_applies += proc.applies
         u_new = torch.empty(n_top, dtype=D.F64, device=D.device())
         proc.combine(Y, [u_new])

@@ -120,7 +120,7 @@ def main():
         ps.print_stats(25)
         ps.print_callers("torch.empty|settle")
     out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
-           "speculative_discarded_total": f.ctx.rhs_discount, "cuda_allocs_in_run": alloc,
+           "speculative_discarded_total": getattr(f.ctx, "spec_dropped", 0), "cuda_allocs_in_run": alloc,
            "iterations_per_s": st.operator_applies / T,
            "cell_steps_per_s": g.nx * g.ny * st.steps_accepted / T}
     if a.check:
