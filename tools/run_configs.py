@@ -107,6 +107,7 @@ def main():
         prof = cProfile.Profile()
         prof.enable()
     ms0 = torch.cuda.memory_stats()
+    drop0 = getattr(f.ctx, "spec_dropped", 0)
     t0 = time.perf_counter()
     y, st = go(f, yd)
     torch.cuda.synchronize()
@@ -120,7 +121,7 @@ def main():
         ps.print_stats(25)
         ps.print_callers("torch.empty|settle")
     out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
-           "speculative_discarded_total": getattr(f.ctx, "spec_dropped", 0), "cuda_allocs_in_run": alloc,
+           "speculative_discarded": getattr(f.ctx, "spec_dropped", 0) - drop0, "cuda_allocs_in_run": alloc,
            "iterations_per_s": st.operator_applies / T,
            "cell_steps_per_s": g.nx * g.ny * st.steps_accepted / T}
     if a.check:
