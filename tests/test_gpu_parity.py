@@ -474,3 +474,76 @@ def test_rhs_preserves_discrete_divergence(P):
     dB[4:7] = dU[4:7]
     _, peak = P.div_B(dB, g, bc)
     assert peak <= 1e-14
+
+
+# --------------------------------------- look-ahead residual checks (forced on small grids)
+
+@pytest.fixture
+def lookahead4():
+    from paper_1604_02614_b200 import krylov
+    old = krylov.LOOKAHEAD_OVERRIDE
+    krylov.LOOKAHEAD_OVERRIDE = 4
+    yield
+    krylov.LOOKAHEAD_OVERRIDE = old
+
+
+def test_lookahead_config0_trajectory_matches_reference(P, lookahead4):
+    """Config 0 with 4 cancellable look-ahead iterations behind every batch of residual
+    checks: same trajectory and the reference's counters (discarded iterations, cancelled or
+    not, leave no trace in RHS counts)."""
+    z = golden("config0_recon64.npz")
+    with open(os.path.join(GOLDEN, "config0_stats.json")) as fh:
+        st = json.load(fh)["run20"]
+    g = P.ReconnectionSpec().grid(64, 64)
+    f = P.make_rhs(P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3), g, P.default_bc("reconnection"))
+    dropped0 = getattr(f.ctx, "spec_dropped", 0)
+    y, S = P.integrate_fixed("epirk4", f, z["U0"].reshape(-1), 0.0, 2.0, 0.1, tol_krylov=1e-10)
+    assert np.linalg.norm(y - z["y20"]) <= 1e-8 * np.linalg.norm(z["y20"])
+    for k, v in st.items():
+        assert getattr(S, k) == v, k
+    assert getattr(f.ctx, "spec_dropped", 0) > dropped0      # look-ahead iterations were discarded
+
+
+def test_lookahead_epirk5p1_adaptive_matches_reference(P, lookahead4):
+    z = golden("epirk5p1_kh32.npz")
+    with open(os.path.join(GOLDEN, "epirk5p1_kh32.json")) as fh:
+        st = json.load(fh)
+    from paper_1604_02614_b200.problems import kh_shear_grid
+    g = kh_shear_grid(32)
+    f = P.make_rhs(P.MhdParams(mu=1e-4, eta=1e-4, kappa=1e-4), g, P.BoundaryPolicy("periodic", "reflect"))
+    y, S = P.integrate_adaptive(f, z["U0"].reshape(-1), 0.0, 0.05, P.StepController(tol=1e-6))
+    assert np.linalg.norm(y - z["y"]) <= 1e-8 * np.linalg.norm(z["y"])
+    for k, v in st.items():
+        assert getattr(S, k) == v, k
+
+
+def test_lookahead_projection_equals_stream_ordered(P):
+    """One multi-scale projection and one phi_comb of an MHD Jacobian, look-ahead 0 vs 4:
+    identical basis sizes, applies and device RHS counts, results within round-off."""
+    from paper_1604_02614_b200 import krylov
+    g = P.ReconnectionSpec().grid(64, 64)
+    prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    f = P.make_rhs(prm, g, P.default_bc("reconnection"))
+    y = P.reconnection_ic(g, params=prm).reshape(-1)
+    op = P.FdJacobianOperator(f, dev(y))
+    v = f(dev(y))
+    out = {}
+    old = krylov.LOOKAHEAD_OVERRIDE
+    try:
+        for L in (0, 4):
+            krylov.LOOKAHEAD_OVERRIDE = L
+            ev0 = f.ctx.status().rhs_evals
+            d0 = f.ctx.rhs_discount
+            ys, s1 = P.multi_scale_eval(op, 0.5, v, [0.5, 1.0], 1e-10)
+            req = P.PhiCombRequest(operator=op, h=0.5, c=1.0, vectors=[v, 0.5 * v], tol=1e-10)
+            w, s2 = P.phi_comb(req)
+            evals = f.ctx.status().rhs_evals - ev0 - (f.ctx.rhs_discount - d0)
+            out[L] = (ys, w, (s1.operator_applies, s1.max_basis_size, s2.operator_applies,
+                              s2.max_basis_size, s2.substeps), evals)
+    finally:
+        krylov.LOOKAHEAD_OVERRIDE = old
+    assert out[0][2] == out[4][2]
+    assert out[0][3] == out[4][3]
+    for a, b in zip(out[0][0], out[4][0]):
+        assert torch.linalg.norm(a - b).item() <= 1e-12 * torch.linalg.norm(a).item()
+    assert torch.linalg.norm(out[0][1] - out[4][1]).item() <= 1e-12 * torch.linalg.norm(out[0][1]).item()
