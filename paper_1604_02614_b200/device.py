@@ -8,15 +8,28 @@ from . import _native as N
 F64 = torch.float64
 
 
+_CUDA_OK = False
+_DEVICES = {}
+
+
 def require_cuda():
+    global _CUDA_OK
+    if _CUDA_OK:
+        return
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1604_02614_b200 needs a CUDA device (sm_100a); "
                            "there is no CPU fallback")
+    _CUDA_OK = True
 
 
 def device():
+    # hot on small grids: one cached torch.device per device index, no availability probe
     require_cuda()
-    return torch.device("cuda", torch.cuda.current_device())
+    i = torch._C._cuda_getDevice()
+    d = _DEVICES.get(i)
+    if d is None:
+        d = _DEVICES[i] = torch.device("cuda", i)
+    return d
 
 
 def is_host(x):
@@ -53,7 +66,8 @@ def ptr(t):
 
 
 def stream_handle():
-    return torch.cuda.current_stream().cuda_stream
+    # the raw cudaStream_t of torch's current stream (no Stream object per call)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 class Scratch:

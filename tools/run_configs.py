@@ -117,8 +117,8 @@ def main():
     if prof is not None:
         prof.disable()
         import pstats
-        ps = pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime")
-        ps.print_stats(25)
+        ps = pstats.Stats(prof, stream=sys.stderr).sort_stats(os.environ.get("PROF_SORT", "tottime"))
+        ps.print_stats(int(os.environ.get("PROF_N", "25")))
         ps.print_callers("torch.empty|settle")
     out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
            "speculative_discarded": getattr(f.ctx, "spec_dropped", 0) - drop0, "cuda_allocs_in_run": alloc,
