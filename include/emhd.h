@@ -126,6 +126,23 @@ int emhd_multidot(emhd_ctx* ctx, const double* w, const double* V, long long ldv
  * mode 1: out = {sum w^2 over len_dot, max|w| over len_max} */
 int emhd_update(emhd_ctx* ctx, double* w, const double* V, long long ldv, int nvec, const double* h,
                 long long len_upd, long long len_dot, long long len_max, int mode, double* out);
+/* mode 0 writes nvec + 2 values: V^T w_new, then ||w_new||^2 (over len_dot) and max|w_new|
+ * (over len_max) — the inputs of the selective re-orthogonalisation test below. */
+/* Selective (DGKS) re-orthogonalisation after pass 1 (r = emhd_update mode-0 output,
+ * all-reduced on slab ranks): when ||w1|| >= eta ||w|| (||w||^2 = *selfdot) set *gate = 1 and
+ * finish column j with h1 alone (H, hnext = ||w1||, breakdown test, scal), else *gate = 0.
+ * The reference always runs the second pass (krylov.py:156-160); skipping it when the first
+ * left w1 orthogonal to working precision changes H and V at round-off level only. */
+int emhd_reorth_decide(emhd_ctx* ctx, const double* h1, const double* r, int nvec,
+                       const double* selfdot, int j, double* H, long long ldh, double* scal,
+                       double* brk_hist, double eta, double* gate);
+/* the next pass-2 launch on ctx (emhd_update mode 1, emhd_update_finish, emhd_update_push,
+ * emhd_arnoldi_finish) does no work when *gate != 0 (device-side test) */
+int emhd_skip_next(emhd_ctx* ctx, const double* gate);
+/* slab ranks: rows {0,1} / {nx-2,nx-1} of w into the lo / hi neighbours' halo buffers (peer
+ * pointers, NULL = none) when *gate != 0 (gate NULL: always) — the halo push of an iteration
+ * whose second pass was skipped (emhd_update_push does it otherwise) */
+int emhd_push_edges(emhd_ctx* ctx, const double* w, double* lo_halo, double* hi_halo, const double* gate);
 /* emhd_update(mode 1) + emhd_arnoldi_finish in one launch (single rank: the norms need no
  * all-reduce before the column bookkeeping). */
 int emhd_update_finish(emhd_ctx* ctx, double* w, const double* V, long long ldv, int nvec,

@@ -30,7 +30,15 @@ struct emhd_ctx {
   int epoch = 0;
   unsigned long long* cancel = nullptr;       // look-ahead cancel word {generation, epoch}
   unsigned long long* cancel_host = nullptr;  // pinned source of its async updates
+  const double* skip_next = nullptr;          // emhd_skip_next: gate of the next pass-2 launch
 };
+
+// the gate set by emhd_skip_next, consumed by exactly one pass-2 launch
+static const double* take_skip(emhd_ctx* c) {
+  const double* g = c->skip_next;
+  c->skip_next = nullptr;
+  return g;
+}
 
 static int cerr(cudaError_t e) {
   if (e == cudaSuccess) return EMHD_OK;
@@ -243,7 +251,33 @@ extern "C" int emhd_update(emhd_ctx* c, double* w, const double* V, long long ld
                            long long len_upd, long long len_dot, long long len_max, int mode, double* out) {
   if (!c || !w || !out || nvec < 0 || nvec > c->max_vectors || (nvec > 0 && (!V || !h))) return EMHD_ERR_ARG;
   KWork k = kwork(c);
-  return cerr(launch_update(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode, k, out, c->stream));
+  const double* g = mode == 1 ? take_skip(c) : nullptr;
+  Reorth ro{};
+  ro.skip2 = g;
+  return cerr(launch_update(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode, k, out, c->stream,
+                            FinishArgs{}, nullptr, ro));
+}
+
+// Selective re-orthogonalisation decision after an (all-reduced) mode-0 update: r = {V^T w1
+// (nvec), ||w1||^2, max|w1_top|}; gate = 1 and the column finished with h1 when
+// ||w1||^2 >= eta^2 selfdot, else gate = 0 (the second pass must run).
+extern "C" int emhd_reorth_decide(emhd_ctx* c, const double* h1, const double* r, int nvec,
+                                  const double* selfdot, int j, double* H, long long ldh, double* scal,
+                                  double* brk_hist, double eta, double* gate) {
+  if (!c || !h1 || !r || !selfdot || !H || !scal || !gate || nvec < 1 || j < 0 || !(eta > 0.0))
+    return EMHD_ERR_ARG;
+  FinishArgs F;
+  F.h1 = h1; F.h2 = nullptr; F.selfdot = selfdot; F.j = j; F.H = H; F.ldh = ldh; F.scal = scal;
+  F.brk_hist = brk_hist; F.st = c->st; F.rtol = 1e-12;
+  return cerr(launch_reorth_decide(F, r, nvec, eta * eta, gate, c->stream));
+}
+
+// The next pass-2 launch on this context (emhd_update mode 1, emhd_update_finish,
+// emhd_update_push or emhd_arnoldi_finish) does no work when *gate != 0 (device-side).
+extern "C" int emhd_skip_next(emhd_ctx* c, const double* gate) {
+  if (!c) return EMHD_ERR_ARG;
+  c->skip_next = gate;
+  return EMHD_OK;
 }
 
 // emhd_update mode 1 whose final w also lands, rows {0,1} and {nx-2,nx-1} of every field, in
@@ -262,7 +296,24 @@ extern "C" int emhd_update_push(emhd_ctx* c, double* w, const double* V, long lo
   P.nx = (unsigned)c->g.nx;
   P.ny = (unsigned)c->g.ny;
   if (P.n_top >= (1LL << 32)) return EMHD_ERR_ARG;
-  return cerr(launch_update_push(w, V, ldv, nvec, h, len_upd, len_dot, len_max, k, out, P, c->stream));
+  return cerr(launch_update_push(w, V, ldv, nvec, h, len_upd, len_dot, len_max, k, out, P, c->stream,
+                                 take_skip(c)));
+}
+
+// Edge rows {0,1} and {nx-2,nx-1} of w into the neighbours' halo buffers (as emhd_update_push
+// stores them) when *gate != 0 (gate null: always); ordered by the collective that follows.
+extern "C" int emhd_push_edges(emhd_ctx* c, const double* w, double* lo_halo, double* hi_halo,
+                               const double* gate) {
+  if (!c || !w || c->g.nx < 4) return EMHD_ERR_ARG;
+  HaloPush P;
+  P.lo = lo_halo;
+  P.hi = hi_halo;
+  P.n_top = 8LL * c->g.nx * c->g.ny;
+  P.plane = (unsigned)((long long)c->g.nx * c->g.ny);
+  P.nx = (unsigned)c->g.nx;
+  P.ny = (unsigned)c->g.ny;
+  if (P.n_top >= (1LL << 32)) return EMHD_ERR_ARG;
+  return cerr(launch_push_edges(w, P, gate, c->stream));
 }
 
 extern "C" int emhd_update_finish(emhd_ctx* c, double* w, const double* V, long long ldv, int nvec,
@@ -277,7 +328,10 @@ extern "C" int emhd_update_finish(emhd_ctx* c, double* w, const double* V, long 
   FinishArgs F;
   F.h1 = h1; F.h2 = h2; F.selfdot = selfdot; F.j = j; F.H = H; F.ldh = ldh; F.scal = scal;
   F.brk_hist = brk_hist; F.st = c->st; F.rtol = 1e-12;
-  return cerr(launch_update(w, V, ldv, nvec, h2, len_upd, len_dot, len_max, 1, k, nrm, c->stream, F));
+  Reorth ro{};
+  ro.skip2 = take_skip(c);
+  return cerr(launch_update(w, V, ldv, nvec, h2, len_upd, len_dot, len_max, 1, k, nrm, c->stream, F,
+                            nullptr, ro));
 }
 
 extern "C" int emhd_norms(emhd_ctx* c, const double* x, long long len_sum, long long len_max, double* out) {
@@ -291,7 +345,7 @@ extern "C" int emhd_arnoldi_finish(emhd_ctx* c, const double* h1, const double* 
                                    double* brk_hist) {
   if (!c || !h1 || !h2 || !nrm || !selfdot || !H || !scal || j < 0) return EMHD_ERR_ARG;
   return cerr(launch_arnoldi_finish(h1, h2, nrm, selfdot, j, H, ldh, scal, brk_hist, c->st, 1e-12,
-                                    c->stream));
+                                    c->stream, take_skip(c)));
 }
 
 extern "C" int emhd_div_scalar(emhd_ctx* c, const double* x, const double* d, int take_sqrt, double* out,
@@ -597,6 +651,8 @@ struct emhd_arnoldi_args_s {
   int gen;             // process generation (look-ahead cancellation)
   double* gate;        // [m_cap + 1] per-iteration gates (look-ahead launches)
   double* evals;       // [m_cap + 1] 1 where iteration j evaluated the RHS (or null)
+  double eta;          // selective re-orthogonalisation threshold (<= 0: always two passes)
+  double* reorth;      // [m_cap + 1] 1 where iteration j skipped the second pass
 };
 
 // Iteration j of krylov.py:144-168 on one rank: (normalise w_{j-1} +) Jv, pass-1 multi-dot with
@@ -638,15 +694,23 @@ static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   }
   if (rc) return rc;
   const int nv = j + 1;
-  rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream, skip));
-  if (!rc) rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
-                                   A->d2, c->stream, FinishArgs{}, skip));
-  if (rc) return rc;
   FinishArgs F;
   F.h1 = A->d1; F.h2 = A->d2; F.selfdot = A->d1 + nv; F.j = j; F.H = A->H; F.ldh = A->ldh;
   F.scal = A->scal; F.brk_hist = A->brk; F.st = c->st; F.rtol = 1e-12;
+  // pass 1 (multi-dot, update + re-projection + norms); with eta > 0 its last CTA decides
+  // whether pass 2 is needed (selective re-orthogonalisation) and, if not, finishes the column
+  Reorth r1{}, r2{};
+  if (A->eta > 0.0 && A->reorth) {
+    r1.eta2 = A->eta * A->eta;
+    r1.gate_out = A->reorth + j;
+    r2.skip2 = A->reorth + j;
+  }
+  rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream, skip));
+  if (!rc) rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
+                                   A->d2, c->stream, F, skip, r1));
+  if (rc) return rc;
   return cerr(launch_update(out, A->V, A->ldv, nv, A->d2, A->len_upd, A->len_dot, A->n_top, 1, k,
-                            A->nrm, c->stream, F, skip));
+                            A->nrm, c->stream, F, skip, r2));
 }
 
 extern "C" int emhd_arnoldi_iter(emhd_ctx* c, const void* args, int j) {

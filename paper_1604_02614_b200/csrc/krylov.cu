@@ -51,6 +51,34 @@ __device__ bool finish_partials(const double* partials, int nval, int G, const i
   return true;
 }
 
+// finish_partials with value max_idx reduced by max, all others by sum
+__device__ bool finish_partials_maxidx(const double* partials, int nval, int G, int max_idx,
+                                       double* out, unsigned int* ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int prev = atomicAdd(ticket, 1u);
+    last = (prev == (unsigned)G - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int v = warp; v < nval; v += NWARP) {
+    const bool mx = v == max_idx;
+    double acc = 0.0;
+    for (int c = lane; c < G; c += 32) {
+      const double x = __ldcg(partials + (size_t)v * G + c);
+      acc = mx ? fmax(acc, x) : acc + x;
+    }
+    acc = mx ? warp_max(acc) : warp_sum(acc);
+    if (lane == 0) out[v] = acc;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;     // re-arm for the next launch
+  return true;
+}
+
 // per-warp slot accumulation of one double per vector, then CTA partial
 __device__ __forceinline__ void cta_store_partials(double* s_acc, int nval, double* partials, int G) {
   __syncthreads();
@@ -135,17 +163,39 @@ __global__ void __launch_bounds__(KT, 4) multidot_kernel(const double* __restric
 // MODE 1: out = {sum w^2 over len_dot, max|w| over len_max}.
 __device__ __forceinline__ void finish_column(const FinishArgs& F, const double* nrm) {
   // krylov.py:161-166: H[:j+1, j] = h1 + h2, hnext = ||w||, breakdown test, scal for the next Jv
-  for (int i = threadIdx.x; i <= F.j; i += blockDim.x) F.H[(size_t)i * F.ldh + F.j] = F.h1[i] + F.h2[i];
+  for (int i = threadIdx.x; i <= F.j; i += blockDim.x)
+    F.H[(size_t)i * F.ldh + F.j] = F.h2 ? F.h1[i] + F.h2[i] : F.h1[i];   // h2 null: pass 2 skipped
   if (threadIdx.x == 0) {
     const double hnext = sqrt(nrm[0]);
     const double scale = sqrt(F.selfdot[0]);
-    const bool brk = hnext <= F.rtol * fmax(scale, 1.0);
+    // sticky: an iteration queued after a breakdown works on an unwritten basis row (its
+    // normalised Jv launch did nothing), so whatever it computes must keep the flag raised
+    const bool brk = (F.j > 0 && F.scal[2] != 0.0) || hnext <= F.rtol * fmax(scale, 1.0);
     if (brk) F.st->breakdown = 1;
     else F.H[(size_t)(F.j + 1) * F.ldh + F.j] = hnext;
     F.scal[0] = hnext;
     F.scal[1] = nrm[1];
     F.scal[2] = brk ? 1.0 : 0.0;
     if (F.brk_hist) F.brk_hist[F.j] = brk ? 1.0 : 0.0;
+  }
+}
+
+// Selective re-orthogonalisation (Daniel-Gragg-Kaufman-Stewart): after pass 1, w1 = w - V h1
+// with r[nvec] = ||w1||^2 and r[nvec+1] = max|w1_top|.  When ||w1|| >= eta ||w|| the first
+// projection already left w1 orthogonal to the basis to working precision (its error is
+// O(eps ||w||) <= O(eps ||w1|| / eta)), so the column is finished with h1 and the second
+// sweep is skipped; otherwise the reference's second pass runs.  Called by one CTA.
+__device__ void reorth_decide(const FinishArgs& F, const double* r, int nvec, double eta2, double* gate) {
+  __shared__ int s_skip;
+  if (threadIdx.x == 0) {
+    s_skip = r[nvec] >= eta2 * F.selfdot[0] ? 1 : 0;
+    *gate = s_skip ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (s_skip) {
+    FinishArgs F1 = F;
+    F1.h2 = nullptr;
+    finish_column(F1, r + nvec);
   }
 }
 
@@ -169,13 +219,14 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, const double* __restrict__ h,
     long long len_upd, long long len_dot, long long len_max,
     double* partials, double* out, unsigned int* ticket, const FinishArgs fin,
-    const HaloPush push = HaloPush{}, const double* skip = nullptr) {
+    const HaloPush push = HaloPush{}, const double* skip = nullptr, const Reorth ro = Reorth{}) {
   if (skip && *skip != 0.0) return;            // cancelled look-ahead iteration (all CTAs agree)
+  if (ro.skip2 && *ro.skip2 != 0.0) return;    // pass 2 not needed (decided by pass 1)
   extern __shared__ double sm[];
   constexpr int TL = KT * 2;
   double* s_h = sm;                              // [nvec]
-  double* s_acc = sm + ((nvec + 1) & ~1);        // [(nvec or 2)][NWARP]
-  const int nval = MODE == 0 ? nvec : 2;
+  double* s_acc = sm + ((nvec + 1) & ~1);        // [(nvec + 2 or 2)][NWARP]
+  const int nval = MODE == 0 ? nvec + 2 : 2;
   for (int k = threadIdx.x; k < nvec; k += KT) s_h[k] = h[k];
   for (int k = threadIdx.x; k < nval * NWARP; k += KT) s_acc[k] = 0.0;
   __syncthreads();
@@ -224,12 +275,13 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
           if (i + u < nvec) s_acc[(i + u) * NWARP + warp] += d[0];
         }
       }
-    } else {
-      ss = fma(dx, dx, fma(dy, dy, ss));
-      const double mxx = (e < len_max) ? fabs(wv.x) : 0.0;
-      const double mxy = (e + 1 < len_max) ? fabs(wv.y) : 0.0;
-      mx = fmax(mx, fmax(mxx, mxy));
     }
+    // ||w||^2 and max|w_top| of the updated vector (mode 0: the selective re-orthogonalisation
+    // test and, when pass 2 is skipped, the next sigma; mode 1: hnext and the next sigma)
+    ss = fma(dx, dx, fma(dy, dy, ss));
+    const double mxx = (e < len_max) ? fabs(wv.x) : 0.0;
+    const double mxy = (e + 1 < len_max) ? fabs(wv.y) : 0.0;
+    mx = fmax(mx, fmax(mxx, mxy));
   }
   if (PUSH) __threadfence_system();   // peer stores visible before the ordering collective
   if (MODE == 1) {
@@ -252,9 +304,56 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
       finish_column(fin, out);
     }
   } else {
-    cta_store_partials(s_acc, nval, partials, gridDim.x);
-    finish_partials(partials, nval, gridDim.x, nullptr, out, ticket);
+    ss = warp_sum(ss);
+    mx = warp_max(mx);
+    if (lane == 0) { s_acc[nvec * NWARP + warp] = ss; s_acc[(nvec + 1) * NWARP + warp] = mx; }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nval; v += KT) {
+      double acc = 0.0;
+      if (v == nvec + 1) {
+#pragma unroll
+        for (int q = 0; q < NWARP; ++q) acc = fmax(acc, s_acc[v * NWARP + q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NWARP; ++q) acc += s_acc[v * NWARP + q];
+      }
+      partials[(size_t)v * gridDim.x + blockIdx.x] = acc;
+    }
+    __shared__ int max_kind;
+    if (threadIdx.x == 0) max_kind = nvec + 1;
+    __syncthreads();
+    const bool last = finish_partials_maxidx(partials, nval, gridDim.x, max_kind, out, ticket);
+    if (last && ro.gate_out) {
+      __syncthreads();
+      reorth_decide(fin, out, nvec, ro.eta2, ro.gate_out);
+    }
   }
+}
+
+// slab ranks, pass 2 skipped: w1 is final, so its edge rows go to the neighbours' halo buffers
+// here (otherwise emhd_update_push stores the edges of the final w)
+__global__ void push_edges_kernel(const double* __restrict__ w, const HaloPush H, const double* gate) {
+  if (gate && *gate == 0.0) return;
+  const unsigned total = NF * 4u * H.ny;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+    const unsigned col = q % H.ny, t = q / H.ny;
+    const unsigned r = t % 4u, f = t / 4u;
+    const unsigned row = r < 2u ? r : H.nx - 4u + r;
+    const long long e = (long long)f * H.plane + (long long)row * H.ny + col;
+    push_edge(H, e, w[e]);
+  }
+  __threadfence_system();
+}
+
+cudaError_t launch_push_edges(const double* w, const HaloPush& H, const double* gate, cudaStream_t s) {
+  const unsigned total = NF * 4u * H.ny;
+  push_edges_kernel<<<(total + 255) / 256, 256, 0, s>>>(w, H, gate);
+  return cudaGetLastError();
+}
+
+__global__ void reorth_decide_kernel(const FinishArgs F, const double* r, int nvec, double eta2,
+                                     double* gate) {
+  reorth_decide(F, r, nvec, eta2, gate);
 }
 
 // out = {sum x^2 over len_sum, max|x| over len_max}
@@ -289,7 +388,8 @@ __global__ void __launch_bounds__(KT) norms_kernel(const double* __restrict__ x,
 // scal = {hnext, max|w_top|} for the next fused normalise + Jv.
 __global__ void arnoldi_finish_kernel(const double* h1, const double* h2, const double* nrm,
     const double* selfdot, int j, double* H, long long ldh, double* scal, double* brk_hist,
-    DevStatus* st, double rtol) {
+    DevStatus* st, double rtol, const double* skip2) {
+  if (skip2 && *skip2 != 0.0) return;      // the column was finished by the pass-1 decision
   FinishArgs F;
   F.h1 = h1; F.h2 = h2; F.selfdot = selfdot; F.j = j; F.H = H; F.ldh = ldh; F.scal = scal;
   F.brk_hist = brk_hist; F.st = st; F.rtol = rtol;
@@ -383,26 +483,29 @@ cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int
 
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
-                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin, const double* skip) {
+                          KWork& wk, double* out, cudaStream_t s, FinishArgs fin, const double* skip,
+                          Reorth ro) {
   const int G = grid_for(len_upd, KT * 2, wk.num_sms);
-  const int nval = mode == 0 ? nvec : 2;
-  const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)(nval > 0 ? nval : 1) * NWARP);
+  const int nval = mode == 0 ? nvec + 2 : 2;
+  const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)nval * NWARP);
   if (mode == 0)
     update_kernel<0, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip);
+                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip, ro);
   else
     update_kernel<1, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip);
+                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip, ro);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_push(double* w, const double* V, long long ldv, int nvec, const double* h,
                                long long len_upd, long long len_dot, long long len_max, KWork& wk,
-                               double* out, const HaloPush& push, cudaStream_t s) {
+                               double* out, const HaloPush& push, cudaStream_t s, const double* skip2) {
   const int G = grid_for(len_upd, KT * 2, wk.num_sms);
   const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + 2 * NWARP);
+  Reorth ro{};
+  ro.skip2 = skip2;
   update_kernel<1, 8, true><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                               wk.partials, out, wk.ticket, FinishArgs{}, push);
+                                               wk.partials, out, wk.ticket, FinishArgs{}, push, nullptr, ro);
   return cudaGetLastError();
 }
 
@@ -417,8 +520,16 @@ cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, 
 
 cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,
                                   const double* selfdot, int j, double* H, long long ldh, double* scal,
-                                  double* brk_hist, DevStatus* st, double rtol, cudaStream_t s) {
-  arnoldi_finish_kernel<<<1, 128, 0, s>>>(h1, h2, nrm, selfdot, j, H, ldh, scal, brk_hist, st, rtol);
+                                  double* brk_hist, DevStatus* st, double rtol, cudaStream_t s,
+                                  const double* skip2) {
+  arnoldi_finish_kernel<<<1, 128, 0, s>>>(h1, h2, nrm, selfdot, j, H, ldh, scal, brk_hist, st, rtol,
+                                          skip2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reorth_decide(FinishArgs fin, const double* r, int nvec, double eta2, double* gate,
+                                 cudaStream_t s) {
+  reorth_decide_kernel<<<1, 128, 0, s>>>(fin, r, nvec, eta2, gate);
   return cudaGetLastError();
 }
 

@@ -23,6 +23,12 @@ struct FinishArgs {         // optional Arnoldi column bookkeeping fused into up
   double rtol;
 };
 
+struct Reorth {               // selective (DGKS) re-orthogonalisation of one Arnoldi iteration
+  double eta2;               // pass 2 is skipped when ||w1||^2 >= eta2 ||w||^2 (0: never decide)
+  double* gate_out;          // update mode 0: decision written here (1 = pass 2 skipped)
+  const double* skip2;       // pass-2 launches: no work when *skip2 != 0
+};
+
 struct HaloPush {            // peer halo destinations of a slab's edge rows (null: none)
   double* lo;                // lo neighbour's halo buffer [2][8][2][ny]
   double* hi;                // hi neighbour's halo buffer
@@ -41,17 +47,22 @@ cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
                           KWork& wk, double* out, cudaStream_t s, FinishArgs fin = FinishArgs{},
-                          const double* skip = nullptr);
+                          const double* skip = nullptr, Reorth ro = Reorth{});
+cudaError_t launch_push_edges(const double* w, const HaloPush& H, const double* gate, cudaStream_t s);
+cudaError_t launch_reorth_decide(FinishArgs fin, const double* r, int nvec, double eta2, double* gate,
+                                 cudaStream_t s);
 cudaError_t launch_gate(const unsigned long long* cancel, unsigned gen, int j, double* gate, cudaStream_t s);
 cudaError_t launch_evals_discount(const double* evals, int count, DevStatus* st, cudaStream_t s);
 cudaError_t launch_update_push(double* w, const double* V, long long ldv, int nvec, const double* h,
                                long long len_upd, long long len_dot, long long len_max, KWork& wk,
-                               double* out, const HaloPush& push, cudaStream_t s);
+                               double* out, const HaloPush& push, cudaStream_t s,
+                               const double* skip2 = nullptr);
 cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, KWork& wk, double* out,
                          cudaStream_t s);
 cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,
                                   const double* selfdot, int j, double* H, long long ldh, double* scal,
-                                  double* brk_hist, DevStatus* st, double rtol, cudaStream_t s);
+                                  double* brk_hist, DevStatus* st, double rtol, cudaStream_t s,
+                                  const double* skip2 = nullptr);
 cudaError_t launch_combine(const double* V, long long ldv, int m, const double* Y, int S,
                            const CombineOut& co, long long len, int num_sms, cudaStream_t s);
 

@@ -43,6 +43,12 @@ BREAKDOWN_RTOL = 1e-12
 # Arnoldi iterations queued behind a batch of residual checks while the checks run on a
 # side stream (None: by vector size; EMHD_LOOKAHEAD overrides; 0: checks in stream order)
 LOOKAHEAD_OVERRIDE = None
+# Selective (DGKS) re-orthogonalisation of the fused finite-difference engines: the second
+# Gram-Schmidt pass runs only when the first left ||w1|| < eta ||w|| (the reference's MGS always
+# runs it, krylov.py:156-160; when ||w1|| >= eta ||w|| the first pass already leaves w1
+# orthogonal to working precision, so H and V change at round-off level).  0: always two
+# passes.  EMHD_REORTH_ETA overrides.
+REORTH_ETA = float(os.environ.get("EMHD_REORTH_ETA", str(1.0 / math.sqrt(2.0))))
 
 
 class KrylovConvergenceError(RuntimeError):
@@ -88,6 +94,9 @@ class ArnoldiBasis:
     m: int
     beta: float
     breakdown: bool = False
+    # B200 extension: per iteration, 1.0 where the second Gram-Schmidt pass ran (device
+    # tensor; None when every iteration ran it, i.e. selective re-orthogonalisation off)
+    second_pass: object = None
 
     @property
     def h_next(self):
@@ -200,7 +209,7 @@ class _Process:
         k = self.m_cap + 4
         hw = max(self.m_cap, 1)
         # one zero-filled block for H and every small scalar area (a single fill launch)
-        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + 3 * (self.m_cap + 1) + 4,
+        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + 4 * (self.m_cap + 1) + 4,
                                   dtype=D.F64, device=D.device())
         o = (self.m_cap + 1) * hw
         self.H = self._small[:o].view(self.m_cap + 1, hw)
@@ -213,6 +222,8 @@ class _Process:
         o3 = o2 + self.m_cap + 5
         self.gate = self._small[o3:o3 + self.m_cap + 1]       # look-ahead gates (fast path)
         self.evals = self._small[o3 + self.m_cap + 1:o3 + 2 * (self.m_cap + 1)]   # RHS evals per iteration
+        self.reorth = self._small[o3 + 2 * (self.m_cap + 1):o3 + 3 * (self.m_cap + 1)]  # 1: pass 2 skipped
+        self.eta = REORTH_ETA if engine.fused else 0.0
         self.scal = D.Scratch(4)
         self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
@@ -267,6 +278,7 @@ class _Process:
                 A.bidx[k] = E.bidx[k]
             A.gen = self._new_gen()
             A.gate, A.evals = D.ptr(self.gate), D.ptr(self.evals)
+            A.eta, A.reorth = self.eta, D.ptr(self.reorth)
             self._args = A
             self._args_ref = D.ctypes_byref(A)
 
@@ -386,31 +398,54 @@ class _Process:
         N.check(self.lib.emhd_multidot(h, D.ptr(w), D.ptr(self.V), self.ld, nv, self.len_dot, 1,
                                        D.ptr(self.d1)), "multidot")
         self._allreduce_sum(self.d1[:nv + 1])
-        # w -= V h1 ; h2 = V^T w
+        # w -= V h1 ; h2 = V^T w ; ||w||^2, max|w_top|
         N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d1),
                                      self.len_upd, self.len_dot, self.n_top, 0, D.ptr(self.d2)), "update")
-        self._allreduce_sum(self.d2[:nv])
+        self._allreduce_sum(self.d2[:nv + 1])
+        if self.comm is not None and self.layout.distributed:
+            self.comm.allreduce_max(self.d2[nv + 1:nv + 2])
+        gate = None
+        if self.eta > 0.0:
+            # selective re-orthogonalisation: pass 2 only when ||w1|| < eta ||w|| (on device;
+            # the pass-2 launches below test the gate, no host sync)
+            gate = self.reorth[j:j + 1]
+            N.check(self.lib.emhd_reorth_decide(h, D.ptr(self.d1), D.ptr(self.d2), nv, D.ptr(self.d1[nv:]),
+                                                j, D.ptr(self.H), self.H.shape[1], D.ptr(self.scal.dev),
+                                                D.ptr(self.brk), self.eta, D.ptr(gate)), "reorth_decide")
+            if self.push is not None:
+                N.check(self.lib.emhd_push_edges(h, D.ptr(w), self.push.lo_ptr, self.push.hi_ptr,
+                                                 D.ptr(gate)), "push_edges")
+
+        def gated():
+            if gate is not None:
+                N.check(self.lib.emhd_skip_next(h, D.ptr(gate)), "skip_next")
+
         # w -= V h2 ; ||w||^2, max|w_top| ; column bookkeeping (fused when single-rank)
         if self.comm is None or not self.layout.distributed:
+            gated()
             N.check(self.lib.emhd_update_finish(
                 h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2), self.len_upd, self.len_dot,
                 self.n_top, D.ptr(self.nrm), D.ptr(self.d1), D.ptr(self.d1[nv:]), j, D.ptr(self.H),
                 self.H.shape[1], D.ptr(self.scal.dev), D.ptr(self.brk)), "update_finish")
         elif self.push is not None:
             P = self.push
+            gated()
             N.check(self.lib.emhd_update_push(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2),
                                               self.len_upd, self.len_dot, self.n_top, D.ptr(self.nrm),
                                               P.lo_ptr, P.hi_ptr), "update_push")
             self._allreduce_norms(self.nrm)          # also orders the pushed halo rows
+            gated()
             N.check(self.lib.emhd_arnoldi_finish(h, D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm),
                                                  D.ptr(self.d1[nv:]), j, D.ptr(self.H),
                                                  self.H.shape[1], D.ptr(self.scal.dev), D.ptr(self.brk)),
                     "arnoldi_finish")
         else:
+            gated()
             N.check(self.lib.emhd_update(h, D.ptr(w), D.ptr(self.V), self.ld, nv, D.ptr(self.d2),
                                          self.len_upd, self.len_dot, self.n_top, 1, D.ptr(self.nrm)),
                     "update")
             self._allreduce_norms(self.nrm)
+            gated()
             N.check(self.lib.emhd_arnoldi_finish(h, D.ptr(self.d1), D.ptr(self.d2), D.ptr(self.nrm),
                                                  D.ptr(self.d1[nv:]), j, D.ptr(self.H),
                                                  self.H.shape[1], D.ptr(self.scal.dev), D.ptr(self.brk)),
@@ -544,7 +579,10 @@ class _Process:
             V, H = D.to_host(V.contiguous()), D.to_host(H.contiguous())
         else:
             V, H = V, H.clone()
-        return ArnoldiBasis(V=V, H=H, m=m, beta=self.beta, breakdown=self.breakdown)
+        sp = (1.0 - self.reorth[:m]) if self.eta > 0.0 else None
+        if sp is not None and host:
+            sp = D.to_host(sp)
+        return ArnoldiBasis(V=V, H=H, m=m, beta=self.beta, breakdown=self.breakdown, second_pass=sp)
 
     # -- small dense + combination ---------------------------------------------
     def phi_coeffs(self, order, scales):

@@ -420,6 +420,11 @@ def test_fused_arnoldi_breakdown_queued_iterations_are_inert(P):
     f = P.make_rhs(prm, g, bc)
     op = P.FdJacobianOperator(f, U.reshape(-1))
     ev0 = f.ctx.status().rhs_evals
+    # poison the caching allocator: the basis rows the queued iterations read were never
+    # written (their normalised Jv did nothing), so they must stay inert even on NaN garbage
+    junk = [torch.full((7 * 1024 * (k + 1),), float("nan"), dtype=torch.float64, device="cuda")
+            for k in range(8)]
+    del junk
     b = P.arnoldi(op, v.reshape(-1), 6)
     ref = krylov_cpu.arnoldi(jvp.FdJv(stencil.rhs_closure(prm, g, bc), U.reshape(-1)), v.reshape(-1), 6)
     assert b.breakdown and ref.broke and b.m == ref.m == 1
@@ -547,3 +552,76 @@ def test_lookahead_projection_equals_stream_ordered(P):
     for a, b in zip(out[0][0], out[4][0]):
         assert torch.linalg.norm(a - b).item() <= 1e-12 * torch.linalg.norm(a).item()
     assert torch.linalg.norm(out[0][1] - out[4][1]).item() <= 1e-12 * torch.linalg.norm(out[0][1]).item()
+
+
+# ------------------------------------ selective (DGKS) re-orthogonalisation of the fused engine
+
+def test_selective_reorth_against_reference_and_two_pass(P):
+    """The fused FD engine skips the second Gram-Schmidt pass when ||w1|| >= eta ||w||
+    (krylov.REORTH_ETA).  On the reference's FD-MHD fixture every eta gives the reference's H
+    (1e-8, the FD round-off amplification bar) and an orthonormal basis; on config 0's state
+    both branches occur and the Arnoldi relation J V_m = V_{m+1} H holds to round-off."""
+    from paper_1604_02614_b200 import krylov
+    z = golden("krylov_mhd.npz")
+    gt, pt = z["grid"], z["params"]
+    g = P.Grid2D(int(gt[0]), int(gt[1]), gt[2], gt[3], gt[4], gt[5])
+    prm = P.MhdParams(mu=pt[0], eta=pt[1], kappa=pt[2], gamma=pt[3], b_half=bool(pt[4]))
+    f = P.make_rhs(prm, g, P.BoundaryPolicy("periodic", "reflect"))
+    op = P.FdJacobianOperator(f, z["a"], z["fa"])
+    g0 = P.ReconnectionSpec().grid(64, 64)
+    p0 = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    f0 = P.make_rhs(p0, g0, P.default_bc("reconnection"))
+    y0 = dev(P.reconnection_ic(g0, params=p0).reshape(-1))
+    op0 = P.FdJacobianOperator(f0, y0)
+    old = krylov.REORTH_ETA
+    res = {}
+    try:
+        for eta in (0.0, 0.5, 1.0 / np.sqrt(2.0)):
+            krylov.REORTH_ETA = eta
+            b = P.arnoldi(op, z["v"], 12)
+            assert b.m == 12 and not b.breakdown
+            assert np.linalg.norm(b.H - z["H"]) <= 1e-8 * np.linalg.norm(z["H"]), eta
+            assert np.max(np.abs(b.V.T @ b.V - np.eye(b.V.shape[1]))) <= 1e-12, eta
+            assert (b.second_pass is None) == (eta == 0.0)
+            res[eta] = P.arnoldi(op0, f0(y0), 40)
+    finally:
+        krylov.REORTH_ETA = old
+    b = res[1.0 / np.sqrt(2.0)]
+    sp = b.second_pass.cpu().numpy()
+    assert 0 < sp.sum() < len(sp), sp                # both branches exercised
+    V, H = b.V, b.H
+    G = V.T @ V
+    assert torch.max(torch.abs(G - torch.eye(G.shape[0], dtype=G.dtype, device=G.device))).item() <= 1e-12
+    for j in (0, 7, 20, 39):
+        lhs = op0(V[:, j].contiguous())
+        rhs = V[:, :j + 2] @ H[:j + 2, j]
+        assert torch.linalg.norm(lhs - rhs).item() <= 1e-10 * torch.linalg.norm(lhs).item(), j
+    H2 = res[0.0].H            # measured 2.4e-9: the FD operator amplifies round-off by 1/sigma
+    assert torch.linalg.norm(H - H2).item() <= 1e-8 * torch.linalg.norm(H2).item()
+
+
+def test_push_edges_gate(P):
+    """emhd_push_edges stores exactly emhd_pack_edges's rows into the neighbours' sides when the
+    gate is set, and nothing when it is clear."""
+    from paper_1604_02614_b200 import _native as N
+    from paper_1604_02614_b200 import device as D
+    from paper_1604_02614_b200.mhd import GpuRhs
+    from paper_1604_02614_b200.slab import make_layout
+    rng = np.random.default_rng(6)
+    g = P.Grid2D(37, 70, 0.0, 1.0, 0.0, 1.0)
+    L = make_layout(g.nx, g.ny, "periodic", 1, 3)
+    f = GpuRhs(P.MhdParams(), g, P.BoundaryPolicy("periodic", "reflect"), layout=L)
+    h = f.ctx.sync_stream()
+    w = dev(rng.standard_normal(L.n_local))
+    send = torch.empty((2, 8, 2, g.ny), dtype=torch.float64, device="cuda")
+    N.check(f.ctx.lib.emhd_pack_edges(h, D.ptr(w), D.ptr(send)))
+    for gate_val in (0.0, 1.0):
+        gate = torch.tensor([gate_val], dtype=torch.float64, device="cuda")
+        lo = torch.full((2, 8, 2, g.ny), -7.0, dtype=torch.float64, device="cuda")
+        hi = torch.full((2, 8, 2, g.ny), -7.0, dtype=torch.float64, device="cuda")
+        N.check(f.ctx.lib.emhd_push_edges(h, D.ptr(w), D.ptr(lo), D.ptr(hi), D.ptr(gate)))
+        if gate_val:
+            assert torch.equal(lo[1], send[0]) and torch.equal(hi[0], send[1])
+        else:
+            assert bool((lo[1] == -7.0).all()) and bool((hi[0] == -7.0).all())
+        assert bool((lo[0] == -7.0).all()) and bool((hi[1] == -7.0).all())
