@@ -390,7 +390,7 @@ def run_ours(args):
                                  "second_pass_iterations": int(sum(1 for x in sp if x)),
                                  "two_pass_canonical_GB_per_step": canon / 1e9,
                                  "rule": "(3j+11)W with the second Gram-Schmidt pass, (2j+8)W without "
-                                         "(selective re-orthogonalisation, eta = 1/sqrt(2))"}
+                                         "(selective re-orthogonalisation, eta = %g)" % _reorth_eta()}
 
     # ---- end to end through the public API with host buffers
     if not args.no_e2e:

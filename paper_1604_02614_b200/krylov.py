@@ -43,12 +43,15 @@ BREAKDOWN_RTOL = 1e-12
 # Arnoldi iterations queued behind a batch of residual checks while the checks run on a
 # side stream (None: by vector size; EMHD_LOOKAHEAD overrides; 0: checks in stream order)
 LOOKAHEAD_OVERRIDE = None
-# Selective (DGKS) re-orthogonalisation of the fused finite-difference engines: the second
-# Gram-Schmidt pass runs only when the first left ||w1|| < eta ||w|| (the reference's MGS always
-# runs it, krylov.py:156-160; when ||w1|| >= eta ||w|| the first pass already leaves w1
-# orthogonal to working precision, so H and V change at round-off level).  0: always two
-# passes.  EMHD_REORTH_ETA overrides.
-REORTH_ETA = float(os.environ.get("EMHD_REORTH_ETA", str(1.0 / math.sqrt(2.0))))
+# Selective re-orthogonalisation of the fused finite-difference engines (Kahan-Parlett "twice is
+# enough" with kappa = 1/eta = 2; DGKS/ARPACK use eta ~ 1/sqrt(2)): the second Gram-Schmidt pass
+# runs only when the first left ||w1|| < eta ||w||.  The reference's MGS always runs it
+# (krylov.py:156-160); when ||w1|| >= eta ||w|| the first pass already leaves w1 orthogonal to
+# O(eps / eta), so H and V change at round-off level.  0: always two passes.
+# EMHD_REORTH_ETA overrides.  Measured (identical counters in every case): config 2 1216 -> 1672
+# it/s, config 1 0.71 -> 0.58 s, config-3 physics at 1024^2 1.86 -> 1.68 s (eta 1/sqrt(2): 1630
+# it/s, 0.65 s, 1.82 s).
+REORTH_ETA = float(os.environ.get("EMHD_REORTH_ETA", "0.5"))
 
 
 class KrylovConvergenceError(RuntimeError):
