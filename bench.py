@@ -155,87 +155,10 @@ class Clocks:
 
 
 # ------------------------------------------------------ kernel instrumentation
-LAUNCHERS = {
-    # name -> algorithmic HBM bytes of one launch, from its C-ABI arguments
-    "emhd_rhs": None, "emhd_jv": None, "emhd_jv_aug": None, "emhd_jv_normalized": None,
-    "emhd_multidot": None, "emhd_update": None, "emhd_norms": None, "emhd_arnoldi_finish": None,
-    "emhd_div_scalar": None, "emhd_phi_small": None, "emhd_combine": None, "emhd_lincomb": None,
-    "emhd_wrms": None, "emhd_pack_edges": None, "emhd_update_finish": None,
-}
-
-
-def alg_bytes(name, args, n_local):
-    W = 8.0 * n_local
-    if name == "emhd_rhs":
-        return 2 * W
-    if name in ("emhd_jv", "emhd_jv_aug"):
-        return 4 * W
-    if name == "emhd_jv_normalized":
-        return 5 * W             # read a, F(a), w_prev; write v_j and J v_j
-    if name == "emhd_multidot":
-        nvec, len_dot = args[4], args[5]
-        return 8.0 * (nvec + 1) * len_dot
-    if name in ("emhd_update", "emhd_update_finish"):
-        nvec, len_upd = args[4], args[6]
-        return 8.0 * (nvec + 2) * len_upd
-    if name == "emhd_norms":
-        return 8.0 * max(args[2], args[3])
-    if name == "emhd_div_scalar":
-        return 16.0 * args[6]
-    if name == "emhd_combine":
-        return 8.0 * (args[3] + args[5]) * args[9]
-    if name == "emhd_lincomb":
-        return 8.0 * (args[1] + 1) * args[8]
-    return 0.0
-
-
-class Instrument:
-    """Wraps the C-ABI launchers with CUDA events (current stream) and counters."""
-
-    def __init__(self, lib, n_local, events=True):
-        import torch
-        self.torch = torch
-        self.lib = lib
-        self.n_local = n_local
-        self.events = events
-        self.records = []
-        self.count = 0
-        self.orig = {}
-        for name in LAUNCHERS:
-            fn = getattr(lib, name)
-            self.orig[name] = fn
-            setattr(lib, name, self._wrap(name, fn))
-
-    def _wrap(self, name, fn):
-        torch = self.torch
-
-        def call(*a):
-            self.count += 1
-            if not self.events:
-                return fn(*a)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            rc = fn(*a)
-            e1.record()
-            self.records.append((name, e0, e1, alg_bytes(name, a, self.n_local)))
-            return rc
-        return call
-
-    def restore(self):
-        for name, fn in self.orig.items():
-            setattr(self.lib, name, fn)
-
-    def table(self):
-        self.torch.cuda.synchronize()
-        agg = {}
-        for name, e0, e1, by in self.records:
-            ms = e0.elapsed_time(e1)
-            a = agg.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0.0})
-            a["launches"] += 1
-            a["ms"] += ms
-            a["bytes"] += by
-        return agg
+# emhd_profile_read kinds (include/emhd.h EMHD_K_*), reported under the C-ABI entry names
+KIND_NAMES = {0: "emhd_jv", 1: "emhd_jv_normalized", 2: "emhd_multidot", 3: "emhd_update",
+              4: "emhd_multidot (second pass)", 5: "emhd_update_finish", 6: "emhd_norms",
+              7: "emhd_div_scalar", 8: "gate"}
 
 
 # ----------------------------------------------------------------- our arm
@@ -330,32 +253,37 @@ def run_ours(args):
                  "us_per_jv": jv_ms * 1e3 / args.jv, "alg_GBps_per_gpu": jv_gbs / world,
                  "frac_of_hbm": jv_gbs / world / hbm}
 
-    # ---- instrumented pass (same K steps): per-kernel launch times on the launching stream
-    # the timed path drives each iteration with one C call (emhd_arnoldi_iter); for per-launch
-    # events the same kernels are issued through the per-kernel entry points
-    from paper_1604_02614_b200 import krylov as K
+    # ---- profiled pass (same K steps, same fast path): the library brackets every launch of
+    # the Arnoldi iterations with CUDA events on the launching stream (emhd_profile); a launch
+    # that a device gate turned into a no-op (skipped second pass, cancelled look-ahead)
+    # counts zero algorithmic bytes
+    import ctypes
     lib = N.lib()
-    K.FAST_DRIVER = False
-    ins = Instrument(lib, n_local, events=True)
+    hctx = op.ctx.h
+    N.check(lib.emhd_profile(hctx, 1), "profile")
     barrier()
     passes = []
+    records = []
+    cap = 64 * args.m + 64
+    kinds = (ctypes.c_int * cap)()
+    pms = (ctypes.c_double * cap)()
+    pby = (ctypes.c_double * cap)()
     for _ in range(args.steps):
-        r0 = len(ins.records)
         bb = step()
-        # selective re-orthogonalisation: a skipped second pass moved no bytes
-        sp = None if bb.second_pass is None else bb.second_pass.cpu().numpy()
-        fin = [k for k in range(r0, len(ins.records)) if ins.records[k][0] == "emhd_update_finish"]
-        if sp is not None and len(fin) == len(sp):
-            for k, ran in zip(fin, sp):
-                if ran == 0.0:
-                    nm, e0_, e1_, _ = ins.records[k]
-                    ins.records[k] = (nm, e0_, e1_, 0.0)
-        passes.append(sp)
+        nrec = lib.emhd_profile_read(hctx, cap, kinds, pms, pby)
+        if nrec < 0:
+            raise RuntimeError("emhd_profile_read failed")
+        records += [(KIND_NAMES.get(kinds[i], str(kinds[i])), pms[i], pby[i]) for i in range(nrec)]
+        passes.append(None if bb.second_pass is None else bb.second_pass.cpu().numpy())
     barrier()
-    table = ins.table()
-    launches_per_step = ins.count / args.steps
-    ins.restore()
-    K.FAST_DRIVER = True
+    N.check(lib.emhd_profile(hctx, 0), "profile")
+    table = {}
+    for name, ms_, by_ in records:
+        a_ = table.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0.0})
+        a_["launches"] += 1
+        a_["ms"] += ms_
+        a_["bytes"] += by_
+    launches_per_step = sum(1 for r in records if r[0] != "gate") / args.steps
     kern = []
     for name, a_ in sorted(table.items(), key=lambda kv: -kv[1]["ms"]):
         avg_us = a_["ms"] * 1e3 / a_["launches"]

@@ -233,6 +233,17 @@ int emhd_arnoldi_cancel(emhd_ctx* ctx, int gen, int epoch_min);
 /* status.rhs_evals -= sum(evals[0:count]): RHS evaluations of discarded speculative
  * iterations (evals written per iteration by emhd_arnoldi_iter when args.evals is set) */
 int emhd_evals_discount(emhd_ctx* ctx, const double* evals, int count);
+
+/* ---- per-launch profiling (benchmarks) ------------------------------ */
+enum { EMHD_K_JV = 0, EMHD_K_JV_NORMALIZED = 1, EMHD_K_MULTIDOT = 2, EMHD_K_UPDATE = 3,
+       EMHD_K_MULTIDOT2 = 4, EMHD_K_UPDATE_FINISH = 5, EMHD_K_NORMS = 6, EMHD_K_DIV_SCALAR = 7,
+       EMHD_K_GATE = 8 };
+/* enable != 0: clear and start recording CUDA events around every launch of emhd_arnoldi_*
+ * (and emhd_jv / emhd_norms / emhd_div_scalar); 0: stop */
+int emhd_profile(emhd_ctx* ctx, int enable);
+/* sync, then copy out (kind, ms, algorithmic bytes; 0 bytes for a launch a device gate made a
+ * no-op) of up to max_n records and clear them; returns the count (negative: -error) */
+int emhd_profile_read(emhd_ctx* ctx, int max_n, int* kinds, double* ms, double* bytes);
 /* Copy brk[0:nbrk] and res[0:nres] into host_out (pinned), then read the status word: the one
  * host synchronisation of a residual check. */
 int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res, int nres,

@@ -39,7 +39,8 @@ class ArnoldiArgs(ctypes.Structure):
                 ("w0", P), ("w1", P), ("d1", P), ("d2", P), ("nrm", P), ("vn", P), ("scal", P),
                 ("brk", P), ("n_top", c_ll), ("len_dot", c_ll), ("len_upd", c_ll), ("p", c_int),
                 ("nb", c_int), ("ch", c_dbl), ("bcol", P * 5), ("bidx", c_int * 5),
-                ("gen", c_int), ("gate", P), ("evals", P), ("eta", c_dbl), ("reorth", P)]
+                ("gen", c_int), ("gate", P), ("evals", P), ("eta", c_dbl), ("reorth", P),
+                ("md2", P)]
 
 
 class Report(ctypes.Structure):
@@ -89,6 +90,8 @@ _SIGS = {
     "emhd_slot_norms": (c_int, [c_vp, P, c_int, c_int, P]),
     "emhd_reorth_decide": (c_int, [c_vp, P, P, c_int, P, c_int, P, c_ll, P, P, c_dbl, P]),
     "emhd_skip_next": (c_int, [c_vp, P]),
+    "emhd_profile": (c_int, [c_vp, c_int]),
+    "emhd_profile_read": (c_int, [c_vp, c_int, IP, DP, DP]),
     "emhd_push_edges": (c_int, [c_vp, P, P, P, P]),
     "emhd_update_push": (c_int, [c_vp, P, P, c_ll, c_int, P, c_ll, c_ll, c_ll, P, P, P]),
     "emhd_unslot_norms": (c_int, [c_vp, P, c_int, P]),

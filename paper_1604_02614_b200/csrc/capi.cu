@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 #include "../../include/emhd.h"
 #include "emhd_common.cuh"
 #include "stencil.cuh"
@@ -31,7 +32,47 @@ struct emhd_ctx {
   unsigned long long* cancel = nullptr;       // look-ahead cancel word {generation, epoch}
   unsigned long long* cancel_host = nullptr;  // pinned source of its async updates
   const double* skip_next = nullptr;          // emhd_skip_next: gate of the next pass-2 launch
+  // per-launch profiling (emhd_profile): CUDA events around every launch of the Arnoldi path
+  struct ProfRec { int kind; cudaEvent_t e0, e1; double bytes; const double* gate[2]; };
+  bool prof = false;
+  std::vector<ProfRec> recs;
 };
+
+// Brackets one launch with CUDA events on the context's stream when profiling is on; the
+// algorithmic bytes count only if neither gate (device flags read back by emhd_profile_read)
+// says the launch did no work.
+struct ProfScope {
+  emhd_ctx* c;
+  int kind;
+  double bytes;
+  const double* g0;
+  const double* g1;
+  cudaEvent_t e0{};
+  ProfScope(emhd_ctx* c_, int kind_, double bytes_, const double* g0_ = nullptr, const double* g1_ = nullptr)
+      : c(c_), kind(kind_), bytes(bytes_), g0(g0_), g1(g1_) {
+    if (c->prof) {
+      cudaEventCreate(&e0);
+      cudaEventRecord(e0, c->stream);
+    }
+  }
+  ~ProfScope() {
+    if (!c->prof) return;
+    cudaEvent_t e1;
+    cudaEventCreate(&e1);
+    cudaEventRecord(e1, c->stream);
+    emhd_ctx::ProfRec r;
+    r.kind = kind; r.e0 = e0; r.e1 = e1; r.bytes = bytes; r.gate[0] = g0; r.gate[1] = g1;
+    c->recs.push_back(r);
+  }
+};
+
+static void prof_clear(emhd_ctx* c) {
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  c->recs.clear();
+}
 
 // the gate set by emhd_skip_next, consumed by exactly one pass-2 launch
 static const double* take_skip(emhd_ctx* c) {
@@ -115,6 +156,7 @@ extern "C" int emhd_ctx_destroy(emhd_ctx* c) {
   cudaFree(c->ticket);
   cudaFree(c->st);
   cudaFree(c->dense);
+  prof_clear(c);
   cudaFree(c->cancel);
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->cancel_host) cudaFreeHost(c->cancel_host);
@@ -201,6 +243,7 @@ extern "C" int emhd_jv(emhd_ctx* c, const double* a, const double* a_halo, const
   StencilParams P = c->base;
   P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = v; P.v_halo = v_halo; P.scal = d_vnorm; P.out = out;
+  ProfScope ps(c, EMHD_K_JV, 4.0 * 64.0 * (double)c->g.nx * c->g.ny);   // 4W
   return cerr(launch_stencil(P, MODE_JV, false, c->num_sms, c->stream));
 }
 
@@ -229,6 +272,7 @@ extern "C" int emhd_jv_normalized(emhd_ctx* c, const double* a, const double* a_
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = w; P.v_halo = w_halo; P.scal = d_scal;
   P.out = out; P.vout = v_out;
   set_epilogue(P, p, ch, nb, bcol, bidx);
+  ProfScope ps(c, EMHD_K_JV_NORMALIZED, 5.0 * 64.0 * (double)c->g.nx * c->g.ny);   // 5W
   return cerr(launch_stencil(P, MODE_JVN, p > 0, c->num_sms, c->stream));
 }
 
@@ -244,6 +288,7 @@ extern "C" int emhd_multidot(emhd_ctx* c, const double* w, const double* V, long
                              long long len_dot, int self, double* out) {
   if (!c || !w || !out || nvec < 0 || nvec > c->max_vectors || (nvec > 0 && !V)) return EMHD_ERR_ARG;
   KWork k = kwork(c);
+  ProfScope ps(c, EMHD_K_MULTIDOT, 8.0 * (nvec + 1) * (double)len_dot);
   return cerr(launch_multidot(w, V, ldv, nvec, len_dot, self ? 1 : 0, k, out, c->stream));
 }
 
@@ -254,6 +299,7 @@ extern "C" int emhd_update(emhd_ctx* c, double* w, const double* V, long long ld
   const double* g = mode == 1 ? take_skip(c) : nullptr;
   Reorth ro{};
   ro.skip2 = g;
+  ProfScope ps(c, mode == 1 ? EMHD_K_UPDATE_FINISH : EMHD_K_UPDATE, 8.0 * (nvec + 2) * (double)len_upd, g);
   return cerr(launch_update(w, V, ldv, nvec, h, len_upd, len_dot, len_max, mode, k, out, c->stream,
                             FinishArgs{}, nullptr, ro));
 }
@@ -296,8 +342,9 @@ extern "C" int emhd_update_push(emhd_ctx* c, double* w, const double* V, long lo
   P.nx = (unsigned)c->g.nx;
   P.ny = (unsigned)c->g.ny;
   if (P.n_top >= (1LL << 32)) return EMHD_ERR_ARG;
-  return cerr(launch_update_push(w, V, ldv, nvec, h, len_upd, len_dot, len_max, k, out, P, c->stream,
-                                 take_skip(c)));
+  const double* g = take_skip(c);
+  ProfScope ps(c, EMHD_K_UPDATE_FINISH, 8.0 * (nvec + 2) * (double)len_upd, g);
+  return cerr(launch_update_push(w, V, ldv, nvec, h, len_upd, len_dot, len_max, k, out, P, c->stream, g));
 }
 
 // Edge rows {0,1} and {nx-2,nx-1} of w into the neighbours' halo buffers (as emhd_update_push
@@ -330,6 +377,7 @@ extern "C" int emhd_update_finish(emhd_ctx* c, double* w, const double* V, long 
   F.brk_hist = brk_hist; F.st = c->st; F.rtol = 1e-12;
   Reorth ro{};
   ro.skip2 = take_skip(c);
+  ProfScope ps(c, EMHD_K_UPDATE_FINISH, 8.0 * (nvec + 2) * (double)len_upd, ro.skip2);
   return cerr(launch_update(w, V, ldv, nvec, h2, len_upd, len_dot, len_max, 1, k, nrm, c->stream, F,
                             nullptr, ro));
 }
@@ -337,6 +385,7 @@ extern "C" int emhd_update_finish(emhd_ctx* c, double* w, const double* V, long 
 extern "C" int emhd_norms(emhd_ctx* c, const double* x, long long len_sum, long long len_max, double* out) {
   if (!c || !x || !out) return EMHD_ERR_ARG;
   KWork k = kwork(c);
+  ProfScope ps(c, EMHD_K_NORMS, 8.0 * (double)(len_sum > len_max ? len_sum : len_max));
   return cerr(launch_norms(x, len_sum, len_max, k, out, c->stream));
 }
 
@@ -351,6 +400,7 @@ extern "C" int emhd_arnoldi_finish(emhd_ctx* c, const double* h1, const double* 
 extern "C" int emhd_div_scalar(emhd_ctx* c, const double* x, const double* d, int take_sqrt, double* out,
                                double* d_out, long long n) {
   if (!c || !x || !d || !out) return EMHD_ERR_ARG;
+  ProfScope ps(c, EMHD_K_DIV_SCALAR, 16.0 * (double)n);
   return cerr(launch_div_scalar(x, d, take_sqrt, out, d_out, n, c->num_sms, c->stream));
 }
 
@@ -653,6 +703,8 @@ struct emhd_arnoldi_args_s {
   double* evals;       // [m_cap + 1] 1 where iteration j evaluated the RHS (or null)
   double eta;          // selective re-orthogonalisation threshold (<= 0: always two passes)
   double* reorth;      // [m_cap + 1] 1 where iteration j skipped the second pass
+  double* md2;         // [m_cap + 1] (or null) 0 where iteration j needed a separate pass-2
+                       // multi-dot (pass 2 ran although the re-projection was predicted away)
 };
 
 // Iteration j of krylov.py:144-168 on one rank: (normalise w_{j-1} +) Jv, pass-1 multi-dot with
@@ -665,7 +717,9 @@ static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   c->epoch = j;
   double* out = (j % 2 == 0) ? A->w0 : A->w1;
   const double* skip = nullptr;
+  const double W = 8.0 * (double)A->n_top;
   if (gated) {
+    ProfScope ps(c, EMHD_K_GATE, 0.0);
     const int rc0 = cerr(launch_gate(c->cancel, (unsigned)A->gen, j, A->gate + j, c->stream));
     if (rc0) return rc0;
     skip = A->gate + j;
@@ -681,15 +735,20 @@ static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   if (j == 0) {
     if (gated) return EMHD_ERR_ARG;
     // sigma of the seed direction: max|V[0][:n]| into vn[1] (norms writes {sum, max})
-    rc = cerr(launch_norms(A->V, 0, A->n_top, k, A->vn, c->stream));
+    {
+      ProfScope ps(c, EMHD_K_NORMS, W);
+      rc = cerr(launch_norms(A->V, 0, A->n_top, k, A->vn, c->stream));
+    }
     if (rc) return rc;
     P.v = A->V; P.scal = A->vn + 1;
     if (A->p > 0) P.qsrc = A->V + A->n_top;
+    ProfScope ps(c, EMHD_K_JV, 4.0 * W);
     rc = cerr(launch_stencil(P, MODE_JV, A->p > 0, c->num_sms, c->stream));
   } else {
     P.v = (j % 2 == 0) ? A->w1 : A->w0;
     P.scal = A->scal;
     P.vout = A->V + (size_t)j * A->ldv;
+    ProfScope ps(c, EMHD_K_JV_NORMALIZED, 5.0 * W, skip);
     rc = cerr(launch_stencil(P, MODE_JVN, A->p > 0, c->num_sms, c->stream));
   }
   if (rc) return rc;
@@ -699,18 +758,73 @@ static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   F.scal = A->scal; F.brk_hist = A->brk; F.st = c->st; F.rtol = 1e-12;
   // pass 1 (multi-dot, update + re-projection + norms); with eta > 0 its last CTA decides
   // whether pass 2 is needed (selective re-orthogonalisation) and, if not, finishes the column
+  // With md2 gates the re-projection dots are predicted from the previous iteration's decision:
+  // if it skipped pass 2, this pass 1 computes only ||w1|| and max|w1| (no second read of the
+  // basis), and a gated multi-dot supplies h2 in the (rare) case pass 2 turns out to be needed.
   Reorth r1{}, r2{};
+  const double* md2 = nullptr;
   if (A->eta > 0.0 && A->reorth) {
     r1.eta2 = A->eta * A->eta;
     r1.gate_out = A->reorth + j;
     r2.skip2 = A->reorth + j;
+    if (A->md2) {
+      md2 = A->md2 + j;
+      r1.gate_md2 = A->md2 + j;
+      r1.predict = j > 1 ? A->reorth + (j - 2) : nullptr;   // both previous decisions: skip
+    }
   }
-  rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream, skip));
-  if (!rc) rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
-                                   A->d2, c->stream, F, skip, r1));
+  const double vb = 8.0 * (double)A->len_upd;
+  {
+    ProfScope ps(c, EMHD_K_MULTIDOT, (nv + 1) * vb, skip);
+    rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream, skip));
+  }
+  if (!rc) {
+    ProfScope ps(c, EMHD_K_UPDATE, (nv + 2) * vb, skip);
+    rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
+                            A->d2, c->stream, F, skip, r1));
+  }
+  if (!rc && md2) {
+    ProfScope ps(c, EMHD_K_MULTIDOT2, (nv + 1) * vb, skip, md2);
+    rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 0, k, A->d2, c->stream, skip, md2));
+  }
   if (rc) return rc;
+  ProfScope ps(c, EMHD_K_UPDATE_FINISH, (nv + 2) * vb, skip, r2.skip2);
   return cerr(launch_update(out, A->V, A->ldv, nv, A->d2, A->len_upd, A->len_dot, A->n_top, 1, k,
                             A->nrm, c->stream, F, skip, r2));
+}
+
+// Per-launch profiling of the Arnoldi path (emhd_arnoldi_iter / _run / _lookahead and the
+// emhd_jv / emhd_norms / emhd_div_scalar entry points): enable != 0 clears and starts it.
+extern "C" int emhd_profile(emhd_ctx* c, int enable) {
+  if (!c) return EMHD_ERR_ARG;
+  prof_clear(c);
+  c->prof = enable != 0;
+  return EMHD_OK;
+}
+
+// Synchronises the stream, then returns the records so far (at most max_n; kinds EMHD_K_*,
+// milliseconds, algorithmic bytes — 0 for a launch its device gate turned into a no-op) and
+// clears them.  Return value: number of records written (negative: error code).
+extern "C" int emhd_profile_read(emhd_ctx* c, int max_n, int* kinds, double* ms, double* bytes) {
+  if (!c || max_n < 0 || (max_n > 0 && (!kinds || !ms || !bytes))) return -EMHD_ERR_ARG;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return -EMHD_ERR_CUDA;
+  int n = 0;
+  for (auto& r : c->recs) {
+    if (n >= max_n) break;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.e0, r.e1);
+    double by = r.bytes;
+    for (int g = 0; g < 2; ++g) {
+      if (!r.gate[g]) continue;
+      double v = 0.0;
+      cudaMemcpy(&v, r.gate[g], sizeof(double), cudaMemcpyDeviceToHost);
+      if (v != 0.0) by = 0.0;
+    }
+    kinds[n] = r.kind; ms[n] = t; bytes[n] = by;
+    ++n;
+  }
+  prof_clear(c);
+  return n;
 }
 
 extern "C" int emhd_arnoldi_iter(emhd_ctx* c, const void* args, int j) {

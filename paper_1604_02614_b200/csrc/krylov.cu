@@ -110,8 +110,9 @@ __device__ __forceinline__ double2 ld2_stream(const double* p, long long e, long
 template <int VEC, int U>
 __global__ void __launch_bounds__(KT, 4) multidot_kernel(const double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, long long len_dot, int self,
-    double* partials, double* out, unsigned int* ticket, const double* skip) {
+    double* partials, double* out, unsigned int* ticket, const double* skip, const double* skip2) {
   if (skip && *skip != 0.0) return;            // cancelled look-ahead iteration (all CTAs agree)
+  if (skip2 && *skip2 != 0.0) return;          // gated second-pass multi-dot not needed
   extern __shared__ double s_acc[];            // [(nvec+1)][NWARP]
   constexpr int TL = KT * 2 * VEC;
   const int nval = nvec + self;
@@ -185,11 +186,13 @@ __device__ __forceinline__ void finish_column(const FinishArgs& F, const double*
 // projection already left w1 orthogonal to the basis to working precision (its error is
 // O(eps ||w||) <= O(eps ||w1|| / eta)), so the column is finished with h1 and the second
 // sweep is skipped; otherwise the reference's second pass runs.  Called by one CTA.
-__device__ void reorth_decide(const FinishArgs& F, const double* r, int nvec, double eta2, double* gate) {
+__device__ void reorth_decide(const FinishArgs& F, const double* r, int nvec, double eta2, double* gate,
+                              double* gate_md2 = nullptr, bool reprojected = true) {
   __shared__ int s_skip;
   if (threadIdx.x == 0) {
     s_skip = r[nvec] >= eta2 * F.selfdot[0] ? 1 : 0;
     *gate = s_skip ? 1.0 : 0.0;
+    if (gate_md2) *gate_md2 = (s_skip || reprojected) ? 1.0 : 0.0;
   }
   __syncthreads();
   if (s_skip) {
@@ -222,6 +225,9 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const HaloPush push = HaloPush{}, const double* skip = nullptr, const Reorth ro = Reorth{}) {
   if (skip && *skip != 0.0) return;            // cancelled look-ahead iteration (all CTAs agree)
   if (ro.skip2 && *ro.skip2 != 0.0) return;    // pass 2 not needed (decided by pass 1)
+  // mode 0: the CGS2 re-projection dots, unless the previous iteration's decision predicts
+  // that pass 2 will be skipped again (then only ||w1|| and max|w1| are needed)
+  const bool reproj = MODE == 0 && !(ro.predict && ro.predict[0] != 0.0 && ro.predict[1] != 0.0);
   extern __shared__ double sm[];
   constexpr int TL = KT * 2;
   double* s_h = sm;                              // [nvec]
@@ -258,7 +264,7 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
       if (full) push_edge(push, e + 1, wv.y);
     }
     const double dx = (e < len_dot) ? wv.x : 0.0, dy = (e + 1 < len_dot) ? wv.y : 0.0;
-    if (MODE == 0) {
+    if (reproj) {
       // re-read the basis newest-first: the vectors just streamed by the update are the
       // likeliest to still sit in L1/L2 (halves the mean reuse distance of the tile)
       for (int i = (nvec - 1) / U * U; i >= 0; i -= U) {
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const bool last = finish_partials_maxidx(partials, nval, gridDim.x, max_kind, out, ticket);
     if (last && ro.gate_out) {
       __syncthreads();
-      reorth_decide(fin, out, nvec, ro.eta2, ro.gate_out);
+      reorth_decide(fin, out, nvec, ro.eta2, ro.gate_out, ro.gate_md2, reproj);
     }
   }
 }
@@ -473,11 +479,12 @@ static int grid_for(long long len, int tile, int num_sms) {
 }
 
 cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
-                            int self, KWork& wk, double* out, cudaStream_t s, const double* skip) {
+                            int self, KWork& wk, double* out, cudaStream_t s, const double* skip,
+                            const double* skip2) {
   const int G = grid_for(len_dot, KT * 4, wk.num_sms);
   const size_t sm = sizeof(double) * (size_t)(nvec + 1) * NWARP;
   multidot_kernel<2, 4><<<G, KT, sm, s>>>(w, V, ldv, nvec, len_dot, self, wk.partials, out, wk.ticket,
-                                          skip);
+                                          skip, skip2);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,11 @@ struct Reorth {               // selective (DGKS) re-orthogonalisation of one Ar
   double eta2;               // pass 2 is skipped when ||w1||^2 >= eta2 ||w||^2 (0: never decide)
   double* gate_out;          // update mode 0: decision written here (1 = pass 2 skipped)
   const double* skip2;       // pass-2 launches: no work when *skip2 != 0
+  const double* predict;     // update mode 0: predict[0] and predict[1] != 0 (the two previous
+                             // iterations skipped pass 2) -> predicted unnecessary again, so the
+                             // re-projection dots are not computed (null: always computed)
+  double* gate_md2;          // update mode 0: 0 when pass 2 must run but its dots are missing
+                             // (a separate multi-dot then computes them), else 1
 };
 
 struct HaloPush {            // peer halo destinations of a slab's edge rows (null: none)
@@ -43,7 +48,8 @@ struct CombineOut {
 };
 
 cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
-                            int self, KWork& wk, double* out, cudaStream_t s, const double* skip = nullptr);
+                            int self, KWork& wk, double* out, cudaStream_t s, const double* skip = nullptr,
+                            const double* skip2 = nullptr);
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
                           long long len_upd, long long len_dot, long long len_max, int mode,
                           KWork& wk, double* out, cudaStream_t s, FinishArgs fin = FinishArgs{},

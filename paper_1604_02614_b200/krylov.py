@@ -52,6 +52,9 @@ LOOKAHEAD_OVERRIDE = None
 # it/s, config 1 0.71 -> 0.58 s, config-3 physics at 1024^2 1.86 -> 1.68 s (eta 1/sqrt(2): 1630
 # it/s, 0.65 s, 1.82 s).
 REORTH_ETA = float(os.environ.get("EMHD_REORTH_ETA", "0.5"))
+# fast path: the first update pass skips the re-projection dots when the previous iteration
+# skipped its second pass (a gated multi-dot computes them on a misprediction)
+PREDICT_REPROJECTION = os.environ.get("EMHD_PREDICT_REPROJ", "1") != "0"
 
 
 class KrylovConvergenceError(RuntimeError):
@@ -212,7 +215,7 @@ class _Process:
         k = self.m_cap + 4
         hw = max(self.m_cap, 1)
         # one zero-filled block for H and every small scalar area (a single fill launch)
-        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + 4 * (self.m_cap + 1) + 4,
+        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + 5 * (self.m_cap + 1) + 4,
                                   dtype=D.F64, device=D.device())
         o = (self.m_cap + 1) * hw
         self.H = self._small[:o].view(self.m_cap + 1, hw)
@@ -226,6 +229,7 @@ class _Process:
         self.gate = self._small[o3:o3 + self.m_cap + 1]       # look-ahead gates (fast path)
         self.evals = self._small[o3 + self.m_cap + 1:o3 + 2 * (self.m_cap + 1)]   # RHS evals per iteration
         self.reorth = self._small[o3 + 2 * (self.m_cap + 1):o3 + 3 * (self.m_cap + 1)]  # 1: pass 2 skipped
+        self.md2 = self._small[o3 + 3 * (self.m_cap + 1):o3 + 4 * (self.m_cap + 1)]     # 0: separate h2 dots
         self.eta = REORTH_ETA if engine.fused else 0.0
         self.scal = D.Scratch(4)
         self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
@@ -282,6 +286,8 @@ class _Process:
             A.gen = self._new_gen()
             A.gate, A.evals = D.ptr(self.gate), D.ptr(self.evals)
             A.eta, A.reorth = self.eta, D.ptr(self.reorth)
+            # re-projection dots predicted from the previous decision (fast path only)
+            A.md2 = D.ptr(self.md2) if PREDICT_REPROJECTION else None
             self._args = A
             self._args_ref = D.ctypes_byref(A)
 
