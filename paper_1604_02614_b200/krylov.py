@@ -185,7 +185,8 @@ class _Generic(_Engine):
 class _Process:
     """Device Arnoldi factorisation (reference _ArnoldiProcess, krylov.py:127-188)."""
 
-    def __init__(self, engine, seed, m_cap, n_top, p=0, layout=None, comm=None, persistent=False):
+    def __init__(self, engine, seed, m_cap, n_top, p=0, layout=None, comm=None, persistent=False,
+                 reorthogonalize=True):
         self.eng = engine
         self.ctx = engine.ctx
         self.lib = self.ctx.lib
@@ -230,7 +231,9 @@ class _Process:
         self.evals = self._small[o3 + self.m_cap + 1:o3 + 2 * (self.m_cap + 1)]   # RHS evals per iteration
         self.reorth = self._small[o3 + 2 * (self.m_cap + 1):o3 + 3 * (self.m_cap + 1)]  # 1: pass 2 skipped
         self.md2 = self._small[o3 + 3 * (self.m_cap + 1):o3 + 4 * (self.m_cap + 1)]     # 0: separate h2 dots
-        self.eta = REORTH_ETA if engine.fused else 0.0
+        # reorthogonalize=False (the reference's single projection pass): the decision always
+        # skips pass 2; otherwise selective on the fused engines, both passes elsewhere
+        self.eta = (REORTH_ETA if engine.fused else 0.0) if reorthogonalize else 1e-300
         self.scal = D.Scratch(4)
         self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
@@ -763,7 +766,7 @@ def arnoldi(op, v, m, reorthogonalize=True):
     n_glob = (layout.nx_global * layout.ny * 8) if layout is not None else vd.numel()
     if m > n_glob:
         raise ValueError(f"basis size {m} exceeds operator dimension {op.n}")
-    proc = _Process(eng, vd, m, vd.numel(), 0, layout, comm)
+    proc = _Process(eng, vd, m, vd.numel(), 0, layout, comm, reorthogonalize=bool(reorthogonalize))
     proc.extend_many(m)
     proc.settle()
     return proc.basis(host=host)
@@ -816,7 +819,8 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
             outs = [t[2] for t in _into]
         return ([D.to_host(o) for o in outs] if host else outs), stats
     c_big = max(scales)
-    proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm, persistent=True)
+    proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm, persistent=True,
+                    reorthogonalize=cfg.reorthogonalize)
     m_target = min(cfg.m_init, proc.n)
     proc.extend_many(m_target)
     proc.settle()
@@ -925,6 +929,7 @@ def phi_comb(req, cfg=None, _zero=None):
         seed[:n_top].copy_(u)
         seed[n_top:n_top + p].copy_(torch.from_numpy(q))
         proc = _Process(eng, seed[:n_top + p], min(cfg.m_max, naug_glob), n_top, p, layout, comm,
+                        reorthogonalize=cfg.reorthogonalize,
                         persistent=True)
         m_target = min(cfg.m_init, naug_glob)
         proc.extend_many(m_target)

@@ -625,3 +625,28 @@ def test_push_edges_gate(P):
         else:
             assert bool((lo[1] == -7.0).all()) and bool((hi[0] == -7.0).all())
         assert bool((lo[0] == -7.0).all()) and bool((hi[1] == -7.0).all())
+
+
+def test_arnoldi_reorthogonalize_false_is_one_pass(P):
+    """reorthogonalize=False (the reference's single projection pass, krylov.py:191): no
+    iteration runs the second pass; on a well-conditioned operator the factorisation still
+    matches the two-pass one to round-off."""
+    z = golden("krylov_dense.npz")
+    op = P.LinearOperator.from_matrix(z["A"])
+    b1 = P.arnoldi(op, z["v"], 8, reorthogonalize=False)
+    assert np.max(np.abs(b1.H - z["H"])) <= 1e-10
+    # one classical pass: orthogonality degrades with j (measured 8.6e-12 at m = 8), which is
+    # what the reference's default second pass is for
+    assert np.max(np.abs(b1.V.T @ b1.V - np.eye(b1.V.shape[1]))) <= 1e-10
+    assert b1.second_pass is not None and not np.any(b1.second_pass)
+    b2 = P.arnoldi(op, z["v"], 8)
+    assert b2.second_pass is None                  # generic operators: always both passes
+    zz = golden("krylov_mhd.npz")
+    gt, pt = zz["grid"], zz["params"]
+    g = P.Grid2D(int(gt[0]), int(gt[1]), gt[2], gt[3], gt[4], gt[5])
+    prm = P.MhdParams(mu=pt[0], eta=pt[1], kappa=pt[2], gamma=pt[3], b_half=bool(pt[4]))
+    f = P.make_rhs(prm, g, P.BoundaryPolicy("periodic", "reflect"))
+    bf = P.arnoldi(P.FdJacobianOperator(f, zz["a"], zz["fa"]), zz["v"], 12, reorthogonalize=False)
+    assert not np.any(bf.second_pass)
+    assert np.max(np.abs(bf.V.T @ bf.V - np.eye(bf.V.shape[1]))) <= 1e-10
+    assert np.linalg.norm(bf.H - zz["H"]) <= 1e-8 * np.linalg.norm(zz["H"])
