@@ -55,6 +55,8 @@ REORTH_ETA = float(os.environ.get("EMHD_REORTH_ETA", "0.5"))
 # fast path: the first update pass skips the re-projection dots when the previous iteration
 # skipped its second pass (a gated multi-dot computes them on a misprediction)
 PREDICT_REPROJECTION = os.environ.get("EMHD_PREDICT_REPROJ", "1") != "0"
+# reporting: count kept iterations / second passes per context (tools/run_configs.py)
+COUNT_PASSES = False
 
 
 class KrylovConvergenceError(RuntimeError):
@@ -729,6 +731,18 @@ class _Process:
         elif st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE | N.ST_DENSE):
             self.ctx.reset_status()
 
+    def account_passes(self):
+        """Reporting only (COUNT_PASSES): add this projection's kept iterations and second
+        passes to the context's device counters (no host sync; read with pass_counts(ctx))."""
+        m = self.m
+        if m <= 0 or not COUNT_PASSES:
+            return
+        acc = getattr(self.ctx, "_pass_acc", None)
+        if acc is None:
+            acc = self.ctx._pass_acc = torch.zeros(2, dtype=D.F64, device=D.device())
+        acc[0] += m
+        acc[1] += (m - self.reorth[:m].sum()) if self.eta > 0.0 else float(m)
+
     def _brk(self):
         if not hasattr(self, "_brk_t"):
             self._brk_t = torch.tensor([0.0, 0.0, 1.0, 0.0], dtype=D.F64).to(D.device())
@@ -770,6 +784,16 @@ def arnoldi(op, v, m, reorthogonalize=True):
     proc.extend_many(m)
     proc.settle()
     return proc.basis(host=host)
+
+
+def pass_counts(ctx):
+    """(iterations kept, of which ran the second Gram-Schmidt pass) over the projections of
+    multi_scale_eval / phi_comb on this context so far (reporting; one host sync)."""
+    acc = getattr(ctx, "_pass_acc", None)
+    if acc is None:
+        return 0, 0
+    a = acc.cpu().numpy()
+    return int(a[0]), int(a[1])
 
 
 def residual_estimate(basis, h, c, small_phi_seed):
@@ -868,6 +892,7 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
         proc.resolve_status(hi)
         nxt = hi + 1                              # hi was just checked and failed
     stats.operator_applies += proc.applies
+    proc.account_passes()
     stats.max_basis_size = proc.m
     stats.substeps = 1
     Y, _ = proc.phi_coeffs(order, [c * h for c in scales])
@@ -987,6 +1012,7 @@ def phi_comb(req, cfg=None, _zero=None):
             delta = delta / 2.0                       # soft cap, or hard cap above min_substep
             nxt = proc.m
         stats.operator_applies += proc.applies
+        proc.account_passes()
         u_new = torch.empty(n_top, dtype=D.F64, device=D.device())
         proc.combine(Y, [u_new])
         u = u_new

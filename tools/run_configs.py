@@ -98,8 +98,20 @@ def main():
                                     cfg=cfg, recoverable=(P.AdmissibilityError,),
                                     max_steps=run.get("max_steps"))
 
-    for _ in range(max(a.repeat - 1, 0)):
+    from paper_1604_02614_b200 import krylov as _K
+    from paper_1604_02614_b200.krylov import pass_counts
+    # second-pass counts come from the last warm-up run (the runs are identical); the timed run
+    # does no reporting work (with --repeat 1 it counts itself)
+    passes = None
+    for k in range(max(a.repeat - 1, 0)):
+        _K.COUNT_PASSES = k == a.repeat - 2
+        pc0 = pass_counts(f.ctx)
         go(f, yd)                      # warm-up runs (module loading, allocator)
+        if _K.COUNT_PASSES:
+            pc1 = pass_counts(f.ctx)
+            passes = [pc1[1] - pc0[1], pc1[0] - pc0[0]]
+    _K.COUNT_PASSES = passes is None
+    pc0 = pass_counts(f.ctx)
     torch.cuda.synchronize()
     prof = None
     if a.profile:
@@ -121,7 +133,9 @@ def main():
         ps.print_stats(int(os.environ.get("PROF_N", "25")))
         ps.print_callers("torch.empty|settle")
     out = {"config": a.config, "grid": n, "run": run, "gpu_seconds": T, "stats": stats_dict(st),
-           "speculative_discarded": getattr(f.ctx, "spec_dropped", 0) - drop0, "cuda_allocs_in_run": alloc,
+           "speculative_discarded": getattr(f.ctx, "spec_dropped", 0) - drop0,
+           "second_gram_schmidt_passes": passes if passes is not None else
+               [pass_counts(f.ctx)[1] - pc0[1], pass_counts(f.ctx)[0] - pc0[0]], "cuda_allocs_in_run": alloc,
            "iterations_per_s": st.operator_applies / T,
            "cell_steps_per_s": g.nx * g.ny * st.steps_accepted / T}
     if a.check:
