@@ -53,3 +53,36 @@ def test_phi_dense_random_matrices(n, scale, k, seed):
     want = krylov_cpu.phi_block(k, M)
     for a, b in zip(got, want):
         assert np.max(np.abs(a - b)) <= 1e-11 * max(1.0, np.max(np.abs(b)))
+
+
+@settings(max_examples=12, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(nx=st.integers(8, 40), ny=st.integers(8, 90), bx=st.sampled_from(BCS), by=st.sampled_from(BCS),
+       m=st.integers(3, 24), seed=st.integers(0, 2 ** 31 - 1))
+def test_selective_reorth_fd_arnoldi_random(nx, ny, bx, by, m, seed):
+    """Fused FD Arnoldi on random states: the selective second pass (eta = 0.5) and the
+    reference's always-two-pass order give the oracle's H (1e-8, FD round-off amplification)
+    and an orthonormal basis."""
+    import paper_1604_02614_b200 as P
+    from paper_1604_02614_b200 import krylov
+    from oracle import jvp, krylov_cpu, stencil
+    rng = np.random.default_rng(seed)
+    g = P.Grid2D(nx, ny, 0.0, 1.0, 0.0, 2.0)
+    prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    bc = P.BoundaryPolicy(bx, by)
+    U = _state(rng, nx, ny)
+    y = U.reshape(-1)
+    v = rng.standard_normal(y.size)
+    ref = krylov_cpu.arnoldi(jvp.FdJv(stencil.rhs_closure(prm, g, bc), y), v, m)
+    _, Href = ref.snapshot()
+    f = P.make_rhs(prm, g, bc)
+    old = krylov.REORTH_ETA
+    try:
+        for eta in (0.0, 0.5):
+            krylov.REORTH_ETA = eta
+            b = P.arnoldi(P.FdJacobianOperator(f, y), v, m)
+            assert b.m == ref.m and b.breakdown == ref.broke
+            k = min(b.H.shape[0], Href.shape[0])
+            assert np.linalg.norm(b.H[:k] - Href[:k]) <= 1e-8 * np.linalg.norm(Href), eta
+            assert np.max(np.abs(b.V.T @ b.V - np.eye(b.V.shape[1]))) <= 1e-12, eta
+    finally:
+        krylov.REORTH_ETA = old
