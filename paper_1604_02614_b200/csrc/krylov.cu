@@ -472,10 +472,15 @@ cudaError_t launch_evals_discount(const double* evals, int count, DevStatus* st,
   return cudaGetLastError();
 }
 
+// Up to 4 CTAs per SM, every CTA the same number of tiles (1024 tiles on 592 CTAs would leave
+// 160 CTAs with one tile while the rest do two: 512 CTAs of two tiles finish at the same time)
 static int grid_for(long long len, int tile, int num_sms) {
   long long tiles = (len + tile - 1) / tile;
-  long long g = 4LL * num_sms;
-  return (int)(tiles < g ? (tiles < 1 ? 1 : tiles) : g);
+  if (tiles < 1) tiles = 1;
+  const long long g = 4LL * num_sms;
+  if (tiles <= g) return (int)tiles;
+  const long long per = (tiles + g - 1) / g;
+  return (int)((tiles + per - 1) / per);
 }
 
 cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
