@@ -649,6 +649,210 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
 }
 
 
+// ---- small grids: one thread per output cell on a 2D tile -------------------------------
+// The row-marching kernel above pays (rows + 4) dependent row steps per CTA; on small grids
+// (a few rows per CTA) that latency dominates.  Here a CTA owns a TR x TC tile and runs three
+// barrier-separated phases over it: primitives of the (TR+4) x (TC+4) halo region, x/y fluxes
+// of the cells around the tile, then the outputs.  Every value is produced by the same device
+// functions in the same operation order as the marching kernel, so outputs are bit-identical.
+constexpr int TT_R = 8, TT_C = 32, TT_THREADS = TT_R * TT_C;
+constexpr int TT_QR = TT_R + 4, TT_QC = TT_C + 4, TT_QN = TT_QR * TT_QC;   // primitive region
+
+size_t tile_stencil_smem() {
+  return sizeof(double) * ((size_t)(NQ + NC) * TT_QN + (size_t)NF * (TT_R + 2) * TT_C +
+                           (size_t)NF * TT_R * (TT_C + 2));
+}
+
+template <int MODE, bool AUG, int FXY>
+__global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const StencilParams P) {
+  extern __shared__ double smem[];
+  double* q = smem;                                   // [NQ][TT_QR][TT_QC]
+  double* cq = q + NQ * TT_QN;                        // [NC][TT_QR][TT_QC]
+  double* gxs = cq + NC * TT_QN;                      // [NF][TT_R + 2][TT_C]   rows -1 .. TR
+  double* gys = gxs + NF * (TT_R + 2) * TT_C;         // [NF][TT_R][TT_C + 2]   cols -1 .. TC
+  const int t = threadIdx.x;
+  const int i0 = blockIdx.y * TT_R, j0 = blockIdx.x * TT_C;
+  const bool lead = blockIdx.x == 0 && blockIdx.y == 0 && t == 0;
+  if (P.skip && *P.skip != 0.0) {
+    if (lead && P.evals) *P.evals = 0.0;
+    return;
+  }
+  const int nro = min(TT_R, P.nx - i0), nco = min(TT_C, P.ny - j0);   // output extent
+  const unsigned plane = (unsigned)P.nx * (unsigned)P.ny;
+  double sigma = 1.0, rsig = 1.0, hnext = 1.0, rh = 1.0;
+  bool skip_stencil = false;
+  if (MODE == MODE_JV) {
+    const double vn = P.scal[0];
+    skip_stencil = (vn == 0.0);
+    sigma = fd_sigma(vn);
+    rsig = 1.0 / sigma;
+  } else if (MODE == MODE_JVN) {
+    if (P.scal[2] != 0.0) {
+      // queued after a breakdown: zero output, no flags, no RHS count (as the marching kernel)
+      const int r = t / TT_C, c = t % TT_C;
+      if (r < nro && c < nco)
+        for (int f = 0; f < NF; ++f) P.out[(unsigned)(i0 + r) * P.ny + j0 + c + f * plane] = 0.0;
+      if (lead) for (int k = 0; k < P.p; ++k) P.out[P.n_top + k] = 0.0;
+      if (lead && P.evals) *P.evals = 0.0;
+      return;
+    }
+    hnext = P.scal[0];
+    rh = 1.0 / hnext;
+    const double vn = P.scal[1] / hnext;
+    skip_stencil = (vn == 0.0);
+    sigma = fd_sigma(vn);
+    rsig = 1.0 / sigma;
+  }
+  const bool fsig = recip_tight(sigma, rsig);
+  const bool fh = recip_tight(hnext, rh);
+  double qv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (AUG) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+      if (k < P.p) qv[k] = MODE == MODE_JVN ? div_const(P.v[P.n_top + k], hnext, rh) : P.qsrc[k];
+  }
+  int flag = 0;
+  unsigned long long bad = ~0ull;
+  const int ro = t / TT_C, co = t % TT_C;              // this thread's output cell
+  const bool own = ro < nro && co < nco;
+  const unsigned o = (unsigned)(i0 + ro) * P.ny + j0 + co;
+
+  if (skip_stencil) {
+    if (own) {
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const unsigned idx = o + f * plane;
+        double val = 0.0;
+        if (AUG) {
+          val = __dmul_rn(P.ch, 0.0);
+          for (int k = 0; k < P.nb; ++k) val = __dadd_rn(val, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
+        }
+        P.out[idx] = val;
+        if (MODE == MODE_JVN) P.vout[idx] = div_const(__ldg(P.v + idx), hnext, rh);
+      }
+    }
+  } else {
+    // phase 1: primitives of rows i0-2 .. i0+nro+1, columns j0-2 .. j0+nco+1
+    for (int e = t; e < TT_QN; e += TT_THREADS) {
+      const int rr = e / TT_QC, cc = e % TT_QC;
+      if (rr >= nro + 4 || cc >= nco + 4) continue;
+      const int i = i0 - 2 + rr, j = j0 - 2 + cc;
+      const RowRef R = row_ref(P, i);
+      bool yf;
+      const int js = map_ghost(j, P.ny, P.bcy, yf);
+      RawCell<MODE> x;
+      fetch_cell<MODE>(P, R, js, x);
+      double u[NF];
+      double vj[MODE == MODE_JVN ? NF : 1];
+      const bool owned = rr >= 2 && rr < nro + 2 && cc >= 2 && cc < nco + 2;
+      combine_cell<MODE>(x, R.flip ? 0x80000000u : 0u, yf ? 0x80000000u : 0u, sigma, hnext, rh, fh, u,
+                         (MODE == MODE_JVN && owned) ? vj : nullptr);
+      cell_prims(P, u, q + e, cq + e, TT_QN, flag);
+      if (MODE == MODE_JVN && owned) {
+        const unsigned ov = (unsigned)i * P.ny + j;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) P.vout[ov + f * plane] = vj[f];
+      }
+    }
+    __syncthreads();
+    // phase 2: x-fluxes at rows -1 .. nro (output columns), y-fluxes at columns -1 .. nco
+    // (output rows); flux cell (fr, fc) sits at region cell (fr + 2, fc + 2)
+    constexpr int FR = TT_R + 2, FC = TT_C + 2;
+    for (int e = t; e < FR * FC; e += TT_THREADS) {
+      const int fr = e / FC - 1, fc = e % FC - 1;
+      const bool need_x = fc >= 0 && fc < nco && fr <= nro;
+      const bool need_y = fr >= 0 && fr < nro && fc <= nco;
+      if (!need_x && !need_y) continue;
+      const int rr = fr + 2, cc = fc + 2;
+      double gx[NF], gy[NF];
+      flux_cell<FXY>(P, q + (rr - 1) * TT_QC, q + rr * TT_QC, q + (rr + 1) * TT_QC, cq + rr * TT_QC, cc,
+                     TT_QN, need_x, need_y, gx, gy);
+      if (need_x) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) gxs[(f * (TT_R + 2) + fr + 1) * TT_C + fc] = gx[f];
+      }
+      if (need_y) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) gys[(f * TT_R + fr) * (TT_C + 2) + fc + 1] = gy[f];
+      }
+    }
+    __syncthreads();
+    // phase 3: outputs (as the marching kernel's output stage)
+    if (own) {
+      unsigned nfmask = 0;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const double* gxf = gxs + f * (TT_R + 2) * TT_C;
+        const double* gyf = gys + (f * TT_R + ro) * (TT_C + 2);
+        const double ddx = div_c<FXY>(__dsub_rn(gxf[(ro + 2) * TT_C + co], gxf[ro * TT_C + co]), P.two_hx, P.r_two_hx);
+        const double ddy = div_c<FXY>(__dsub_rn(gyf[co + 2], gyf[co]), P.two_hy, P.r_two_hy);
+        const double F = __dsub_rn(-ddx, ddy);
+        const unsigned idx = o + f * plane;
+        if (MODE == MODE_RHS) {
+          P.out[idx] = F;
+        } else {
+          nfmask |= (((unsigned)__double2hiint(F) & 0x7ff00000u) + 0x00100000u) >> (31 - f) & (1u << f);
+          const double df = __dsub_rn(F, __ldg(P.fa + idx));
+          double jv = fsig ? div_const1(df, sigma, rsig) : div_const(df, sigma, rsig);
+          if (AUG) {
+            jv = __dmul_rn(P.ch, jv);
+            for (int k = 0; k < P.nb; ++k) jv = __dadd_rn(jv, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
+          }
+          P.out[idx] = jv;
+        }
+      }
+      if (MODE != MODE_RHS && nfmask) {
+        const unsigned long long gidx = (unsigned long long)(__ffs(nfmask) - 1) * P.nxg * P.ny +
+            (unsigned long long)(P.x_off + i0 + ro) * P.ny + j0 + co;
+        bad = gidx < bad ? gidx : bad;
+      }
+    }
+  }
+
+  // tail of the augmented output: bottom = upshift(q) (krylov.py:271-272); v_j tail
+  if (AUG && blockIdx.x == 0 && blockIdx.y == 0 && t < P.p) {
+    double nxt = 0.0, cur = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (k == t + 1 && k < P.p) nxt = qv[k];
+      if (k == t) cur = qv[k];
+    }
+    P.out[P.n_top + t] = nxt;
+    if (MODE == MODE_JVN) P.vout[P.n_top + t] = cur;
+  }
+  __shared__ int s_flag;
+  __shared__ unsigned long long s_bad;
+  if (t == 0) { s_flag = 0; s_bad = ~0ull; }
+  __syncthreads();
+  if (flag) atomicOr(&s_flag, flag);
+  if (bad != ~0ull) atomicMin(&s_bad, bad);
+  __syncthreads();
+  if (t == 0) {
+    if (s_flag) {
+      atomicOr(&P.st->flags, s_flag);
+      atomicMin(&P.st->fail_iter, P.epoch);
+    }
+    if (s_bad != ~0ull) {
+      atomicOr(&P.st->flags, (int)ST_NONFINITE);
+      atomicMin(&P.st->first_nonfinite, s_bad);
+      atomicMin(&P.st->fail_iter, P.epoch);
+    }
+    if (!skip_stencil && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&P.st->rhs_evals, 1);
+    if (P.evals && blockIdx.x == 0 && blockIdx.y == 0) *P.evals = skip_stencil ? 0.0 : 1.0;
+  }
+}
+
+template <int MODE, bool AUG, int FXY>
+static cudaError_t launch_tile(const StencilParams& P, cudaStream_t s) {
+  auto k = tile_stencil_kernel<MODE, AUG, FXY>;
+  const size_t sm = tile_stencil_smem();
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid((P.ny + TT_C - 1) / TT_C, (P.nx + TT_R - 1) / TT_R);
+  k<<<grid, TT_THREADS, sm, s>>>(P);
+  return cudaGetLastError();
+}
+
 // ---- admissibility diagnostics (error path only) ---------------------------
 __device__ __forceinline__ unsigned long long ord_key(double x) {
   unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -811,6 +1015,14 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
       if (min_rows < 1) min_rows = 1;
     }
     P.rows_per_cta = rows < min_rows ? min_rows : rows;
+    // few rows per CTA: the marching kernel's dependent row steps dominate; the 2D-tile
+    // kernel (three barrier-separated phases, bit-identical outputs) is faster there
+    static int tile_rows = -1;
+    if (tile_rows < 0) {
+      const char* env = getenv("EMHD_STENCIL_TILE_ROWS");
+      tile_rows = env ? atoi(env) : 6;
+    }
+    if (rows < tile_rows) return launch_tile<MODE, AUG, FXY>(P, s);
   }
   dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
   k<<<grid, TY, sm, s>>>(P);
