@@ -152,3 +152,63 @@ def _worker(rank, size, port, tmpdir):
 @pytest.mark.parametrize("size", [2, 3])
 def test_slab_ranks_on_one_gpu_match_reference(size, tmp_path):
     mp.spawn(_worker, args=(size, _port(), str(tmp_path)), nprocs=size, join=True)
+
+
+def _symm_worker(rank, port, q):
+    """One NCCL rank: torch symmetric memory + the library's halo-push entry points on the
+    rank's own symmetric buffer (its own 'peer' view), the plumbing slab.PushHalo relies on."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+        import paper_1604_02614_b200 as P
+        from paper_1604_02614_b200 import _native as N
+        from paper_1604_02614_b200 import device as D
+        from paper_1604_02614_b200.mhd import GpuRhs
+        from paper_1604_02614_b200.slab import halo_shape, make_layout
+        g = P.Grid2D(24, 40, 0.0, 1.0, 0.0, 1.0)
+        L = make_layout(g.nx, g.ny, "periodic", 1, 3)          # a middle slab's geometry
+        f = GpuRhs(P.MhdParams(), g, P.BoundaryPolicy("periodic", "reflect"), layout=L)
+        n = 2 * 8 * 2 * g.ny
+        buf = symm_mem.empty(n, dtype=torch.float64, device="cuda")
+        buf.fill_(-7.0)
+        hdl = symm_mem.rendezvous(buf, dist.group.WORLD)
+        peer = hdl.get_buffer(0, (n,), torch.float64, 0)
+        rng = np.random.default_rng(3)
+        w = torch.from_numpy(rng.standard_normal(L.n_local)).cuda()
+        h = f.ctx.sync_stream()
+        gate = torch.ones(1, dtype=torch.float64, device="cuda")
+        # own symmetric buffer as both neighbours' halo: lo side 1 <- our rows 0,1; hi side 0 <-
+        # our last two rows (what Comm.exchange would deliver to the neighbours)
+        N.check(f.ctx.lib.emhd_push_edges(h, D.ptr(w), D.ptr(peer), D.ptr(peer), D.ptr(gate)))
+        send = torch.empty(halo_shape(g.ny), dtype=torch.float64, device="cuda")
+        N.check(f.ctx.lib.emhd_pack_edges(h, D.ptr(w), D.ptr(send)))
+        torch.cuda.synchronize()
+        got = buf.view(halo_shape(g.ny))
+        t = torch.ones(3, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        q.put(bool(torch.equal(got[1], send[0]) and torch.equal(got[0], send[1]) and t.sum().item() == 3.0))
+    except Exception as e:                    # noqa: BLE001 - reported to the parent
+        q.put(repr(e))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_symmetric_memory_halo_push_plumbing_single_rank():
+    """torch symmetric memory (allocation, rendezvous, peer view) and emhd_push_edges into a
+    symmetric buffer on a 1-rank NCCL group: the pieces of the multi-GPU halo push that one GPU
+    can exercise (no rank waits on another)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_symm_worker, args=(0, _port(), q))
+    p.start()
+    p.join(timeout=180)
+    if p.is_alive():
+        p.kill()
+        pytest.fail("symmetric-memory worker hung")
+    assert q.get(timeout=5) is True
