@@ -650,3 +650,36 @@ def test_arnoldi_reorthogonalize_false_is_one_pass(P):
     assert not np.any(bf.second_pass)
     assert np.max(np.abs(bf.V.T @ bf.V - np.eye(bf.V.shape[1]))) <= 1e-10
     assert np.linalg.norm(bf.H - zz["H"]) <= 1e-8 * np.linalg.norm(zz["H"])
+
+
+@pytest.mark.parametrize("look", [None, 4])
+def test_adaptive_recoverable_rejections_match_oracle(P, look):
+    """EpiRK5P1 on a near-vacuum reconnection state with an oversized first step: trial steps
+    fail with AdmissibilityError (recoverable) or Krylov non-convergence and are retried with a
+    smaller h, as epirk.py:350-411 does; trajectory and every StepStats counter (rejections
+    included) equal the oracle's, with and without look-ahead iterations."""
+    from paper_1604_02614_b200 import krylov
+    from oracle import epirk_cpu, stencil
+    g = P.ReconnectionSpec().grid(32, 32)
+    prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    U = P.reconnection_ic(g, params=prm)
+    rho = U[0]
+    U[7] = P.energy_from(rho, U[1:4] / rho, U[4:7], 1e-3 * 0.5 * rho, prm)
+    bc = P.default_bc("reconnection")
+    y0 = U.reshape(-1)
+    yo, to = epirk_cpu.run_adaptive(stencil.rhs_closure(prm, g, bc), y0, 0.0, 20.0,
+                                    epirk_cpu.Controller(tol=1e-6, h_init=8.0),
+                                    recoverable=(stencil.InadmissibleState,), max_steps=2)
+    old = krylov.LOOKAHEAD_OVERRIDE
+    krylov.LOOKAHEAD_OVERRIDE = look
+    try:
+        y, S = P.integrate_adaptive(P.make_rhs(prm, g, bc), y0, 0.0, 20.0,
+                                    P.StepController(tol=1e-6, h_init=8.0),
+                                    recoverable=(P.AdmissibilityError,), max_steps=2)
+    finally:
+        krylov.LOOKAHEAD_OVERRIDE = old
+    assert to.steps_rejected > 0
+    for k in ("steps_accepted", "steps_rejected", "projections", "rhs_evals", "operator_applies",
+              "substeps", "max_basis_size"):
+        assert getattr(S, k) == getattr(to, k), k
+    assert np.linalg.norm(y - yo) <= 1e-8 * np.linalg.norm(yo)
