@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <utility>
 
 namespace emhd {
 
@@ -112,6 +113,39 @@ __device__ __forceinline__ int multi_index(int lane) {
 #pragma unroll
   for (int b = K; b > 1; b >>= 1, off >>= 1) idx = idx * 2 + ((lane & off) ? 1 : 0);
   return idx;
+}
+
+// Programmatic dependent launch (Hopper+): a kernel launched with the PDL attribute may be
+// scheduled while its predecessor in the stream is still running.  Every kernel of the Arnoldi
+// fast path starts with pdl_sync(): it lets its own dependents launch early (all of its CTAs
+// are resident: the grids are at most one wave) and then waits until the predecessor grid has
+// completed and its memory is visible — the usual stream order, minus the launch gap.  Without
+// the attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_sync() {
+  asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;\n" ::: "memory");
+}
+
+// host side: launches on the Arnoldi fast path use the PDL attribute while this is set
+extern thread_local bool g_pdl;
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  if (!g_pdl) {
+    k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 }  // namespace emhd

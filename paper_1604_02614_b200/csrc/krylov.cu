@@ -17,6 +17,8 @@
 
 namespace emhd {
 
+thread_local bool g_pdl = false;
+
 constexpr int KT = 256;          // threads per CTA
 constexpr int EPT = 2;           // elements per double2
 constexpr int TILE = KT * EPT;   // 512 elements per combine tile
@@ -111,6 +113,7 @@ template <int VEC, int U>
 __global__ void __launch_bounds__(KT, 4) multidot_kernel(const double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, long long len_dot, int self,
     double* partials, double* out, unsigned int* ticket, const double* skip, const double* skip2) {
+  pdl_sync();
   if (skip && *skip != 0.0) return;            // cancelled look-ahead iteration (all CTAs agree)
   if (skip2 && *skip2 != 0.0) return;          // gated second-pass multi-dot not needed
   extern __shared__ double s_acc[];            // [(nvec+1)][NWARP]
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     long long len_upd, long long len_dot, long long len_max,
     double* partials, double* out, unsigned int* ticket, const FinishArgs fin,
     const HaloPush push = HaloPush{}, const double* skip = nullptr, const Reorth ro = Reorth{}) {
+  pdl_sync();
   if (skip && *skip != 0.0) return;            // cancelled look-ahead iteration (all CTAs agree)
   if (ro.skip2 && *ro.skip2 != 0.0) return;    // pass 2 not needed (decided by pass 1)
   // mode 0: the CGS2 re-projection dots, unless the previous iteration's decision predicts
@@ -365,6 +369,7 @@ __global__ void reorth_decide_kernel(const FinishArgs F, const double* r, int nv
 // out = {sum x^2 over len_sum, max|x| over len_max}
 __global__ void __launch_bounds__(KT) norms_kernel(const double* __restrict__ x, long long len_sum,
     long long len_max, double* partials, double* out, unsigned int* ticket) {
+  pdl_sync();
   __shared__ double s[2 * NWARP];
   __shared__ int kinds_s[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -450,6 +455,7 @@ __global__ void __launch_bounds__(KT) combine_kernel(const double* __restrict__ 
 // an epoch <= j.  Evaluated once, before the iteration's first kernel; the iteration's
 // kernels read *gate, so all of their CTAs agree.
 __global__ void gate_kernel(const unsigned long long* cancel, unsigned gen, int j, double* gate) {
+  pdl_sync();
   const unsigned long long c = *reinterpret_cast<const volatile unsigned long long*>(cancel);
   const bool hit = (unsigned)(c >> 32) == gen && (long long)(c & 0xffffffffull) <= (long long)j;
   *gate = hit ? 1.0 : 0.0;
@@ -463,8 +469,7 @@ __global__ void evals_discount_kernel(const double* evals, int count, DevStatus*
 }
 
 cudaError_t launch_gate(const unsigned long long* cancel, unsigned gen, int j, double* gate, cudaStream_t s) {
-  gate_kernel<<<1, 1, 0, s>>>(cancel, gen, j, gate);
-  return cudaGetLastError();
+  return launch_pdl(gate_kernel, dim3(1), dim3(1), 0, s, cancel, gen, j, gate);
 }
 
 cudaError_t launch_evals_discount(const double* evals, int count, DevStatus* st, cudaStream_t s) {
@@ -488,9 +493,8 @@ cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int
                             const double* skip2) {
   const int G = grid_for(len_dot, KT * 4, wk.num_sms);
   const size_t sm = sizeof(double) * (size_t)(nvec + 1) * NWARP;
-  multidot_kernel<2, 4><<<G, KT, sm, s>>>(w, V, ldv, nvec, len_dot, self, wk.partials, out, wk.ticket,
-                                          skip, skip2);
-  return cudaGetLastError();
+  return launch_pdl(multidot_kernel<2, 4>, dim3(G), dim3(KT), sm, s, w, V, ldv, nvec, len_dot, self,
+                    wk.partials, out, wk.ticket, skip, skip2);
 }
 
 cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, const double* h,
@@ -501,12 +505,10 @@ cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, c
   const int nval = mode == 0 ? nvec + 2 : 2;
   const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)nval * NWARP);
   if (mode == 0)
-    update_kernel<0, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip, ro);
-  else
-    update_kernel<1, 8><<<G, KT, sm, s>>>(w, V, ldv, nvec, h, len_upd, len_dot, len_max,
-                                           wk.partials, out, wk.ticket, fin, HaloPush{}, skip, ro);
-  return cudaGetLastError();
+    return launch_pdl(update_kernel<0, 8>, dim3(G), dim3(KT), sm, s, w, V, ldv, nvec, h, len_upd, len_dot,
+                      len_max, wk.partials, out, wk.ticket, fin, HaloPush{}, (const double*)skip, ro);
+  return launch_pdl(update_kernel<1, 8>, dim3(G), dim3(KT), sm, s, w, V, ldv, nvec, h, len_upd, len_dot,
+                    len_max, wk.partials, out, wk.ticket, fin, HaloPush{}, (const double*)skip, ro);
 }
 
 cudaError_t launch_update_push(double* w, const double* V, long long ldv, int nvec, const double* h,
@@ -526,8 +528,7 @@ cudaError_t launch_norms(const double* x, long long len_sum, long long len_max, 
   const long long len = len_sum > len_max ? len_sum : len_max;
   long long g = (len + KT - 1) / KT;
   const int G = (int)(g < 2LL * wk.num_sms ? (g < 1 ? 1 : g) : 2LL * wk.num_sms);
-  norms_kernel<<<G, KT, 0, s>>>(x, len_sum, len_max, wk.partials, out, wk.ticket);
-  return cudaGetLastError();
+  return launch_pdl(norms_kernel, dim3(G), dim3(KT), 0, s, x, len_sum, len_max, wk.partials, out, wk.ticket);
 }
 
 cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const double* nrm,

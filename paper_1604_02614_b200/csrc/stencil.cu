@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
   double* rawring = cring + 2 * NC * QW;            // [NARR*NF][QW] raw row in flight
   unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NARR * NF * QW);
 
+  pdl_sync();
   const int t = threadIdx.x;
   const int j0 = blockIdx.x * TY;
   const int i0 = blockIdx.y * P.rows_per_cta;
@@ -670,6 +671,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
   double* cq = q + NQ * TT_QN;                        // [NC][TT_QR][TT_QC]
   double* gxs = cq + NC * TT_QN;                      // [NF][TT_R + 2][TT_C]   rows -1 .. TR
   double* gys = gxs + NF * (TT_R + 2) * TT_C;         // [NF][TT_R][TT_C + 2]   cols -1 .. TC
+  pdl_sync();
   const int t = threadIdx.x;
   const int i0 = blockIdx.y * TT_R, j0 = blockIdx.x * TT_C;
   const bool lead = blockIdx.x == 0 && blockIdx.y == 0 && t == 0;
@@ -849,8 +851,7 @@ static cudaError_t launch_tile(const StencilParams& P, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   dim3 grid((P.ny + TT_C - 1) / TT_C, (P.nx + TT_R - 1) / TT_R);
-  k<<<grid, TT_THREADS, sm, s>>>(P);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, dim3(TT_THREADS), sm, s, P);
 }
 
 // ---- admissibility diagnostics (error path only) ---------------------------
@@ -1025,8 +1026,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
     if (rows < tile_rows) return launch_tile<MODE, AUG, FXY>(P, s);
   }
   dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
-  k<<<grid, TY, sm, s>>>(P);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, dim3(TY), sm, s, P);
 }
 
 template <int TY, int FXY>
