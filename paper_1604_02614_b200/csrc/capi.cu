@@ -711,15 +711,15 @@ struct emhd_arnoldi_args_s {
 // Iteration j of krylov.py:144-168 on one rank: (normalise w_{j-1} +) Jv, pass-1 multi-dot with
 // the breakdown scale, update + re-projection, update + norms + column bookkeeping.  Writes
 // w_{j} into w0/w1 (j even/odd) and V[j] (j > 0), H[:, j], scal, brk[j].
-// EMHD_PDL: 0 never, 1 always, unset = vectors of at most 2^21 doubles (measured: +15 % at
-// 256^2, -11 % at 1024^2 where early-resident dependent CTAs skew the one-wave stencil grid)
+// EMHD_PDL=0 disables programmatic dependent launch on the fast path (default on)
 static bool pdl_enabled(long long n) {
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("EMHD_PDL");
-    mode = e ? (atoi(e) != 0 ? 1 : 0) : 2;
+    mode = e ? (atoi(e) != 0 ? 1 : 0) : 1;
   }
-  return mode == 1 || (mode == 2 && n <= (1LL << 21));
+  (void)n;
+  return mode == 1;
 }
 
 // launches of one fast-path iteration use programmatic dependent launch (emhd_common.cuh)
