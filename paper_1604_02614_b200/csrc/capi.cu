@@ -711,28 +711,9 @@ struct emhd_arnoldi_args_s {
 // Iteration j of krylov.py:144-168 on one rank: (normalise w_{j-1} +) Jv, pass-1 multi-dot with
 // the breakdown scale, update + re-projection, update + norms + column bookkeeping.  Writes
 // w_{j} into w0/w1 (j even/odd) and V[j] (j > 0), H[:, j], scal, brk[j].
-// EMHD_PDL=0 disables programmatic dependent launch on the fast path (default on)
-static bool pdl_enabled(long long n) {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("EMHD_PDL");
-    mode = e ? (atoi(e) != 0 ? 1 : 0) : 1;
-  }
-  (void)n;
-  return mode == 1;
-}
-
-// launches of one fast-path iteration use programmatic dependent launch (emhd_common.cuh)
-struct PdlScope {
-  bool prev;
-  explicit PdlScope(long long n) : prev(g_pdl) { g_pdl = pdl_enabled(n); }
-  ~PdlScope() { g_pdl = prev; }
-};
-
 static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   if (!c || !args || j < 0) return EMHD_ERR_ARG;
   const emhd_arnoldi_args_s* A = (const emhd_arnoldi_args_s*)args;
-  PdlScope pdl_scope(A->n_top);
   if (j + 1 > c->max_vectors || (gated && !A->gate)) return EMHD_ERR_ARG;
   c->epoch = j;
   double* out = (j % 2 == 0) ? A->w0 : A->w1;

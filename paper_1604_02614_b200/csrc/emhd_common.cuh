@@ -126,13 +126,14 @@ __device__ __forceinline__ void pdl_sync() {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
-// host side: launches on the Arnoldi fast path use the PDL attribute while this is set
-extern thread_local bool g_pdl;
+// host side: kernels that begin with pdl_sync() are launched with the PDL attribute (always
+// safe: they wait for their predecessor whatever it is); EMHD_PDL=0 turns it off
+bool pdl_on();
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
-  if (!g_pdl) {
+  if (!pdl_on()) {
     k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
     return cudaGetLastError();
   }

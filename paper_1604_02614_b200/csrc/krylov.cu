@@ -12,12 +12,20 @@
 // Reductions are deterministic: every CTA reduces its own elements in a fixed
 // order into a per-CTA partial, and the last CTA to finish (threadfence +
 // ticket) sums the partials in CTA order.  No floating-point atomics.
+#include <cstdlib>
 #include "emhd_common.cuh"
 #include "krylov.cuh"
 
 namespace emhd {
 
-thread_local bool g_pdl = false;
+bool pdl_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("EMHD_PDL");
+    on = e ? (atoi(e) != 0 ? 1 : 0) : 1;
+  }
+  return on != 0;
+}
 
 constexpr int KT = 256;          // threads per CTA
 constexpr int EPT = 2;           // elements per double2
