@@ -418,6 +418,7 @@ __global__ void arnoldi_finish_kernel(const double* h1, const double* h2, const 
 // out[s] = base[s] (+) coef[s] * sum_i Y[s*m + i] V_i   (S <= 4 outputs, one sweep over V)
 __global__ void __launch_bounds__(KT) combine_kernel(const double* __restrict__ V, long long ldv, int m,
     const double* __restrict__ Y, int S, const CombineOut co, long long len) {
+  pdl_sync();
   extern __shared__ double s_y[];               // [S][m]
   for (int k = threadIdx.x; k < S * m; k += KT) s_y[k] = Y[k];
   __syncthreads();
@@ -559,8 +560,7 @@ cudaError_t launch_combine(const double* V, long long ldv, int m, const double* 
   long long g = (len + TILE - 1) / TILE;
   const int G = (int)(g < 4LL * num_sms ? (g < 1 ? 1 : g) : 4LL * num_sms);
   const size_t sm = sizeof(double) * (size_t)S * m;
-  combine_kernel<<<G, KT, sm, s>>>(V, ldv, m, Y, S, co, len);
-  return cudaGetLastError();
+  return launch_pdl(combine_kernel, dim3(G), dim3(KT), sm, s, V, ldv, m, Y, S, co, len);
 }
 
 }  // namespace emhd

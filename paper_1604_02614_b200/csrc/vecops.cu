@@ -41,6 +41,7 @@ __device__ bool finish2(const double* partials, int G, double* out, unsigned int
 __global__ void __launch_bounds__(VT) lincomb_kernel(const LinComb L, long long n, long long len_max,
                                                      double* partials, double* red_out,
                                                      unsigned int* ticket) {
+  pdl_sync();
   __shared__ double s[2 * VW];
   double mx = 0.0;
   for (long long e = (long long)blockIdx.x * VT + threadIdx.x; e < n; e += (long long)gridDim.x * VT) {
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(VT) lincomb_kernel(const LinComb L, long long 
 
 // out[1] = max|x| over len (separate final kernel keeps lincomb simple)
 __global__ void __launch_bounds__(VT) lincomb_max_finish(const double* partials, int G, double* out) {
+  pdl_sync();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x < 32) {
     double acc = 0.0;
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(VT) wrms_kernel(const double* err, const doubl
 // v / d with d a device scalar (sqrt of d2 when take_sqrt): exact IEEE division
 __global__ void __launch_bounds__(VT) div_scalar_kernel(const double* x, const double* d2, int take_sqrt,
                                                         double* out, double* d_out, long long n) {
+  pdl_sync();
   const double d = take_sqrt ? sqrt(d2[0]) : d2[0];
   const double r = 1.0 / d;
   for (long long e = (long long)blockIdx.x * VT + threadIdx.x; e < n; e += (long long)gridDim.x * VT)
@@ -126,11 +129,10 @@ static int vgrid(long long n, int num_sms) {
 cudaError_t launch_lincomb(const LinComb& L, long long n, long long len_max, double* partials,
                            double* max_out, unsigned int* ticket, int num_sms, cudaStream_t s) {
   const int G = vgrid(n, num_sms);
-  lincomb_kernel<<<G, VT, 0, s>>>(L, n, len_max, partials, max_out, ticket);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(lincomb_kernel, dim3(G), dim3(VT), 0, s, L, n, len_max, partials, max_out,
+                             ticket);
   if (e != cudaSuccess || !max_out) return e;
-  lincomb_max_finish<<<1, 32, 0, s>>>(partials, G, max_out);
-  return cudaGetLastError();
+  return launch_pdl(lincomb_max_finish, dim3(1), dim3(32), 0, s, (const double*)partials, G, max_out);
 }
 
 cudaError_t launch_wrms(const double* err, const double* y, double tol, long long n, double* partials,
@@ -141,8 +143,7 @@ cudaError_t launch_wrms(const double* err, const double* y, double tol, long lon
 
 cudaError_t launch_div_scalar(const double* x, const double* d2, int take_sqrt, double* out, double* d_out,
                               long long n, int num_sms, cudaStream_t s) {
-  div_scalar_kernel<<<vgrid(n, num_sms), VT, 0, s>>>(x, d2, take_sqrt, out, d_out, n);
-  return cudaGetLastError();
+  return launch_pdl(div_scalar_kernel, dim3(vgrid(n, num_sms)), dim3(VT), 0, s, x, d2, take_sqrt, out, d_out, n);
 }
 
 }  // namespace emhd
