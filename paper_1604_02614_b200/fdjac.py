@@ -106,7 +106,13 @@ class FdJacobianOperator(LinearOperator):
         self.a_halo = self.gpu.halo(self.a) if self.gpu is not None else None
         self.ctx = self.gpu.ctx if self.gpu is not None else (ctx or _generic_ctx())
         self._scr = D.Scratch(4)
-        super().__init__(self.a.numel(), self._apply)
+        # no bound method stored on self (the reference passes self._apply as the matvec):
+        # that would be a reference cycle, and the operator's a / F(a) (2 W of HBM per step)
+        # would then live until the garbage collector happens to run
+        super().__init__(self.a.numel(), None)
+
+    def __call__(self, v):
+        return self._apply(v)
 
     # raw device apply (no status check); vnorm_dev: device scalar ||v||_inf or None
     def apply_device(self, v, out=None, vnorm_dev=None, v_halo=None):

@@ -366,6 +366,32 @@ def test_config0_epirk4_trajectory_20_steps(P):
         assert getattr(S, k) == v, k
 
 
+def test_steps_leave_no_cyclic_device_garbage(P):
+    """Every per-step device vector is freed by reference counting, not by a later gc pass:
+    at 4096^2 each leaked FD operator holds 2 GiB (a, F(a)), and ten EpiRK4 steps of leaked
+    operators next to a 129 GiB basis exhausted the GPU (config 4)."""
+    import gc
+    z = golden("config0_recon64.npz")
+    g = P.ReconnectionSpec().grid(64, 64)
+    f = P.make_rhs(P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3), g, P.default_bc("reconnection"))
+    y0 = torch.from_numpy(z["U0"].reshape(-1)).cuda()
+    gc.collect()
+    gc.disable()
+    try:
+        y, _ = P.integrate_fixed("epirk4", f, y0, 0.0, 0.3, 0.1, tol_krylov=1e-10)
+        P.epirk5p1_step(f, y, 0.05, 1e-8)
+        del y
+        gc.set_debug(gc.DEBUG_SAVEALL)
+        gc.collect()
+        leaked = [type(o).__qualname__ for o in gc.garbage
+                  if (isinstance(o, torch.Tensor) and o.is_cuda) or type(o).__name__ == "FdJacobianOperator"]
+    finally:
+        gc.set_debug(0)
+        gc.garbage.clear()
+        gc.enable()
+    assert leaked == [], leaked
+
+
 def test_epirk5p1_adaptive_kh32(P):
     z = golden("epirk5p1_kh32.npz")
     with open(os.path.join(GOLDEN, "epirk5p1_kh32.json")) as fh:
