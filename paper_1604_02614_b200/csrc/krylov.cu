@@ -251,7 +251,10 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double ss = 0.0, mx = 0.0;
   const long long ntiles = (len_upd + TL - 1) / TL;
-  for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+  for (long long k = blockIdx.x; k < ntiles; k += gridDim.x) {
+    // last tile first: the multi-dot just streamed the vectors front to back, so their tail
+    // is what the L2 still holds
+    const long long tl = ntiles - 1 - k;
     const long long e = tl * TL + 2LL * threadIdx.x;
     const bool full = e + 1 < len_upd;
     double2 wv = ld2(w, e, len_upd);
