@@ -234,6 +234,10 @@ int emhd_arnoldi_cancel(emhd_ctx* ctx, int gen, int epoch_min);
  * iterations (evals written per iteration by emhd_arnoldi_iter when args.evals is set) */
 int emhd_evals_discount(emhd_ctx* ctx, const double* evals, int count);
 
+/* Persisting-L2 window over [base, base + bytes) on the context's stream (bytes = 0: none);
+ * B200-specific residency control for small Krylov bases, no reference counterpart. */
+int emhd_l2_window(emhd_ctx* ctx, const void* base, long long bytes);
+
 /* ---- per-launch profiling (benchmarks) ------------------------------ */
 enum { EMHD_K_JV = 0, EMHD_K_JV_NORMALIZED = 1, EMHD_K_MULTIDOT = 2, EMHD_K_UPDATE = 3,
        EMHD_K_MULTIDOT2 = 4, EMHD_K_UPDATE_FINISH = 5, EMHD_K_NORMS = 6, EMHD_K_DIV_SCALAR = 7,

@@ -90,6 +90,7 @@ _SIGS = {
     "emhd_slot_norms": (c_int, [c_vp, P, c_int, c_int, P]),
     "emhd_reorth_decide": (c_int, [c_vp, P, P, c_int, P, c_int, P, c_ll, P, P, c_dbl, P]),
     "emhd_skip_next": (c_int, [c_vp, P]),
+    "emhd_l2_window": (c_int, [c_vp, P, c_ll]),
     "emhd_profile": (c_int, [c_vp, c_int]),
     "emhd_profile_read": (c_int, [c_vp, c_int, IP, DP, DP]),
     "emhd_push_edges": (c_int, [c_vp, P, P, P, P]),

@@ -173,6 +173,34 @@ extern "C" int emhd_set_stream(emhd_ctx* c, void* s) {
 
 extern "C" int emhd_num_sms(emhd_ctx* c) { return c ? c->num_sms : 0; }
 
+// Persisting-L2 access window on the context's stream over [base, base + bytes): the head of
+// a Krylov basis that fits the L2 stays resident across iterations (its lines are kept while
+// the streaming vectors evict each other).  bytes = 0 removes the window and releases the
+// persisting lines.  Clamped to the device's window and persisting-L2 limits.
+extern "C" int emhd_l2_window(emhd_ctx* c, const void* base, long long bytes) {
+  if (!c || bytes < 0) return EMHD_ERR_ARG;
+  int maxwin = 0, maxpers = 0;
+  int rc = cerr(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
+  if (!rc) rc = cerr(cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, c->device));
+  if (rc) return rc;
+  if (bytes > maxwin) bytes = maxwin;
+  cudaStreamAttrValue v{};
+  if (bytes > 0 && maxpers > 0) {
+    rc = cerr(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)(bytes < maxpers ? bytes : maxpers)));
+    if (rc) return rc;
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = (size_t)bytes;
+    v.accessPolicyWindow.hitRatio = bytes <= maxpers ? 1.0f : (float)maxpers / (float)bytes;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  } else {
+    v.accessPolicyWindow.num_bytes = 0;
+  }
+  rc = cerr(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+  if (!rc && bytes == 0) rc = cerr(cudaCtxResetPersistingL2Cache());
+  return rc;
+}
+
 extern "C" int emhd_set_epoch(emhd_ctx* c, int epoch) {
   if (!c) return EMHD_ERR_ARG;
   c->epoch = epoch;

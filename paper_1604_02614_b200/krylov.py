@@ -57,6 +57,8 @@ REORTH_ETA = float(os.environ.get("EMHD_REORTH_ETA", "0.5"))
 PREDICT_REPROJECTION = os.environ.get("EMHD_PREDICT_REPROJ", "1") != "0"
 # reporting: count kept iterations / second passes per context (tools/run_configs.py)
 COUNT_PASSES = False
+# persisting-L2 window over the head of the basis (see _l2_window); env override in MiB
+L2_WINDOW_MB = os.environ.get("EMHD_L2_WINDOW_MB")
 
 
 class KrylovConvergenceError(RuntimeError):
@@ -140,6 +142,26 @@ class PhiCombRequest:
 
 def _ld(n):
     return (n + 31) // 32 * 32
+
+
+def _l2_window(ctx, h, V, vec_bytes):
+    """Keep the first 40 MiB of the basis in L2 across iterations (persisting access window on
+    the launching stream): every multi-dot and update pass re-reads it, and the vectors that
+    stream through evict each other instead of it.  Measured on the config-2 workload: 512²
+    +3.8 %, 1024² +1.6 %, 2048² +0.3 %; at 256² (-1 to -2 %) the whole working set competes
+    for L2 and at 2048² with 64 MiB the stencil loses more than the passes gain, so it is on
+    for 16 MiB <= W <= 256 MiB only.  Set once per (stream, basis buffer)."""
+    if L2_WINDOW_MB is not None:
+        want = int(float(L2_WINDOW_MB) * 2 ** 20)
+    else:
+        want = 40 * 2 ** 20 if 16 * 2 ** 20 <= vec_bytes <= 256 * 2 ** 20 else 0
+    want = min(want, V.numel() * 8)
+    key = (ctx._stream, D.ptr(V), want)
+    prev = getattr(ctx, "_l2win", None)
+    if prev == key or (want == 0 and (prev is None or prev[0] != ctx._stream)):
+        return
+    N.check(ctx.lib.emhd_l2_window(h, D.ptr(V), want), "l2_window")
+    ctx._l2win = key
 
 
 def _persistent_basis(ctx, rows, ld):
@@ -263,6 +285,7 @@ class _Process:
         # beta = ||seed||_2, V[0] = seed / beta  (krylov.py:132-137)
         sd = seed.reshape(-1)
         h = self.ctx.sync_stream()
+        _l2_window(self.ctx, h, self.V, self.ld * 8)
         N.check(self.lib.emhd_norms(h, D.ptr(sd), self.len_dot, n_top, D.ptr(self.nb)), "norms")
         self._allreduce_norms(self.nb)
         b2 = float(self.nb[0].item())
