@@ -678,6 +678,35 @@ def test_arnoldi_reorthogonalize_false_is_one_pass(P):
     assert np.linalg.norm(bf.H - zz["H"]) <= 1e-8 * np.linalg.norm(zz["H"])
 
 
+def test_l2_window_changes_no_bits(P):
+    """The persisting-L2 window over the basis head (on by default for 16-256 MiB vectors) is
+    a cache policy only: the 512^2 FD Arnoldi factorisation is bit-identical with the window
+    off, on by default, and over the whole basis."""
+    from paper_1604_02614_b200 import krylov
+    from paper_1604_02614_b200.problems import fourier_grid, fourier_state, unit_start_vector
+    g = fourier_grid(512)
+    prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    U, rng = fourier_state(g, prm, seed=5)
+    v = dev(unit_start_vector(rng, U.size))
+    f = P.make_rhs(prm, g, P.BoundaryPolicy("periodic", "periodic"))
+    op = P.FdJacobianOperator(f, dev(U.reshape(-1)))
+    saved = krylov.L2_WINDOW_MB
+    out = []
+    try:
+        for mb in ("0", None, "4096"):
+            krylov.L2_WINDOW_MB = mb
+            b = P.arnoldi(op, v, 12)
+            tonp = lambda x: x.cpu().numpy().copy() if torch.is_tensor(x) else np.array(x)
+            out.append((tonp(b.H), tonp(b.V)))      # V may view the reused basis buffer
+    finally:
+        krylov.L2_WINDOW_MB = saved
+    h = f.ctx.sync_stream()
+    assert f.ctx.lib.emhd_l2_window(h, None, 0) == 0
+    f.ctx._l2win = None
+    for H, V in out[1:]:
+        assert np.array_equal(H, out[0][0]) and np.array_equal(V, out[0][1])
+
+
 @pytest.mark.parametrize("look", [None, 4])
 def test_adaptive_recoverable_rejections_match_oracle(P, look):
     """EpiRK5P1 on a near-vacuum reconnection state with an oversized first step: trial steps
