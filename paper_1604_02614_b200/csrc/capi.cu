@@ -33,6 +33,7 @@ struct emhd_ctx {
   unsigned long long* cancel = nullptr;       // look-ahead cancel word {generation, epoch}
   unsigned long long* cancel_host = nullptr;  // pinned source of its async updates
   const double* skip_next = nullptr;          // emhd_skip_next: gate of the next pass-2 launch
+  bool l2win = false;                         // emhd_l2_window set on this context's stream
   // per-launch profiling (emhd_profile): CUDA events around every launch of the Arnoldi path
   struct ProfRec { int kind; cudaEvent_t e0, e1; double bytes; const double* gate[2]; };
   bool prof = false;
@@ -197,6 +198,7 @@ extern "C" int emhd_l2_window(emhd_ctx* c, const void* base, long long bytes) {
     v.accessPolicyWindow.num_bytes = 0;
   }
   rc = cerr(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+  if (!rc) c->l2win = v.accessPolicyWindow.num_bytes > 0;
   if (!rc && bytes == 0) rc = cerr(cudaCtxResetPersistingL2Cache());
   return rc;
 }
@@ -310,6 +312,7 @@ static KWork kwork(emhd_ctx* c) {
   w.partials = c->partials;
   w.ticket = c->ticket;
   w.num_sms = c->num_sms;
+  w.stream_basis = c->l2win;
   return w;
 }
 

@@ -228,7 +228,7 @@ __device__ __forceinline__ void push_edge(const HaloPush& H, long long e, double
   if (H.hi && row + 2 >= H.nx) H.hi[((size_t)f * 2 + (row + 2 - H.nx)) * H.ny + col] = val;
 }
 
-template <int MODE, int U, bool PUSH = false>
+template <int MODE, int U, bool PUSH = false, bool CS = false>
 __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     const double* __restrict__ V, long long ldv, int nvec, const double* __restrict__ h,
     long long len_upd, long long len_dot, long long len_max,
@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
       double2 x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        x[u] = (i + u < nvec) ? ld2(V + (size_t)(i + u) * ldv, e, len_upd) : make_double2(0.0, 0.0);
+        x[u] = (i + u < nvec) ? (CS ? ld2_stream(V + (size_t)(i + u) * ldv, e, len_upd)
+                                    : ld2(V + (size_t)(i + u) * ldv, e, len_upd))
+                              : make_double2(0.0, 0.0);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (i + u < nvec) {
@@ -516,10 +518,11 @@ cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, c
   const int G = grid_for(len_upd, KT * 2, wk.num_sms);
   const int nval = mode == 0 ? nvec + 2 : 2;
   const size_t sm = sizeof(double) * ((size_t)((nvec + 1) & ~1) + (size_t)nval * NWARP);
-  if (mode == 0)
-    return launch_pdl(update_kernel<0, 8>, dim3(G), dim3(KT), sm, s, w, V, ldv, nvec, h, len_upd, len_dot,
-                      len_max, wk.partials, out, wk.ticket, fin, HaloPush{}, (const double*)skip, ro);
-  return launch_pdl(update_kernel<1, 8>, dim3(G), dim3(KT), sm, s, w, V, ldv, nvec, h, len_upd, len_dot,
+  // with a persisting L2 window over the basis head, the rest of V is read evict-first so the
+  // lines of w written here survive for the next stencil (512^2 +2 %, 1024^2 +0.9 %)
+  auto k = mode == 0 ? (wk.stream_basis ? update_kernel<0, 8, false, true> : update_kernel<0, 8>)
+                     : (wk.stream_basis ? update_kernel<1, 8, false, true> : update_kernel<1, 8>);
+  return launch_pdl(k, dim3(G), dim3(KT), sm, s, w, V, ldv, nvec, h, len_upd, len_dot,
                     len_max, wk.partials, out, wk.ticket, fin, HaloPush{}, (const double*)skip, ro);
 }
 

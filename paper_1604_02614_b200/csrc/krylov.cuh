@@ -8,6 +8,7 @@ struct KWork {
   double* partials;          // >= (m_cap + 3) * 2 * num_sms doubles
   unsigned int* ticket;      // zero-initialised, re-armed by each reduction
   int num_sms;
+  bool stream_basis = false; // update passes read V evict-first (a persisting L2 window holds its head)
 };
 
 struct FinishArgs {         // optional Arnoldi column bookkeeping fused into update mode 1
