@@ -187,7 +187,10 @@ extern "C" int emhd_l2_window(emhd_ctx* c, const void* base, long long bytes) {
   if (bytes > maxwin) bytes = maxwin;
   cudaStreamAttrValue v{};
   if (bytes > 0 && maxpers > 0) {
-    rc = cerr(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)(bytes < maxpers ? bytes : maxpers)));
+    const size_t lim = (size_t)(bytes < maxpers ? bytes : maxpers);
+    size_t cur = 0;
+    rc = cerr(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    if (!rc && cur != lim) rc = cerr(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
     if (rc) return rc;
     v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
     v.accessPolicyWindow.num_bytes = (size_t)bytes;
