@@ -167,7 +167,7 @@ __device__ void axpby_mat(double* out, const double* const* terms, const double*
 // Gauss–Jordan with partial pivoting on M = [Q | R] (n x 2n): R <- Q^{-1} R.
 // The pivot row is staged (scaled) in shared memory, rows are distributed over warps and
 // columns over lanes: no integer division in the elimination, one broadcast read per column.
-__device__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac, double* prow) {
+__device__ __noinline__ bool gj_solve(double* M, int n, double* red, int* ired, double* fac, double* prow) {
   const int w2 = 2 * n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NWD = DT / 32;
