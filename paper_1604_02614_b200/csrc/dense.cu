@@ -185,16 +185,12 @@ __device__ __noinline__ bool gj_solve(double* M, int n, double* red, int* ired, 
     }
     if (lane == 0) { red[warp] = best; ired[warp] = bi; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = -1.0; int ii = n;
-      for (int w = 0; w < NWD; ++w)
-        if (red[w] > b || (red[w] == b && ired[w] < ii)) { b = red[w]; ii = ired[w]; }
-      ired[NWD] = ii;
-      red[NWD] = b;
-    }
-    __syncthreads();
-    const int piv = ired[NWD];
-    if (!(red[NWD] > 0.0)) return false;
+    // every thread combines the warp results itself (same order, same answer), so no second
+    // barrier; red/ired are rewritten only after this step's two later barriers
+    double bb = -1.0; int piv = n;
+    for (int w = 0; w < NWD; ++w)
+      if (red[w] > bb || (red[w] == bb && ired[w] < piv)) { bb = red[w]; piv = ired[w]; }
+    if (!(bb > 0.0)) return false;
     const double d = M[piv * w2 + k];
     // stage the scaled pivot row (columns > k) and swap rows k <-> piv
     for (int c = k + 1 + threadIdx.x; c < w2; c += DT) {
