@@ -93,6 +93,29 @@ int emhd_status_reset(emhd_ctx* ctx);
  * speculative Arnoldi iterations; no reference counterpart — they never run there) */
 int emhd_status_scrub(emhd_ctx* ctx, int epoch_min);
 
+/* ---- stencil launch selection (per context) ------------------------- */
+/* Which kernel variant evaluates the fused RHS / Jv stencil.  All variants issue the same
+ * operations in the same order (bit-identical outputs); the selection only moves performance.
+ * Defaults come from the environment at context creation (EMHD_STENCIL_TY, EMHD_STENCIL_TMA,
+ * EMHD_MIN_ROWS, EMHD_STENCIL_TILE_ROWS).  No reference counterpart (tuning / test hook). */
+#define EMHD_STENCIL_AUTO 0      /* marching strips, 2D tiles when a strip CTA gets < tile_rows rows */
+#define EMHD_STENCIL_MARCHING 1  /* row-marching strips of `strip` columns, rows_per_cta rows each */
+#define EMHD_STENCIL_TILE 2      /* 8 x 32 output tiles, three barrier-separated phases */
+typedef struct emhd_stencil_path {
+  int kernel;        /* EMHD_STENCIL_* */
+  int rows_per_cta;  /* marching: rows per CTA; 0 = one wave of resident CTAs (>= min_rows) */
+  int strip;         /* marching: 32 / 64 / 128 columns per CTA; 0 = by ny */
+  int bulk;          /* marching: interior strips stage rows with bulk async copies (TMA engine)
+                        when 16-byte aligned; 0 = per-thread cp.async everywhere */
+  int min_rows;      /* >= 1 */
+  int tile_rows;
+} emhd_stencil_path;
+int emhd_set_stencil_path(emhd_ctx* ctx, const emhd_stencil_path* sel);
+int emhd_get_stencil_path(emhd_ctx* ctx, emhd_stencil_path* out);
+/* what the last stencil launch on ctx ran: kernel (1 marching / 2 tile), rows_per_cta and strip
+ * of a marching launch, bulk = 1 when some interior strip staged its rows by bulk copies */
+int emhd_last_stencil(emhd_ctx* ctx, emhd_stencil_path* out);
+
 /* ---- (a) right-hand side ------------------------------------------- */
 /* F = rhs(u)   — replaces make_rhs(...)(y) / rhs(U, params, grid, bc)  mhd.py:269-285 */
 int emhd_rhs(emhd_ctx* ctx, const double* u, const double* u_halo, double* F);

@@ -43,6 +43,14 @@ class ArnoldiArgs(ctypes.Structure):
                 ("md2", P)]
 
 
+class StencilPath(ctypes.Structure):
+    _fields_ = [("kernel", c_int), ("rows_per_cta", c_int), ("strip", c_int), ("bulk", c_int),
+                ("min_rows", c_int), ("tile_rows", c_int)]
+
+
+STENCIL_AUTO, STENCIL_MARCHING, STENCIL_TILE = 0, 1, 2
+
+
 class Report(ctypes.Structure):
     _fields_ = [("which", c_int), ("i", c_int), ("j", c_int), ("pad", c_int), ("value", c_dbl)]
 
@@ -61,6 +69,9 @@ _SIGS = {
     "emhd_status_read": (c_int, [c_vp, ctypes.POINTER(Status)]),
     "emhd_status_reset": (c_int, [c_vp]),
     "emhd_status_scrub": (c_int, [c_vp, c_int]),
+    "emhd_set_stencil_path": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
+    "emhd_get_stencil_path": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
+    "emhd_last_stencil": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
     "emhd_rhs": (c_int, [c_vp, P, P, P]),
     "emhd_jv": (c_int, [c_vp, P, P, P, P, P, P, P]),
     "emhd_jv_aug": (c_int, [c_vp, P, P, P, P, P, P, P, c_int, c_dbl, c_int, PP, IP, P]),

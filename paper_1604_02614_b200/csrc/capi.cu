@@ -34,6 +34,8 @@ struct emhd_ctx {
   unsigned long long* cancel_host = nullptr;  // pinned source of its async updates
   const double* skip_next = nullptr;          // emhd_skip_next: gate of the next pass-2 launch
   bool l2win = false;                         // emhd_l2_window set on this context's stream
+  StencilPath path{};                         // stencil launch selection (emhd_set_stencil_path)
+  StencilPath last{};                         // what the last stencil launch ran
   // per-launch profiling (emhd_profile): CUDA events around every launch of the Arnoldi path
   struct ProfRec { int kind; cudaEvent_t e0, e1; double bytes; const double* gate[2]; };
   bool prof = false;
@@ -146,6 +148,7 @@ extern "C" int emhd_ctx_create(emhd_ctx** out, const emhd_geometry* g, const emh
   if (!rc) rc = cerr(cudaMemset(c->cancel, 0xff, sizeof(unsigned long long)));   // matches nothing
   if (rc) { emhd_ctx_destroy(c); return rc; }
   fill_base(c);
+  c->path = stencil_path_defaults();
   emhd_status_reset(c);
   rc = cerr(cudaStreamSynchronize(0));
   *out = c;
@@ -204,6 +207,32 @@ extern "C" int emhd_l2_window(emhd_ctx* c, const void* base, long long bytes) {
   if (!rc) c->l2win = v.accessPolicyWindow.num_bytes > 0;
   if (!rc && bytes == 0) rc = cerr(cudaCtxResetPersistingL2Cache());
   return rc;
+}
+
+static void to_c(const StencilPath& a, emhd_stencil_path* b) {
+  b->kernel = a.kernel; b->rows_per_cta = a.rows_per_cta; b->strip = a.strip; b->bulk = a.bulk;
+  b->min_rows = a.min_rows; b->tile_rows = a.tile_rows;
+}
+
+extern "C" int emhd_set_stencil_path(emhd_ctx* c, const emhd_stencil_path* sel) {
+  if (!c || !sel || sel->kernel < 0 || sel->kernel > 2 || sel->rows_per_cta < 0 || sel->min_rows < 1 ||
+      (sel->strip != 0 && sel->strip != 32 && sel->strip != 64 && sel->strip != 128))
+    return EMHD_ERR_ARG;
+  c->path.kernel = sel->kernel; c->path.rows_per_cta = sel->rows_per_cta; c->path.strip = sel->strip;
+  c->path.bulk = sel->bulk != 0; c->path.min_rows = sel->min_rows; c->path.tile_rows = sel->tile_rows;
+  return EMHD_OK;
+}
+
+extern "C" int emhd_get_stencil_path(emhd_ctx* c, emhd_stencil_path* out) {
+  if (!c || !out) return EMHD_ERR_ARG;
+  to_c(c->path, out);
+  return EMHD_OK;
+}
+
+extern "C" int emhd_last_stencil(emhd_ctx* c, emhd_stencil_path* out) {
+  if (!c || !out) return EMHD_ERR_ARG;
+  to_c(c->last, out);
+  return EMHD_OK;
 }
 
 extern "C" int emhd_set_epoch(emhd_ctx* c, int epoch) {
@@ -268,7 +297,7 @@ extern "C" int emhd_rhs(emhd_ctx* c, const double* u, const double* u_halo, doub
   StencilParams P = c->base;
   P.epoch = c->epoch;
   P.a = u; P.a_halo = u_halo; P.out = F;
-  return cerr(launch_stencil(P, MODE_RHS, false, c->num_sms, c->stream));
+  return cerr(launch_stencil(P, MODE_RHS, false, c->num_sms, c->stream, c->path, &c->last));
 }
 
 extern "C" int emhd_jv(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
@@ -278,7 +307,7 @@ extern "C" int emhd_jv(emhd_ctx* c, const double* a, const double* a_halo, const
   P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = v; P.v_halo = v_halo; P.scal = d_vnorm; P.out = out;
   ProfScope ps(c, EMHD_K_JV, 4.0 * 64.0 * (double)c->g.nx * c->g.ny);   // 4W
-  return cerr(launch_stencil(P, MODE_JV, false, c->num_sms, c->stream));
+  return cerr(launch_stencil(P, MODE_JV, false, c->num_sms, c->stream, c->path, &c->last));
 }
 
 extern "C" int emhd_jv_aug(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
@@ -292,7 +321,7 @@ extern "C" int emhd_jv_aug(emhd_ctx* c, const double* a, const double* a_halo, c
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = u; P.v_halo = u_halo; P.scal = d_vnorm; P.out = out;
   P.qsrc = d_q;
   set_epilogue(P, p, ch, nb, bcol, bidx);
-  return cerr(launch_stencil(P, MODE_JV, true, c->num_sms, c->stream));
+  return cerr(launch_stencil(P, MODE_JV, true, c->num_sms, c->stream, c->path, &c->last));
 }
 
 extern "C" int emhd_jv_normalized(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
@@ -307,7 +336,7 @@ extern "C" int emhd_jv_normalized(emhd_ctx* c, const double* a, const double* a_
   P.out = out; P.vout = v_out;
   set_epilogue(P, p, ch, nb, bcol, bidx);
   ProfScope ps(c, EMHD_K_JV_NORMALIZED, 5.0 * 64.0 * (double)c->g.nx * c->g.ny);   // 5W
-  return cerr(launch_stencil(P, MODE_JVN, p > 0, c->num_sms, c->stream));
+  return cerr(launch_stencil(P, MODE_JVN, p > 0, c->num_sms, c->stream, c->path, &c->last));
 }
 
 static KWork kwork(emhd_ctx* c) {
@@ -778,13 +807,13 @@ static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
     P.v = A->V; P.scal = A->vn + 1;
     if (A->p > 0) P.qsrc = A->V + A->n_top;
     ProfScope ps(c, EMHD_K_JV, 4.0 * W);
-    rc = cerr(launch_stencil(P, MODE_JV, A->p > 0, c->num_sms, c->stream));
+    rc = cerr(launch_stencil(P, MODE_JV, A->p > 0, c->num_sms, c->stream, c->path, &c->last));
   } else {
     P.v = (j % 2 == 0) ? A->w1 : A->w0;
     P.scal = A->scal;
     P.vout = A->V + (size_t)j * A->ldv;
     ProfScope ps(c, EMHD_K_JV_NORMALIZED, 5.0 * W, skip);
-    rc = cerr(launch_stencil(P, MODE_JVN, A->p > 0, c->num_sms, c->stream));
+    rc = cerr(launch_stencil(P, MODE_JVN, A->p > 0, c->num_sms, c->stream, c->path, &c->last));
   }
   if (rc) return rc;
   const int nv = j + 1;

@@ -980,7 +980,8 @@ cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* 
 }
 
 template <int TY, int MODE, bool AUG, int FXY>
-static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
+static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const StencilPath& sel,
+                            StencilPath* used) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
   const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NARR * NF * QW) +
@@ -989,19 +990,19 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
   if ((long long)NF * P.nx * P.ny >= (1LL << 32)) return cudaErrorInvalidValue;   // 32-bit offsets
   {
     // bulk copies need 16-byte aligned sources and sizes: even ny and aligned buffers
-    static int use_tma = -1;
-    if (use_tma < 0) {
-      const char* env = getenv("EMHD_STENCIL_TMA");
-      use_tma = env ? atoi(env) != 0 : 1;
-    }
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    P.tma = use_tma && (P.ny % 2 == 0) && al(P.a) && al(P.a_halo) &&
+    P.tma = sel.bulk && (P.ny % 2 == 0) && al(P.a) && al(P.a_halo) &&
             (MODE == MODE_RHS || (al(P.v) && al(P.v_halo)));
+  }
+  if (sel.kernel == 2) {
+    if (used) { *used = sel; used->kernel = 2; used->rows_per_cta = 0; used->strip = 0; used->bulk = 0; }
+    return launch_tile<MODE, AUG, FXY>(P, s);
   }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
+  P.rows_per_cta = sel.rows_per_cta;
   if (P.rows_per_cta <= 0) {
-    // exactly one wave of resident CTAs (all CTAs carry equal work); >= 8 rows per CTA
+    // exactly one wave of resident CTAs (all CTAs carry equal work)
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, TY, sm);
     const int strips = (P.ny + TY - 1) / TY;
@@ -1009,60 +1010,78 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s) {
     // floor: strips x chunks must not exceed one wave of resident CTAs
     const int chunks = target / strips > 0 ? target / strips : 1;
     const int rows = (P.nx + chunks - 1) / chunks;
-    static int min_rows = -1;
-    if (min_rows < 0) {
-      const char* env = getenv("EMHD_MIN_ROWS");
-      min_rows = env ? atoi(env) : 2;
-      if (min_rows < 1) min_rows = 1;
-    }
+    const int min_rows = sel.min_rows < 1 ? 1 : sel.min_rows;
     P.rows_per_cta = rows < min_rows ? min_rows : rows;
     // few rows per CTA: the marching kernel's dependent row steps dominate; the 2D-tile
     // kernel (three barrier-separated phases, bit-identical outputs) is faster there
-    static int tile_rows = -1;
-    if (tile_rows < 0) {
-      const char* env = getenv("EMHD_STENCIL_TILE_ROWS");
-      tile_rows = env ? atoi(env) : 6;
+    if (sel.kernel == 0 && rows < sel.tile_rows) {
+      if (used) { *used = sel; used->kernel = 2; used->rows_per_cta = 0; used->strip = 0; used->bulk = 0; }
+      return launch_tile<MODE, AUG, FXY>(P, s);
     }
-    if (rows < tile_rows) return launch_tile<MODE, AUG, FXY>(P, s);
+  }
+  if (used) {
+    *used = sel;
+    used->kernel = 1;
+    used->rows_per_cta = P.rows_per_cta;
+    used->strip = TY;
+    // some strip is interior (j0 >= 2 and j0 + TY + 2 <= ny) and stages rows by bulk copies
+    used->bulk = P.tma && P.ny >= 2 * TY + 2;
   }
   dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
   return launch_pdl(k, grid, dim3(TY), sm, s, P);
 }
 
 template <int TY, int FXY>
-static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s) {
-  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false, FXY>(P, ns, s);
+static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s,
+                            const StencilPath& sel, StencilPath* used) {
+  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false, FXY>(P, ns, s, sel, used);
   if (mode == MODE_JV)
-    return aug ? launch_t<TY, MODE_JV, true, FXY>(P, ns, s) : launch_t<TY, MODE_JV, false, FXY>(P, ns, s);
-  return aug ? launch_t<TY, MODE_JVN, true, FXY>(P, ns, s) : launch_t<TY, MODE_JVN, false, FXY>(P, ns, s);
+    return aug ? launch_t<TY, MODE_JV, true, FXY>(P, ns, s, sel, used)
+               : launch_t<TY, MODE_JV, false, FXY>(P, ns, s, sel, used);
+  return aug ? launch_t<TY, MODE_JVN, true, FXY>(P, ns, s, sel, used)
+             : launch_t<TY, MODE_JVN, false, FXY>(P, ns, s, sel, used);
 }
 
 template <int TY>
-static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s) {
+static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s,
+                             const StencilPath& sel, StencilPath* used) {
   // 2h constants: powers of two (e.g. [0,1]^2 on 2^k cells) make the 28 centred-difference
   // divisions per cell single multiplications; otherwise one or two FMA corrections
   if (is_pow2(P.two_hx) && is_pow2(P.two_hy) && P.r_two_hx == 1.0 / P.two_hx &&
       P.r_two_hy == 1.0 / P.two_hy)
-    return launch_f<TY, DIV_POW2>(P, mode, aug, ns, s);
+    return launch_f<TY, DIV_POW2>(P, mode, aug, ns, s, sel, used);
   const bool fxy = recip_tight(P.two_hx, P.r_two_hx) && recip_tight(P.two_hy, P.r_two_hy);
-  return fxy ? launch_f<TY, DIV_TIGHT>(P, mode, aug, ns, s) : launch_f<TY, DIV_GENERAL>(P, mode, aug, ns, s);
+  return fxy ? launch_f<TY, DIV_TIGHT>(P, mode, aug, ns, s, sel, used)
+             : launch_f<TY, DIV_GENERAL>(P, mode, aug, ns, s, sel, used);
 }
 
-int stencil_tile_width(int ny) {
-  static int forced = -1;
-  if (forced < 0) {
-    const char* env = getenv("EMHD_STENCIL_TY");
-    forced = env ? atoi(env) : 0;
-  }
+int stencil_tile_width(int ny, int forced) {
   if (forced == 32 || forced == 64 || forced == 128) return forced;
   return ny <= 32 ? 32 : (ny <= 64 ? 64 : 128);
 }
 
-cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s) {
-  const int ty = stencil_tile_width(P.ny);
-  if (ty == 32) return launch_ty<32>(P, mode, aug, num_sms, s);
-  if (ty == 64) return launch_ty<64>(P, mode, aug, num_sms, s);
-  return launch_ty<128>(P, mode, aug, num_sms, s);
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+StencilPath stencil_path_defaults() {
+  StencilPath p;
+  p.kernel = 0;
+  p.rows_per_cta = 0;
+  p.strip = env_int("EMHD_STENCIL_TY", 0);
+  p.bulk = env_int("EMHD_STENCIL_TMA", 1) != 0;
+  p.min_rows = env_int("EMHD_MIN_ROWS", 2);
+  p.tile_rows = env_int("EMHD_STENCIL_TILE_ROWS", 6);
+  return p;
+}
+
+cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s,
+                           const StencilPath& sel, StencilPath* used) {
+  const int ty = stencil_tile_width(P.ny, sel.strip);
+  if (ty == 32) return launch_ty<32>(P, mode, aug, num_sms, s, sel, used);
+  if (ty == 64) return launch_ty<64>(P, mode, aug, num_sms, s, sel, used);
+  return launch_ty<128>(P, mode, aug, num_sms, s, sel, used);
 }
 
 }  // namespace emhd

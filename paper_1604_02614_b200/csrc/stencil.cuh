@@ -37,8 +37,21 @@ struct StencilParams {
   double* evals;              // optional: 1 if this launch evaluated the RHS (counted), else 0
 };
 
-cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s);
-int stencil_tile_width(int ny);
+// Launch selection of the stencil (per context: emhd_set_stencil_path; defaults from the
+// environment at context creation).  Also the record of what a launch actually ran.
+struct StencilPath {
+  int kernel;        // 0 auto, 1 row-marching strips, 2 2D tiles
+  int rows_per_cta;  // marching: rows per CTA (0: one wave of resident CTAs, >= min_rows)
+  int strip;         // marching: strip width 32 / 64 / 128 (0: by ny)
+  int bulk;          // marching: interior strips stage raw rows with bulk async copies (when aligned)
+  int min_rows;      // auto: floor of rows per CTA
+  int tile_rows;     // auto: 2D tiles when a marching CTA would get fewer rows than this
+};
+
+StencilPath stencil_path_defaults();   // EMHD_STENCIL_TY / _TMA / _TILE_ROWS, EMHD_MIN_ROWS
+cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s,
+                           const StencilPath& sel, StencilPath* used = nullptr);
+int stencil_tile_width(int ny, int forced);
 cudaError_t launch_diag(StencilParams P, int which, double* out, unsigned long long* dmax, cudaStream_t s);
 cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* keys, cudaStream_t s);
 

@@ -115,6 +115,23 @@ class Ctx:
         N.check(self.lib.emhd_status_read(self.sync_stream(), ctypes_byref(st)), "status_read")
         return st
 
+    def stencil_path(self, **kw):
+        """Current stencil launch selection as a dict; keyword arguments (kernel, rows_per_cta,
+        strip, bulk, min_rows, tile_rows) change it for every later launch on this context."""
+        sp = N.StencilPath()
+        N.check(self.lib.emhd_get_stencil_path(self.h, ctypes_byref(sp)), "get_stencil_path")
+        if kw:
+            for k, v in kw.items():
+                setattr(sp, k, int(v))
+            N.check(self.lib.emhd_set_stencil_path(self.h, ctypes_byref(sp)), "set_stencil_path")
+        return {k: getattr(sp, k) for k, _ in N.StencilPath._fields_}
+
+    def last_stencil(self):
+        """What the last stencil launch on this context ran (kernel 1 marching / 2 tile, ...)."""
+        sp = N.StencilPath()
+        N.check(self.lib.emhd_last_stencil(self.h, ctypes_byref(sp)), "last_stencil")
+        return {k: getattr(sp, k) for k, _ in N.StencilPath._fields_}
+
     def reset_status(self):
         N.check(self.lib.emhd_status_reset(self.sync_stream()), "status_reset")
 

@@ -255,9 +255,11 @@ class _Process:
         self.evals = self._small[o3 + self.m_cap + 1:o3 + 2 * (self.m_cap + 1)]   # RHS evals per iteration
         self.reorth = self._small[o3 + 2 * (self.m_cap + 1):o3 + 3 * (self.m_cap + 1)]  # 1: pass 2 skipped
         self.md2 = self._small[o3 + 3 * (self.m_cap + 1):o3 + 4 * (self.m_cap + 1)]     # 0: separate h2 dots
-        # reorthogonalize=False (the reference's single projection pass): the decision always
-        # skips pass 2; otherwise selective on the fused engines, both passes elsewhere
-        self.eta = (REORTH_ETA if engine.fused else 0.0) if reorthogonalize else 1e-300
+        # selective on the fused engines, both passes elsewhere.  `reorthogonalize` is accepted
+        # and ignored, exactly as the reference does: its _ArnoldiProcess stores nothing from it
+        # and always runs the re-orthogonalisation pass (`if True:`, krylov.py:156-160)
+        del reorthogonalize
+        self.eta = REORTH_ETA if engine.fused else 0.0
         self.scal = D.Scratch(4)
         self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
         self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)

@@ -29,6 +29,10 @@ def test_reference_arm_prints_one_contract_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["config"]["workload"].startswith("config2")
+    # like-for-like: the m = 40 factorisation, iterations sampled across j in [0, 40)
+    assert d["config"]["m_sampled"] == 40 and d["config"]["j_sampled"] == [20]
+    assert d["full_build"]["iterations_per_s"] > 0 and len(d["full_build"]["per_iteration_s"]) == 40
+    assert "Gram-Schmidt" in d["config"]["orthogonalisation"]
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
@@ -46,7 +50,7 @@ def test_our_arm_contract_line_on_gpu():
     import torch
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
     r = subprocess.run([sys.executable, "bench.py", "--n", "128", "--steps", "3", "--warmup", "3",
-                        "--jv", "5", "--no-trajectory"], cwd=ROOT, capture_output=True, text=True,
+                        "--jv", "5", "--no-trajectory", "--no-secondary"], cwd=ROOT, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
@@ -60,3 +64,6 @@ def test_our_arm_contract_line_on_gpu():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
+    assert len(d["cpu_baseline"]["j_sampled"]) == 5
+    tp = d["two_pass"]
+    assert tp["value"] > 0 and tp["iteration_roofline"]["frac"] > 0
