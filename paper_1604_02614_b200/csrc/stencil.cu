@@ -427,10 +427,12 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
     }
   } else {
     // column slots handled by this thread: main slot c = t + 2 (column j0 + t), extra
-    // halo slots 1,0 (threads 0,1) and TY+3, TY+2 (threads TY-2, TY-1): the threads that
-    // compute the halo y-fluxes (slots 1 and TY+2) own those columns' centre quantities
+    // halo slots 1, 0, TY+3, TY+2 (threads 0..3: all four in warp 0, so the halo columns cost
+    // ONE extra warp-wide evaluation per row instead of one in each edge warp); the threads
+    // that compute the halo y-fluxes (slots 1 and TY+2: threads 0 and 3) own those columns'
+    // centre quantities
     const int cmain = t + 2;
-    const int cextra = t == 0 ? 1 : t == 1 ? 0 : t == TY - 2 ? TY + 3 : t == TY - 1 ? TY + 2 : -1;
+    const int cextra = t == 0 ? 1 : t == 1 ? 0 : t == 2 ? TY + 3 : t == 3 ? TY + 2 : -1;
     auto col_ok = [&](int c) { int j = j0 - 2 + c; return j >= -2 && j <= P.ny + 1; };
     bool fm, fe = false;
     const int jm = map_ghost(j0 - 2 + cmain, P.ny, P.bcy, fm);
@@ -554,11 +556,11 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
         }
         if (out_row) {
           // y-fluxes at the strip's halo columns j0-1 (thread 0, extra slot 1) and
-          // j0+ncols (thread TY-1's extra slot TY+2 on a full strip, else the main slot of
+          // j0+ncols (thread 3's extra slot TY+2 on a full strip, else the main slot of
           // thread ncols): each computed by the owner of that column's centre quantities
           int cs = -1, gslot = 0;
           if (t == 0) { cs = 1; gslot = 0; }
-          if (t == (ncols_out == TY ? TY - 1 : ncols_out)) { cs = ncols_out + 2; gslot = ncols_out + 1; }
+          if (t == (ncols_out == TY ? 3 : ncols_out)) { cs = ncols_out + 2; gslot = ncols_out + 1; }
           if (cs >= 0) {
             double gdummy[NF];
             flux_cell<FXY>(P, qm, q0, qp, c0, cs, QW, false, true, gdummy, gy);

@@ -740,51 +740,89 @@ def test_adaptive_recoverable_rejections_match_oracle(P, look):
     assert np.linalg.norm(y - yo) <= 1e-8 * np.linalg.norm(yo)
 
 
+def _invariant_pair_seed(op, n, X, Y, k, l):
+    """A unit vector u spanning (with A u) a 2-D invariant subspace of the FD Jacobian at a
+    uniform state: the linearised operator maps the 16 (field, cos/sin) patterns of wavevector
+    (k, l) into themselves, so the real part of an eigenvector of that 16 x 16 block (found by
+    least squares from 16 FD applies) is invariant to the FD round-off level."""
+    pats = []
+    for f in range(8):
+        for t in (np.cos(2 * np.pi * (k * X + l * Y)), np.sin(2 * np.pi * (k * X + l * Y))):
+            e = np.zeros((8, n, n))
+            e[f] = t
+            pats.append(e.reshape(-1))
+    B = np.array(pats).T
+    AB = np.column_stack([op(B[:, i]) for i in range(16)])
+    M = np.linalg.lstsq(B, AB, rcond=None)[0]
+    lam, Z = np.linalg.eig(M)
+    i = int(np.argmax(np.abs(lam.imag)))
+    u = B @ Z[:, i].real
+    return u / np.linalg.norm(u)
+
+
 def test_selective_reorth_stress_m120_near_dependent(P):
-    """Selective re-orthogonalisation under stress: m = 120 on the FD-MHD operator at a uniform
-    state (a constant-coefficient Jacobian: every Fourier mode spans an invariant subspace) with
-    a start vector of three modes plus a 1e-3 random part.  Once the modes' subspace is
-    exhausted the new directions come from the small random part, so w is nearly dependent on
-    the basis (||w_final|| / ||A v|| ~ 1e-3) and the second pass must run there.  For eta = 0.5
-    (default) and 1/sqrt(2): the second pass fires, V stays orthonormal to 1e-12, Krylov
-    dimension and breakdown status equal the always-two-pass run, H within 1e-8 of it."""
+    """Selective re-orthogonalisation under stress, m = 120.  FD-MHD operator at a uniform state
+    (constant-coefficient Jacobian: each wavevector's 16 patterns span an invariant subspace);
+    seed = a 2-D invariant eigen-pair direction + 1e-5 of two other modes, so iteration 1's
+    A v_1 lies in span(v_0, v_1) up to 1.7e-3 (a near-breakdown direction 300x below eta);
+    the other iterations explore the remaining modes and the FD round-off directions.
+
+    Past ~20 columns H of this operator is chaotic at the FD round-off level: the always-two-pass
+    factorisation of a seed perturbed by ONE ulp drifts from the unperturbed one by 1e-8 at
+    column ~19, 1e-5 at 80 and 1e-1 at 120 (measured, tools/probe_reorth_stress.py) — the
+    reference's own MGS2 is as sensitive.  So the bar is: for eta = 0.5 (default) and 1/sqrt(2),
+    identical Krylov dimension and breakdown status, V orthonormal to 1e-12 at m = 120, the
+    second pass taken at the near-dependent iteration, H within 1e-8 of two-pass over the
+    columns where the two-pass run is itself reproducible to 1e-8 under a 1-ulp perturbation,
+    and beyond them within 4x that run's own 1-ulp drift."""
+    from oracle import jvp, stencil
     from paper_1604_02614_b200 import krylov
     n = 32
     g = P.Grid2D(n, n, 0.0, 1.0, 0.0, 1.0)
     prm = P.MhdParams(mu=1e-2, eta=1e-2, kappa=1e-2)
-    f = P.make_rhs(prm, g, P.BoundaryPolicy("periodic", "periodic"))
+    bc = P.BoundaryPolicy("periodic", "periodic")
     U = np.zeros((8, n, n))
     U[0] = 1.0
     U[4] = 1.0                  # uniform Bx
-    U[7] = 1.5 + 0.5            # p = 1 with |B|^2 / 2 = 0.5 (gamma = 5/3)
+    U[7] = 2.0                  # p = (gamma - 1)(E - |B|^2 / 2) = 1
     x = (np.arange(n) + 0.5) / n
     X, Y = np.meshgrid(x, x, indexing="ij")
-    rng = np.random.default_rng(120)
-    v = np.zeros((8, n, n))
-    for (k, l) in ((1, 0), (0, 2), (3, 1)):
-        v += rng.standard_normal((8, 1, 1)) * np.cos(2 * np.pi * (k * X + l * Y) + rng.uniform(0, 6))
-    v = v.reshape(-1)
-    v /= np.linalg.norm(v)
-    v += 1e-3 * rng.standard_normal(v.size) / np.sqrt(v.size)
-    op = P.FdJacobianOperator(f, U.reshape(-1))
+    u = _invariant_pair_seed(jvp.FdJv(stencil.rhs_closure(prm, g, bc), U.reshape(-1)), n, X, Y, 1, 1)
+    rng = np.random.default_rng(5)
+    v = u.copy()
+    for (k, l) in ((2, 1), (0, 3)):
+        v += (1e-5 * rng.standard_normal((8, 1, 1)) *
+              np.cos(2 * np.pi * (k * X + l * Y) + rng.uniform(0, 6))).reshape(-1)
+    op = P.FdJacobianOperator(P.make_rhs(prm, g, bc), U.reshape(-1))
     old = krylov.REORTH_ETA
     out = {}
     try:
-        for eta in (0.0, 0.5, 1.0 / np.sqrt(2.0)):
+        for name, eta, seed in (("two", 0.0, v), ("up", 0.0, np.nextafter(v, np.inf)),
+                                ("down", 0.0, np.nextafter(v, -np.inf)),
+                                (0.5, 0.5, v), ("r2", 1.0 / np.sqrt(2.0), v)):
             krylov.REORTH_ETA = eta
-            b = P.arnoldi(op, dev(v), 120)
-            out[eta] = (b.m, b.breakdown, b.H.cpu().numpy(), b.V,
-                        None if b.second_pass is None else b.second_pass.cpu().numpy())
+            b = P.arnoldi(op, dev(seed), 120)
+            G = (b.V.T @ b.V).cpu().numpy()
+            out[name] = (b.m, b.breakdown, b.H.cpu().numpy(), np.max(np.abs(G - np.eye(G.shape[0]))),
+                         None if b.second_pass is None else b.second_pass.cpu().numpy())
     finally:
         krylov.REORTH_ETA = old
-    m2, brk2, H2, V2, _ = out[0.0]
-    assert m2 == 120 and not brk2
-    sub = H2[1:, :].diagonal() / np.abs(H2).max(axis=0)      # h_{j+1,j} relative to column scale
-    assert sub.min() < 1e-2, sub.min()                         # the near-dependence is real
-    for eta in (0.5, 1.0 / np.sqrt(2.0)):
-        m, brk, H, V, sp = out[eta]
-        assert (m, brk) == (m2, brk2), eta
-        assert 0 < sp.sum() < len(sp), (eta, sp.sum())        # both branches taken
-        G = (V.T @ V).cpu().numpy()
-        assert np.max(np.abs(G - np.eye(G.shape[0]))) <= 1e-12, eta
-        assert np.linalg.norm(H - H2) <= 1e-8 * np.linalg.norm(H2), (eta, np.linalg.norm(H - H2) / np.linalg.norm(H2))
+    m2, brk2, H2, orth2, _ = out["two"]
+    assert m2 == 120 and not brk2 and orth2 <= 1e-12
+
+    def drift(H, k):
+        return np.linalg.norm(H[:, :k] - H2[:, :k]) / np.linalg.norm(H2[:, :k])
+
+    # the near-dependence is real: h_{2,1} / ||A v_1|| ~ 1e-3 in the two-pass factorisation
+    assert H2[2, 1] / np.linalg.norm(H2[:3, 1]) < 1e-2
+    floor = {k: max(drift(out["up"][2], k), drift(out["down"][2], k)) for k in range(1, 121)}
+    k_rep = max(k for k in range(1, 121) if floor[k] <= 1e-8)      # reproducible columns
+    assert k_rep >= 12, k_rep
+    for name in (0.5, "r2"):
+        m, brk, H, orth, sp = out[name]
+        assert (m, brk) == (m2, brk2), name
+        assert orth <= 1e-12, (name, orth)
+        assert sp[1] == 1.0 and 1 < sp.sum() < len(sp), (name, sp.sum())   # pass 2 where needed
+        assert drift(H, k_rep) <= 1e-8, (name, k_rep, drift(H, k_rep))
+        for k in (40, 60, 80):
+            assert drift(H, k) <= 4.0 * floor[k] + 1e-9, (name, k, drift(H, k), floor[k])
