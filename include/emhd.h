@@ -35,6 +35,7 @@ extern "C" {
 #define EMHD_ERR_PRESSURE 2
 #define EMHD_ERR_NONFINITE 3
 #define EMHD_ERR_CUDA 4
+/* 5: EMHD_ERR_NCCL (below) */
 #define EMHD_ERR_ARG 6
 #define EMHD_ERR_DENSE 7
 
@@ -275,6 +276,36 @@ int emhd_profile_read(emhd_ctx* ctx, int max_n, int* kinds, double* ms, double* 
  * host synchronisation of a residual check. */
 int emhd_readback(emhd_ctx* ctx, const double* brk, int nbrk, const double* res, int nres,
                   double* host_out, emhd_status* st);
+
+/* ---- slab-rank collectives (x-slab decomposition, one process per GPU) ---- */
+/* A context placed on an x-slab (EXTERNAL x sides) owns a communicator: the Arnoldi driver
+ * (emhd_arnoldi_iter) then all-reduces its dot products and norms from C (stream-ordered, no
+ * host sync) and every stencil entry point called with a NULL halo for the array it perturbs
+ * exchanges that halo itself, on a second stream, while the interior rows [2, nx-2) run; the
+ * edge rows follow when the halo has landed.  The reference is single-process; these replace
+ * the distributed form of its sums (krylov.py:151,153,158,161) and ghosts (mhd.py:144-165). */
+#define EMHD_ERR_NCCL 5
+#define EMHD_OP_SUM 0
+#define EMHD_OP_MAX 2
+#define EMHD_OP_MIN 3
+/* 128-byte NCCL unique id (rank 0 creates two: reduce and halo communicators) */
+int emhd_nccl_unique_id(void* out128);
+/* NCCL transport; lo / hi: neighbour ranks of the EXTERNAL x sides (-1: none, must match the
+ * geometry's bc_x_lo / bc_x_hi); a rank may be its own neighbour (periodic ring of one) */
+int emhd_comm_init_nccl(emhd_ctx* ctx, int nranks, int rank, int lo, int hi, const void* uid_reduce,
+                        const void* uid_halo);
+/* Host-callback transport (tests: ranks sharing one GPU over a CPU channel): ar(user, buf, n, op)
+ * reduces n host doubles in place across ranks; ex(user, send, recv, n_side) delivers send[2][n_side]
+ * (rows {0,1}, rows {nx-2,nx-1}) and fills recv[2][n_side] (lo neighbour's top rows, hi neighbour's
+ * bottom rows).  Both return 0 on success.  Collectives synchronise the context's stream. */
+typedef int (*emhd_host_allreduce_fn)(void* user, double* buf, int n, int op);
+typedef int (*emhd_host_exchange_fn)(void* user, const double* send, double* recv, long long n_side);
+int emhd_comm_init_host(emhd_ctx* ctx, int nranks, int rank, int lo, int hi, emhd_host_allreduce_fn ar,
+                        emhd_host_exchange_fn ex, void* user);
+/* in-place all-reduce of n device doubles (EMHD_OP_*) across the context's ranks (no comm: no-op) */
+int emhd_allreduce(emhd_ctx* ctx, double* buf, int n, int op);
+/* halo[2][8][2][ny] = x-halo of x (pack + exchange, ordered on the context's stream) */
+int emhd_halo_exchange(emhd_ctx* ctx, const double* x, double* halo);
 
 /* ---- slab halos ------------------------------------------------------ */
 /* sendbuf[2][8][2][ny] = rows {0,1} and {nx-2, nx-1} of every field of x */

@@ -40,7 +40,7 @@ class ArnoldiArgs(ctypes.Structure):
                 ("brk", P), ("n_top", c_ll), ("len_dot", c_ll), ("len_upd", c_ll), ("p", c_int),
                 ("nb", c_int), ("ch", c_dbl), ("bcol", P * 5), ("bidx", c_int * 5),
                 ("gen", c_int), ("gate", P), ("evals", P), ("eta", c_dbl), ("reorth", P),
-                ("md2", P)]
+                ("md2", P), ("a_halo", P)]
 
 
 class StencilPath(ctypes.Structure):
@@ -56,6 +56,9 @@ class Report(ctypes.Structure):
 
 
 ST_RHO, ST_PRESSURE, ST_NONFINITE, ST_BREAKDOWN, ST_DENSE = 1, 2, 4, 8, 16
+OP_SUM, OP_MAX, OP_MIN = 0, 2, 3
+HostAllreduceFn = ctypes.CFUNCTYPE(c_int, c_vp, DP, c_int, c_int)
+HostExchangeFn = ctypes.CFUNCTYPE(c_int, c_vp, DP, DP, c_ll)
 BC = {"periodic": 0, "reflect": 1, "zero-gradient": 2, "external": 3}
 
 _SIGS = {
@@ -115,6 +118,12 @@ _SIGS = {
     "emhd_max_signal_speed": (c_int, [c_vp, P, P]),
     "emhd_field_sqdiff": (c_int, [c_vp, P, P, P]),
     "emhd_lincomb_onto": (c_int, [c_vp, P, c_int, PP, DP, IP, c_dbl, c_int, P, c_ll]),
+    "emhd_nccl_unique_id": (c_int, [ctypes.c_char_p]),
+    "emhd_comm_init_nccl": (c_int, [c_vp, c_int, c_int, c_int, c_int, ctypes.c_char_p, ctypes.c_char_p]),
+    "emhd_comm_init_host": (c_int, [c_vp, c_int, c_int, c_int, c_int, HostAllreduceFn, HostExchangeFn,
+                                    c_vp]),
+    "emhd_allreduce": (c_int, [c_vp, P, c_int, c_int]),
+    "emhd_halo_exchange": (c_int, [c_vp, P, P]),
 }
 
 _lib = None

@@ -24,6 +24,7 @@ SOURCES = {
     "harness.cu": ["-fmad=false"],
     "krylov.cu": [],
     "dense.cu": [],
+    "slabcomm.cu": [],
     "capi.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -63,7 +64,7 @@ def build(verbose=False, force=False):
         if proc.wait() != 0:
             raise subprocess.CalledProcessError(proc.returncode, cmd)
     if force or _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -11,6 +11,7 @@
 #include "dense.cuh"
 #include "vecops.cuh"
 #include "harness.cuh"
+#include "slabcomm.cuh"
 
 using namespace emhd;
 
@@ -36,6 +37,13 @@ struct emhd_ctx {
   bool l2win = false;                         // emhd_l2_window set on this context's stream
   StencilPath path{};                         // stencil launch selection (emhd_set_stencil_path)
   StencilPath last{};                         // what the last stencil launch ran
+  // slab-rank collectives (emhd_comm_init_*): all-reduces on `stream`, halo exchange on
+  // halo_stream into hrecv, overlapped with the interior rows of the stencil that needs it
+  SlabComm* comm = nullptr;
+  cudaStream_t halo_stream = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_halo = nullptr;
+  double* hsend = nullptr;                    // [2][8][2][ny] edge rows of the exchanged array
+  double* hrecv = nullptr;                    // [2][8][2][ny] halo the stencil reads
   // per-launch profiling (emhd_profile): CUDA events around every launch of the Arnoldi path
   struct ProfRec { int kind; cudaEvent_t e0, e1; double bytes; const double* gate[2]; };
   bool prof = false;
@@ -100,6 +108,7 @@ extern "C" const char* emhd_error_string(int code) {
     case EMHD_ERR_PRESSURE: return "non-positive pressure";
     case EMHD_ERR_NONFINITE: return "non-finite rhs value during Jacobian apply";
     case EMHD_ERR_CUDA: return "CUDA error";
+    case EMHD_ERR_NCCL: return "NCCL / slab communication error";
     case EMHD_ERR_ARG: return "bad argument";
     case EMHD_ERR_DENSE: return "non-finite small dense exponential";
     default: return "unknown";
@@ -122,6 +131,7 @@ static void fill_base(emhd_ctx* c) {
   P.two_hy = 2.0 * c->g.hy; P.r_two_hy = 1.0 / P.two_hy;    // mhd.py:206
   P.n_top = (long long)NF * c->g.nx * c->g.ny;
   P.st = c->st;
+  P.rows_mode = 0; P.row_lo = 0; P.row_hi = c->g.nx; P.count = 1;
 }
 
 extern "C" int emhd_ctx_create(emhd_ctx** out, const emhd_geometry* g, const emhd_physics* p,
@@ -163,6 +173,12 @@ extern "C" int emhd_ctx_destroy(emhd_ctx* c) {
   cudaFree(c->dense);
   prof_clear(c);
   cudaFree(c->cancel);
+  if (c->comm) slabcomm_destroy(c->comm);
+  if (c->halo_stream) cudaStreamDestroy(c->halo_stream);
+  if (c->ev_x) cudaEventDestroy(c->ev_x);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  cudaFree(c->hsend);
+  cudaFree(c->hrecv);
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->cancel_host) cudaFreeHost(c->cancel_host);
   delete c;
@@ -292,12 +308,117 @@ static void set_epilogue(StencilParams& P, int p, double ch, int nb, const doubl
   for (int k = 0; k < nb; ++k) { P.bcol[k] = bcol[k]; P.bidx[k] = bidx[k]; }
 }
 
+// ---- slab-rank collectives -------------------------------------------------------------
+extern "C" int emhd_nccl_unique_id(void* out128) {
+  return slabcomm_nccl_unique_id(out128) ? EMHD_ERR_NCCL : EMHD_OK;
+}
+
+static int comm_buffers(emhd_ctx* c) {
+  const size_t n = (size_t)2 * NF * 2 * c->g.ny;
+  int rc = cerr(cudaMalloc(&c->hsend, n * sizeof(double)));
+  if (!rc) rc = cerr(cudaMalloc(&c->hrecv, n * sizeof(double)));
+  if (!rc) rc = cerr(cudaMemset(c->hrecv, 0, n * sizeof(double)));
+  if (!rc) rc = cerr(cudaStreamCreateWithFlags(&c->halo_stream, cudaStreamNonBlocking));
+  if (!rc) rc = cerr(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
+  if (!rc) rc = cerr(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  return rc;
+}
+
+static int comm_args_ok(emhd_ctx* c, int nranks, int rank, int lo, int hi) {
+  return c && !c->comm && nranks >= 1 && rank >= 0 && rank < nranks && lo >= -1 && lo < nranks &&
+         hi >= -1 && hi < nranks && (lo >= 0) == (c->g.bc_x_lo == EMHD_BC_EXTERNAL) &&
+         (hi >= 0) == (c->g.bc_x_hi == EMHD_BC_EXTERNAL);
+}
+
+extern "C" int emhd_comm_init_nccl(emhd_ctx* c, int nranks, int rank, int lo, int hi,
+                                   const void* uid_reduce, const void* uid_halo) {
+  if (!comm_args_ok(c, nranks, rank, lo, hi) || !uid_reduce || !uid_halo) return EMHD_ERR_ARG;
+  int rc = cerr(cudaSetDevice(c->device));
+  if (rc) return rc;
+  int err = 0;
+  SlabComm* sc = slabcomm_create_nccl(nranks, rank, lo, hi, uid_reduce, uid_halo, &err);
+  if (!sc) return err == 6 ? EMHD_ERR_ARG : EMHD_ERR_NCCL;
+  c->comm = sc;
+  return comm_buffers(c);
+}
+
+extern "C" int emhd_comm_init_host(emhd_ctx* c, int nranks, int rank, int lo, int hi,
+                                   emhd_host_allreduce_fn ar, emhd_host_exchange_fn ex, void* user) {
+  if (!comm_args_ok(c, nranks, rank, lo, hi) || !ar || !ex) return EMHD_ERR_ARG;
+  c->comm = slabcomm_create_host(nranks, rank, lo, hi, ar, ex, user);
+  if (!c->comm) return EMHD_ERR_ARG;
+  return comm_buffers(c);
+}
+
+extern "C" int emhd_allreduce(emhd_ctx* c, double* buf, int n, int op) {
+  if (!c || !buf || n < 0 || (op != EMHD_OP_SUM && op != EMHD_OP_MAX && op != EMHD_OP_MIN)) return EMHD_ERR_ARG;
+  if (!c->comm) return EMHD_OK;
+  const int rc = slabcomm_allreduce(c->comm, buf, n, op, c->stream);
+  return rc == 4 ? EMHD_ERR_CUDA : (rc ? EMHD_ERR_NCCL : EMHD_OK);
+}
+
+__global__ void pack_edges_kernel(const double* x, double* buf, int nx, int ny);
+
+static cudaError_t pack_edges(emhd_ctx* c, const double* x, double* buf, cudaStream_t s) {
+  const long long total = 2LL * NF * 2 * c->g.ny;
+  pack_edges_kernel<<<(int)((total + 255) / 256), 256, 0, s>>>(x, buf, c->g.nx, c->g.ny);
+  return cudaGetLastError();
+}
+
+static int comm_rc(int rc) { return rc == 4 ? EMHD_ERR_CUDA : (rc ? EMHD_ERR_NCCL : EMHD_OK); }
+
+// x-halo of x into `halo` ([2][8][2][ny]) on the context's stream (host transport: synchronous)
+extern "C" int emhd_halo_exchange(emhd_ctx* c, const double* x, double* halo) {
+  if (!c || !x || !halo) return EMHD_ERR_ARG;
+  if (!c->comm) return EMHD_ERR_ARG;
+  int rc = cerr(pack_edges(c, x, c->hsend, c->stream));
+  if (rc) return rc;
+  return comm_rc(slabcomm_exchange(c->comm, c->hsend, halo, (long long)NF * 2 * c->g.ny, c->stream));
+}
+
+// The stencil P over the whole slab.  When the context has a communicator and the caller gave
+// no halo for `x` (*halo_field == null on an EXTERNAL side), the halo is exchanged here: the
+// exchange runs on the halo stream while the interior rows [2, nx-2) — which need no halo —
+// run on the compute stream; the two edge row pairs follow once the halo has landed.
+static int stencil_with_halo(emhd_ctx* c, StencilParams P, int mode, bool aug, const double* x,
+                             bool x_is_a) {
+  const bool external = c->g.bc_x_lo == EMHD_BC_EXTERNAL || c->g.bc_x_hi == EMHD_BC_EXTERNAL;
+  const double*& halo_field = x_is_a ? P.a_halo : P.v_halo;
+  if (!c->comm || !external || halo_field != nullptr)
+    return cerr(launch_stencil(P, mode, aug, c->num_sms, c->stream, c->path, &c->last));
+  halo_field = c->hrecv;
+  const long long n_side = (long long)NF * 2 * c->g.ny;
+  if (slabcomm_is_host(c->comm) || c->g.nx < 4) {
+    int rc = cerr(pack_edges(c, x, c->hsend, c->stream));
+    if (!rc) rc = comm_rc(slabcomm_exchange(c->comm, c->hsend, c->hrecv, n_side, c->stream));
+    if (!rc) rc = cerr(launch_stencil(P, mode, aug, c->num_sms, c->stream, c->path, &c->last));
+    return rc;
+  }
+  int rc = cerr(cudaEventRecord(c->ev_x, c->stream));
+  if (!rc) rc = cerr(cudaStreamWaitEvent(c->halo_stream, c->ev_x, 0));
+  if (!rc) rc = cerr(pack_edges(c, x, c->hsend, c->halo_stream));
+  if (!rc) rc = comm_rc(slabcomm_exchange(c->comm, c->hsend, c->hrecv, n_side, c->halo_stream));
+  if (!rc) rc = cerr(cudaEventRecord(c->ev_halo, c->halo_stream));
+  if (rc) return rc;
+  if (c->g.nx > 4) {
+    StencilParams Pi = P;
+    Pi.rows_mode = 1; Pi.row_lo = 2; Pi.row_hi = c->g.nx - 2; Pi.count = 1;
+    rc = cerr(launch_stencil(Pi, mode, aug, c->num_sms, c->stream, c->path, &c->last));
+    if (rc) return rc;
+  }
+  rc = cerr(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+  if (rc) return rc;
+  StencilParams Pb = P;
+  Pb.rows_mode = 2; Pb.count = c->g.nx > 4 ? 0 : 1;
+  return cerr(launch_stencil(Pb, mode, aug, c->num_sms, c->stream, c->path, &c->last));
+}
+
 extern "C" int emhd_rhs(emhd_ctx* c, const double* u, const double* u_halo, double* F) {
   if (!c || !u || !F) return EMHD_ERR_ARG;
   StencilParams P = c->base;
   P.epoch = c->epoch;
   P.a = u; P.a_halo = u_halo; P.out = F;
-  return cerr(launch_stencil(P, MODE_RHS, false, c->num_sms, c->stream, c->path, &c->last));
+  return stencil_with_halo(c, P, MODE_RHS, false, u, true);
 }
 
 extern "C" int emhd_jv(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
@@ -307,7 +428,7 @@ extern "C" int emhd_jv(emhd_ctx* c, const double* a, const double* a_halo, const
   P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = v; P.v_halo = v_halo; P.scal = d_vnorm; P.out = out;
   ProfScope ps(c, EMHD_K_JV, 4.0 * 64.0 * (double)c->g.nx * c->g.ny);   // 4W
-  return cerr(launch_stencil(P, MODE_JV, false, c->num_sms, c->stream, c->path, &c->last));
+  return stencil_with_halo(c, P, MODE_JV, false, v, false);
 }
 
 extern "C" int emhd_jv_aug(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
@@ -321,7 +442,7 @@ extern "C" int emhd_jv_aug(emhd_ctx* c, const double* a, const double* a_halo, c
   P.a = a; P.a_halo = a_halo; P.fa = fa; P.v = u; P.v_halo = u_halo; P.scal = d_vnorm; P.out = out;
   P.qsrc = d_q;
   set_epilogue(P, p, ch, nb, bcol, bidx);
-  return cerr(launch_stencil(P, MODE_JV, true, c->num_sms, c->stream, c->path, &c->last));
+  return stencil_with_halo(c, P, MODE_JV, true, u, false);
 }
 
 extern "C" int emhd_jv_normalized(emhd_ctx* c, const double* a, const double* a_halo, const double* fa,
@@ -336,7 +457,7 @@ extern "C" int emhd_jv_normalized(emhd_ctx* c, const double* a, const double* a_
   P.out = out; P.vout = v_out;
   set_epilogue(P, p, ch, nb, bcol, bidx);
   ProfScope ps(c, EMHD_K_JV_NORMALIZED, 5.0 * 64.0 * (double)c->g.nx * c->g.ny);   // 5W
-  return cerr(launch_stencil(P, MODE_JVN, p > 0, c->num_sms, c->stream, c->path, &c->last));
+  return stencil_with_halo(c, P, MODE_JVN, p > 0, w, false);
 }
 
 static KWork kwork(emhd_ctx* c) {
@@ -722,6 +843,9 @@ extern "C" int emhd_admissibility_report(emhd_ctx* c, int mode, const double* a,
   StencilParams P = c->base;
   P.epoch = c->epoch;
   P.a = a; P.a_halo = a_halo; P.v = v; P.v_halo = v_halo; P.scal = scal;
+  // a halo exchanged inside the library (caller passed none) is the context's own buffer
+  if (c->comm && mode == 0 && !P.a_halo) P.a_halo = c->hrecv;
+  if (c->comm && mode != 0 && !P.v_halo) P.v_halo = c->hrecv;
   unsigned long long* keys = nullptr;
   int rc = cerr(cudaMalloc(&keys, 4 * sizeof(unsigned long long)));
   if (rc) return rc;
@@ -769,16 +893,100 @@ struct emhd_arnoldi_args_s {
   double* reorth;      // [m_cap + 1] 1 where iteration j skipped the second pass
   double* md2;         // [m_cap + 1] (or null) 0 where iteration j needed a separate pass-2
                        // multi-dot (pass 2 ran although the re-projection was predicted away)
+  const double* a_halo;  // slab ranks: x-halo of a (exchanged once per operator)
 };
 
 // Iteration j of krylov.py:144-168 on one rank: (normalise w_{j-1} +) Jv, pass-1 multi-dot with
 // the breakdown scale, update + re-projection, update + norms + column bookkeeping.  Writes
 // w_{j} into w0/w1 (j even/odd) and V[j] (j > 0), H[:, j], scal, brk[j].
+// Iteration j on a slab rank (context with a communicator): the same kernels as the
+// single-rank iteration below, with the reductions of krylov.py:151,153,158,161 all-reduced in
+// between (stream-ordered NCCL, no host sync) and the x-halo of the vector the stencil
+// perturbs exchanged while the stencil's interior rows run.  The selective re-orthogonalisation
+// decision is taken by a one-CTA kernel from the all-reduced sums, so every rank takes the same
+// branch; the pass-2 launches test its gate, the pass-2 norm all-reduce is issued regardless
+// (unused when skipped).  No prediction of the re-projection dots (pass 1 always computes them).
+static int arnoldi_iter_slab(emhd_ctx* c, const emhd_arnoldi_args_s* A, int j) {
+  double* out = (j % 2 == 0) ? A->w0 : A->w1;
+  const double W = 8.0 * (double)A->n_top;
+  StencilParams P = c->base;
+  P.epoch = j;
+  P.evals = A->evals ? A->evals + j : nullptr;
+  P.a = A->a; P.fa = A->fa; P.out = out;
+  P.a_halo = A->a_halo;
+  set_epilogue(P, A->p, A->ch, A->nb, A->bcol, A->bidx);
+  KWork k = kwork(c);
+  int rc;
+  if (j == 0) {
+    {
+      ProfScope ps(c, EMHD_K_NORMS, W);
+      rc = cerr(launch_norms(A->V, 0, A->n_top, k, A->vn, c->stream));
+    }
+    if (!rc) rc = comm_rc(slabcomm_allreduce(c->comm, A->vn + 1, 1, EMHD_OP_MAX, c->stream));
+    if (rc) return rc;
+    P.v = A->V; P.scal = A->vn + 1;
+    if (A->p > 0) P.qsrc = A->V + A->n_top;
+    ProfScope ps(c, EMHD_K_JV, 4.0 * W);
+    rc = stencil_with_halo(c, P, MODE_JV, A->p > 0, A->V, false);
+  } else {
+    P.v = (j % 2 == 0) ? A->w1 : A->w0;
+    P.scal = A->scal;
+    P.vout = A->V + (size_t)j * A->ldv;
+    ProfScope ps(c, EMHD_K_JV_NORMALIZED, 5.0 * W);
+    rc = stencil_with_halo(c, P, MODE_JVN, A->p > 0, P.v, false);
+  }
+  if (rc) return rc;
+  const int nv = j + 1;
+  FinishArgs F;
+  F.h1 = A->d1; F.h2 = A->d2; F.selfdot = A->d1 + nv; F.j = j; F.H = A->H; F.ldh = A->ldh;
+  F.scal = A->scal; F.brk_hist = A->brk; F.st = c->st; F.rtol = 1e-12;
+  const double vb = 8.0 * (double)A->len_upd;
+  const bool selective = A->eta > 0.0 && A->reorth;
+  // pass 1: h1 = V^T w and ||w||^2 (the breakdown scale)
+  {
+    ProfScope ps(c, EMHD_K_MULTIDOT, (nv + 1) * vb);
+    rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream));
+  }
+  if (!rc) rc = comm_rc(slabcomm_allreduce(c->comm, A->d1, nv + 1, EMHD_OP_SUM, c->stream));
+  // w -= V h1 with the re-projection dots h2 = V^T w1, ||w1||^2 (SUM) and max|w1_top| (MAX)
+  if (!rc) {
+    ProfScope ps(c, EMHD_K_UPDATE, (nv + 2) * vb);
+    rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
+                            A->d2, c->stream, F, nullptr, Reorth{}));
+  }
+  if (!rc) rc = comm_rc(slabcomm_allreduce_sum_max(c->comm, A->d2, nv + 1, 1, c->stream));
+  if (rc) return rc;
+  const double* gate = nullptr;
+  if (selective) {
+    gate = A->reorth + j;
+    rc = cerr(launch_reorth_decide(F, A->d2, nv, A->eta * A->eta, A->reorth + j, c->stream));
+    if (rc) return rc;
+  }
+  // pass 2 (gated): w -= V h2 ; {||w||^2, max|w_top|} all-reduced ; column bookkeeping
+  Reorth r2{};
+  r2.skip2 = gate;
+  {
+    ProfScope ps(c, EMHD_K_UPDATE_FINISH, (nv + 2) * vb, gate);
+    rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d2, A->len_upd, A->len_dot, A->n_top, 1, k,
+                            A->nrm, c->stream, FinishArgs{}, nullptr, r2));
+  }
+  if (!rc) rc = comm_rc(slabcomm_allreduce_sum_max(c->comm, A->nrm, 1, 1, c->stream));
+  if (!rc) rc = cerr(launch_arnoldi_finish(A->d1, A->d2, A->nrm, A->d1 + nv, j, A->H, A->ldh, A->scal,
+                                           A->brk, c->st, 1e-12, c->stream, gate));
+  return rc;
+}
+
 static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   if (!c || !args || j < 0) return EMHD_ERR_ARG;
   const emhd_arnoldi_args_s* A = (const emhd_arnoldi_args_s*)args;
   if (j + 1 > c->max_vectors || (gated && !A->gate)) return EMHD_ERR_ARG;
   c->epoch = j;
+  if (c->comm) {
+    // slab ranks: no look-ahead (a device-side cancellation could differ between ranks while
+    // their collectives must match one to one)
+    if (gated) return EMHD_ERR_ARG;
+    return arnoldi_iter_slab(c, A, j);
+  }
   double* out = (j % 2 == 0) ? A->w0 : A->w1;
   const double* skip = nullptr;
   const double W = 8.0 * (double)A->n_top;

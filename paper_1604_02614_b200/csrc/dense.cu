@@ -396,6 +396,18 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   const int m = P.batch ? P.mb[sidx] : P.m, n = m + P.order;
   const int col = (P.order == 0) ? 0 : m + P.order - 1;
   DenseWork W = P.work[sidx];
+  if (P.smem_work) {
+    // small n: every work matrix lives in shared memory (the same code, generic pointers):
+    // the ~100 dependent steps of an exponential (products, norms, the 2m+1 |A|-products of
+    // ell, the elimination) then wait on shared-memory latency instead of L2 round trips
+    double* b = prow + 2 * n;
+    const size_t nn = (size_t)n * n;
+    W.a = b;
+    W.e = b + nn;
+    for (int k = 0; k < 7; ++k) W.m[k] = b + (2 + k) * nn;
+    W.m[7] = b + 9 * nn;
+    W.vec = b + 11 * nn;
+  }
   double* A = W.a;
   double* E = W.e;
   double* Yrow = P.Y + (size_t)sidx * (P.batch ? P.ldy : P.m);
@@ -423,7 +435,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   for (int e = threadIdx.x; e < m * m; e += DT) if (!isfinite(A[(e / m) * n + e % m])) finite = false;
   finite = __syncthreads_and(finite);
   double* ycol = W.vec + 3 * n;                    // [2n] column result / ping-pong
-  double* sM = (n <= P.smem_n) ? prow + 2 * n : nullptr;
+  double* sM = (!P.smem_work && n <= P.smem_n) ? prow + 2 * n : nullptr;
   bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol, sM);
   if (ok) {
     bool fin2 = true;
@@ -487,7 +499,12 @@ cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t 
   }
   size_t dyn = sizeof(double) * 2 * n;
   P.smem_n = 0;
-  if (use_smem && sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
+  P.smem_work = 0;
+  const size_t whole = sizeof(double) * (2 * (size_t)n + 11 * (size_t)n * n + 5 * (size_t)n + 64);
+  if (use_smem && whole <= (size_t)max_dyn) {
+    dyn = whole;                        // n <= ~42: the whole exponential on chip
+    P.smem_work = 1;
+  } else if (use_smem && sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
     dyn = sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n);
     P.smem_n = n;
   }

@@ -33,7 +33,9 @@ struct PhiSmallArgs {
   long long ldy;            // row stride of Y in batch mode
   double sv[DENSE_MAX_SCALES];
   double rv[DENSE_MAX_SCALES];
-  int smem_n;               // set by the launcher: largest n whose [n][2n] system is on chip            // optional: full n x n exponential of scale_0 * A (S = 1)
+  int smem_n;               // set by the launcher: largest n whose [n][2n] system is on chip
+  int smem_work;            // set by the launcher: the whole workspace (11 n^2 + 5 n doubles) is
+                            // carved from dynamic shared memory instead of the global work[]
 };
 
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s);

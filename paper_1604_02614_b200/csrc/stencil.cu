@@ -349,15 +349,25 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
   pdl_sync();
   const int t = threadIdx.x;
   const int j0 = blockIdx.x * TY;
-  const int i0 = blockIdx.y * P.rows_per_cta;
-  const bool lead = blockIdx.x == 0 && blockIdx.y == 0 && t == 0;
+  // output rows [i0, i1) of this CTA: a chunk of [row_lo, row_hi) (rows_mode 0/1), or the
+  // two edge row pairs {0, 1} / {nx-2, nx-1} (rows_mode 2, the launch that waits for the halo)
+  int i0, i1;
+  if (P.rows_mode == 2) {
+    i0 = blockIdx.y == 0 ? 0 : P.nx - 2;
+    i1 = i0 + 2;
+  } else {
+    i0 = P.row_lo + blockIdx.y * P.rows_per_cta;
+    i1 = min(i0 + P.rows_per_cta, P.row_hi);
+  }
+  // the launch's bookkeeping (RHS count, evals, augmented tail) is done by the counting launch
+  const bool head = P.count && blockIdx.x == 0 && blockIdx.y == 0;
+  const bool lead = head && t == 0;
   if (P.skip && *P.skip != 0.0) {
     // cancelled look-ahead iteration (its gate was written by an earlier launch)
     if (lead && P.evals) *P.evals = 0.0;
     return;
   }
-  if (i0 >= P.nx) return;
-  const int i1 = min(i0 + P.rows_per_cta, P.nx);   // exclusive end of output rows
+  if (i0 >= i1) return;
 
   // per-call scalars: sigma, 1/sigma, h_next, 1/h_next
   double sigma = 1.0, rsig = 1.0, hnext = 1.0, rh = 1.0;
@@ -375,7 +385,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
         if (t < min(TY, P.ny - j0))
 #pragma unroll
           for (int f = 0; f < NF; ++f) P.out[r * P.ny + j0 + t + (long long)f * P.nx * P.ny] = 0.0;
-      if (blockIdx.x == 0 && blockIdx.y == 0 && t < P.p) P.out[P.n_top + t] = 0.0;
+      if (head && t < P.p) P.out[P.n_top + t] = 0.0;
       if (lead && P.evals) *P.evals = 0.0;
       return;
     }
@@ -615,7 +625,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
   }
 
   // tail of the augmented output: bottom = upshift(q) (krylov.py:271-272); v_j tail
-  if (AUG && blockIdx.x == 0 && blockIdx.y == 0 && t < P.p) {
+  if (AUG && head && t < P.p) {
     double nxt = 0.0;
 #pragma unroll
     for (int k = 1; k < 5; ++k) if (k == t + 1 && k < P.p) nxt = qv[k];
@@ -646,8 +656,8 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
       atomicMin(&P.st->first_nonfinite, s_bad);
       atomicMin(&P.st->fail_iter, P.epoch);
     }
-    if (!skip_stencil && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&P.st->rhs_evals, 1);
-    if (P.evals && blockIdx.x == 0 && blockIdx.y == 0) *P.evals = skip_stencil ? 0.0 : 1.0;
+    if (!skip_stencil && head) atomicAdd(&P.st->rhs_evals, 1);
+    if (P.evals && head) *P.evals = skip_stencil ? 0.0 : 1.0;
   }
 }
 
@@ -675,13 +685,22 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
   double* gys = gxs + NF * (TT_R + 2) * TT_C;         // [NF][TT_R][TT_C + 2]   cols -1 .. TC
   pdl_sync();
   const int t = threadIdx.x;
-  const int i0 = blockIdx.y * TT_R, j0 = blockIdx.x * TT_C;
-  const bool lead = blockIdx.x == 0 && blockIdx.y == 0 && t == 0;
+  const int j0 = blockIdx.x * TT_C;
+  int i0, nro;                                         // output rows [i0, i0 + nro)
+  if (P.rows_mode == 2) {
+    i0 = blockIdx.y == 0 ? 0 : P.nx - 2;
+    nro = 2;
+  } else {
+    i0 = P.row_lo + blockIdx.y * TT_R;
+    nro = min(TT_R, P.row_hi - i0);
+  }
+  const bool head = P.count && blockIdx.x == 0 && blockIdx.y == 0;
+  const bool lead = head && t == 0;
   if (P.skip && *P.skip != 0.0) {
     if (lead && P.evals) *P.evals = 0.0;
     return;
   }
-  const int nro = min(TT_R, P.nx - i0), nco = min(TT_C, P.ny - j0);   // output extent
+  const int nco = min(TT_C, P.ny - j0);                // output extent
   const unsigned plane = (unsigned)P.nx * (unsigned)P.ny;
   double sigma = 1.0, rsig = 1.0, hnext = 1.0, rh = 1.0;
   bool skip_stencil = false;
@@ -814,7 +833,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
   }
 
   // tail of the augmented output: bottom = upshift(q) (krylov.py:271-272); v_j tail
-  if (AUG && blockIdx.x == 0 && blockIdx.y == 0 && t < P.p) {
+  if (AUG && head && t < P.p) {
     double nxt = 0.0, cur = 0.0;
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -841,8 +860,8 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
       atomicMin(&P.st->first_nonfinite, s_bad);
       atomicMin(&P.st->fail_iter, P.epoch);
     }
-    if (!skip_stencil && blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&P.st->rhs_evals, 1);
-    if (P.evals && blockIdx.x == 0 && blockIdx.y == 0) *P.evals = skip_stencil ? 0.0 : 1.0;
+    if (!skip_stencil && head) atomicAdd(&P.st->rhs_evals, 1);
+    if (P.evals && head) *P.evals = skip_stencil ? 0.0 : 1.0;
   }
 }
 
@@ -852,7 +871,8 @@ static cudaError_t launch_tile(const StencilParams& P, cudaStream_t s) {
   const size_t sm = tile_stencil_smem();
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  dim3 grid((P.ny + TT_C - 1) / TT_C, (P.nx + TT_R - 1) / TT_R);
+  const int rows = P.rows_mode == 2 ? 0 : P.row_hi - P.row_lo;
+  dim3 grid((P.ny + TT_C - 1) / TT_C, P.rows_mode == 2 ? 2 : (rows + TT_R - 1) / TT_R);
   return launch_pdl(k, grid, dim3(TT_THREADS), sm, s, P);
 }
 
@@ -1002,7 +1022,8 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
   }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  P.rows_per_cta = sel.rows_per_cta;
+  P.rows_per_cta = P.rows_mode == 2 ? 2 : sel.rows_per_cta;
+  const int nrows = P.rows_mode == 2 ? 4 : P.row_hi - P.row_lo;   // output rows of this launch
   if (P.rows_per_cta <= 0) {
     // exactly one wave of resident CTAs (all CTAs carry equal work)
     int occ = 1;
@@ -1011,7 +1032,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
     const int target = (occ < 1 ? 1 : occ) * num_sms;
     // floor: strips x chunks must not exceed one wave of resident CTAs
     const int chunks = target / strips > 0 ? target / strips : 1;
-    const int rows = (P.nx + chunks - 1) / chunks;
+    const int rows = (nrows + chunks - 1) / chunks;
     const int min_rows = sel.min_rows < 1 ? 1 : sel.min_rows;
     P.rows_per_cta = rows < min_rows ? min_rows : rows;
     // few rows per CTA: the marching kernel's dependent row steps dominate; the 2D-tile
@@ -1029,7 +1050,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
     // some strip is interior (j0 >= 2 and j0 + TY + 2 <= ny) and stages rows by bulk copies
     used->bulk = P.tma && P.ny >= 2 * TY + 2;
   }
-  dim3 grid((P.ny + TY - 1) / TY, (P.nx + P.rows_per_cta - 1) / P.rows_per_cta);
+  dim3 grid((P.ny + TY - 1) / TY, P.rows_mode == 2 ? 2 : (nrows + P.rows_per_cta - 1) / P.rows_per_cta);
   return launch_pdl(k, grid, dim3(TY), sm, s, P);
 }
 

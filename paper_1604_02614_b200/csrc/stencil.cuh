@@ -35,6 +35,10 @@ struct StencilParams {
   int tma;                    // interior strips stage raw rows with bulk async copies (set by the launcher)
   const double* skip;         // gated launch: *skip != 0 -> no work (cancelled look-ahead iteration)
   double* evals;              // optional: 1 if this launch evaluated the RHS (counted), else 0
+  // output rows: rows_mode 0/1: [row_lo, row_hi); rows_mode 2: rows {0, 1} and {nx-2, nx-1}
+  // (the halo-dependent edge rows of a slab, launched after the halo exchange while the
+  // interior [2, nx-2) ran without it); count: this launch does the RHS count / evals / tail
+  int rows_mode, row_lo, row_hi, count;
 };
 
 // Launch selection of the stencil (per context: emhd_set_stencil_path; defaults from the

@@ -123,7 +123,7 @@ class FdJacobianOperator(LinearOperator):
             vnorm_dev = self._scr.dev[0:2]
             self.vnorm_into(v, vnorm_dev)
         if self.gpu is not None:
-            if v_halo is None:
+            if v_halo is None and not self.gpu.defer_halo:
                 v_halo = self.gpu.halo(v)
             N.check(self.ctx.lib.emhd_jv(self.ctx.sync_stream(), D.ptr(self.a), D.ptr(self.a_halo),
                                          D.ptr(self.f_a), D.ptr(v), D.ptr(v_halo), D.ptr(vnorm_dev),
@@ -162,7 +162,7 @@ class FdJacobianOperator(LinearOperator):
         if self.gpu is None:
             out = self.apply_device(vd)
             return D.to_host(out) if host else out
-        vh = self.gpu.halo(vd)
+        vh = None if self.gpu.defer_halo else self.gpu.halo(vd)
         scal = self._scr.dev[0:2]
         self.vnorm_into(vd, scal)
         out = self.apply_device(vd, vnorm_dev=scal, v_halo=vh)

@@ -274,7 +274,8 @@ class _Process:
         # slab ranks with symmetric memory: w's edge rows are pushed into the neighbours'
         # halo buffers by the update pass itself (emhd_update_push), no P2P exchange per Jv
         self.push = None
-        if engine.fused and layout is not None and layout.distributed:
+        native = engine.fused and getattr(engine.gpu, "native", False)
+        if engine.fused and layout is not None and layout.distributed and not native:
             g = engine.gpu
             if "_push_halo" not in g.__dict__:
                 g._push_halo = PushHalo.create(g.layout, g.comm)
@@ -298,7 +299,8 @@ class _Process:
                                          D.ptr(self.beta_dev), self.naug), "div_scalar")
         self._vm_ready = 1
         # single-rank fused engine: one C call per iteration (emhd_arnoldi_iter)
-        self.fast = FAST_DRIVER and engine.fused and (layout is None or not layout.distributed)
+        # slab ranks whose collectives live in the library (slab.NativeComm) keep it too
+        self.fast = FAST_DRIVER and engine.fused and (layout is None or not layout.distributed or native)
         if self.fast:
             E = engine
             A = N.ArnoldiArgs()
@@ -318,6 +320,7 @@ class _Process:
             A.eta, A.reorth = self.eta, D.ptr(self.reorth)
             # re-projection dots predicted from the previous decision (fast path only)
             A.md2 = D.ptr(self.md2) if PREDICT_REPROJECTION else None
+            A.a_halo = D.ptr(E.jop.a_halo)
             self._args = A
             self._args_ref = D.ctypes_byref(A)
 
@@ -355,7 +358,7 @@ class _Process:
             a, ah, fa = E.jop.a, E.jop.a_halo, E.jop.f_a
             if j == 0:
                 v = self.V[0]
-                vh = E.gpu.halo(v[:self.n_top])
+                vh = None if E.gpu.defer_halo else E.gpu.halo(v[:self.n_top])
                 N.check(self.lib.emhd_norms(h, D.ptr(v), 0, self.n_top, D.ptr(E._vn)), "norms")
                 if self.layout is not None and self.layout.distributed:
                     self.comm.allreduce_max(E._vn[1:2])
@@ -693,7 +696,7 @@ class _Process:
         """Iterations to queue behind a batch of residual checks run on the side stream: about
         one small dense exponential's worth of Arnoldi work (0 on very large grids, where one
         iteration outlasts it, and on the per-kernel / multi-rank paths)."""
-        if not self.fast:
+        if not self.fast or (self.layout is not None and self.layout.distributed):
             return 0
         env = os.environ.get("EMHD_LOOKAHEAD")
         if LOOKAHEAD_OVERRIDE is not None:

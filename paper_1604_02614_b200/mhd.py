@@ -195,6 +195,17 @@ class GpuRhs:
         self._send = None
         if L.distributed:
             self._send = torch.empty(halo_shape(grid.ny), dtype=D.F64, device=D.device())
+        # slab collectives inside the library (slab.NativeComm): the stencil entry points then
+        # exchange the halo of the vector they perturb themselves, overlapped with the interior
+        self.native = bool(getattr(self.comm, "native", False)) and L.distributed
+        if self.native:
+            self.comm.attach(self.ctx)
+
+    @property
+    def defer_halo(self):
+        """True when hot-path callers should pass no halo and let the library exchange it
+        (overlapped with the stencil's interior rows)."""
+        return self.native
 
     # -- halos -------------------------------------------------------------
     def halo(self, x, out=None):
@@ -202,9 +213,12 @@ class GpuRhs:
         if not self.layout.distributed:
             return None
         h = self.ctx.sync_stream()
-        N.check(self.ctx.lib.emhd_pack_edges(h, D.ptr(x), D.ptr(self._send)), "pack_edges")
         if out is None:
             out = torch.zeros(halo_shape(self.grid.ny), dtype=D.F64, device=D.device())
+        if self.native:
+            N.check(self.ctx.lib.emhd_halo_exchange(h, D.ptr(x), D.ptr(out)), "halo_exchange")
+            return out
+        N.check(self.ctx.lib.emhd_pack_edges(h, D.ptr(x), D.ptr(self._send)), "pack_edges")
         self.comm.exchange(self._send, out)
         return out
 
@@ -222,7 +236,7 @@ class GpuRhs:
         yd = D.to_device(y).reshape(-1)
         if yd.numel() != self.n:
             raise ValueError(f"state has {yd.numel()} entries, expected {self.n}")
-        yh = self.halo(yd)
+        yh = None if self.defer_halo else self.halo(yd)
         out = torch.empty_like(yd)
         self.launch(yd, out, yh)
         if self.check:

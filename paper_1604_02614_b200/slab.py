@@ -15,6 +15,7 @@ SUM / MAX all-reduces of a few doubles per Arnoldi pass.
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -37,7 +38,9 @@ class SlabLayout:
 
     @property
     def distributed(self):
-        return self.size > 1
+        # any EXTERNAL side: halos come from a neighbour (a rank may be its own neighbour: the
+        # periodic ring of one, used to exercise the slab path on a single GPU)
+        return self.size > 1 or self.lo_neighbor >= 0 or self.hi_neighbor >= 0
 
     @property
     def n_local(self):
@@ -69,6 +72,13 @@ def make_layout(nx_global, ny, bc_x, rank=0, size=1):
     return SlabLayout(nx_global, ny, rank, size, counts[rank], offs[rank], bc_lo, bc_hi, lo_nb, hi_nb)
 
 
+def make_ring_layout(nx, ny):
+    """One rank owning a periodic x-ring with itself as both neighbours: every slab-path code
+    path (EXTERNAL boundaries, halo exchange, all-reduces) on one GPU, bit-identical to the
+    periodic single-domain result."""
+    return SlabLayout(nx, ny, 0, 1, nx, 0, EXTERNAL, EXTERNAL, 0, 0)
+
+
 class Comm:
     """Halo exchange and small all-reduces for one slab layout."""
 
@@ -87,6 +97,10 @@ class Comm:
             return recvbuf
         s = sendbuf.view(2, -1)
         r = recvbuf.view(2, -1)
+        if L.size == 1:                       # ring of one: this rank is both neighbours
+            r[0].copy_(s[1])
+            r[1].copy_(s[0])
+            return recvbuf
         # Two ordered phases so that P2P matching (in posting order per peer
         # pair, no tags) stays correct when lo and hi neighbour coincide (P=2):
         # phase 1 shifts top rows upwards, phase 2 bottom rows downwards.
@@ -105,22 +119,22 @@ class Comm:
         return recvbuf
 
     def allreduce_sum(self, t):
-        if self.layout.distributed:
+        if self.layout.size > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 
     def allreduce_max(self, t):
-        if self.layout.distributed:
+        if self.layout.size > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return t
 
     def allreduce_min(self, t):
-        if self.layout.distributed:
+        if self.layout.size > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
         return t
 
     def barrier(self):
-        if self.layout.distributed:
+        if self.layout.size > 1:
             dist.barrier(group=self.group)
 
 
@@ -198,3 +212,97 @@ class PushHalo:
         dist.barrier(group=comm.group)
         return PushHalo(buf.view(halo_shape(layout.ny)), None if lo is None else lo.data_ptr(),
                         None if hi is None else hi.data_ptr(), (hdl, lo, hi))
+
+
+class NativeComm(Comm):
+    """Slab collectives issued by libemhd itself (emhd_comm_init_nccl / _host).
+
+    Once attached to the rank's context, the Arnoldi driver keeps its one C call per iteration
+    on slab ranks: the dot and norm all-reduces are stream-ordered NCCL collectives issued from
+    C (no host sync, no Python between kernels) and the halo of the vector a stencil perturbs is
+    exchanged on a second stream while the stencil's interior rows run.  ``transport``:
+    ``"nccl"`` (one process per GPU; the two 128-byte unique ids travel by a torch.distributed
+    broadcast) or ``"host"`` (several ranks on one GPU; collectives stage through pinned host
+    memory and this object's torch.distributed group — gloo in the tests).
+    """
+
+    native = True
+
+    def __init__(self, layout, group=None, transport="nccl"):
+        super().__init__(layout, group)
+        if transport not in ("nccl", "host"):
+            raise ValueError("transport must be 'nccl' or 'host'")
+        self.transport = transport
+        self.ctx = None
+        self._cb = None
+
+    def attach(self, ctx):
+        """Collective over the group: create this rank's communicator inside ``ctx``."""
+        import ctypes
+        from . import _native as N
+        L = self.layout
+        if self.transport == "nccl":
+            ids = None
+            if L.rank == 0:
+                a, b = ctypes.create_string_buffer(128), ctypes.create_string_buffer(128)
+                N.check(ctx.lib.emhd_nccl_unique_id(a), "nccl_unique_id")
+                N.check(ctx.lib.emhd_nccl_unique_id(b), "nccl_unique_id")
+                ids = [a.raw, b.raw]
+            if L.size > 1:
+                box = [ids]
+                src = 0 if self.group is None else dist.get_global_rank(self.group, 0)
+                dist.broadcast_object_list(box, src=src, group=self.group)
+                ids = box[0]
+            N.check(ctx.lib.emhd_comm_init_nccl(ctx.h, L.size, L.rank, L.lo_neighbor, L.hi_neighbor,
+                                                ids[0], ids[1]), "comm_init_nccl")
+        else:
+            def ar(user, buf, n, op):
+                try:
+                    t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,)))
+                    red = {0: dist.ReduceOp.SUM, 2: dist.ReduceOp.MAX, 3: dist.ReduceOp.MIN}[op]
+                    if L.size > 1:
+                        dist.all_reduce(t, op=red, group=self.group)
+                    return 0
+                except Exception:
+                    return 1
+
+            def ex(user, send, recv, n_side):
+                try:
+                    s_ = torch.from_numpy(np.ctypeslib.as_array(send, shape=(2 * n_side,))).clone()
+                    r_ = torch.from_numpy(np.ctypeslib.as_array(recv, shape=(2 * n_side,)))
+                    if L.size == 1:           # ring of one: my top rows are my lo halo
+                        r_[:n_side].copy_(s_[n_side:])
+                        r_[n_side:].copy_(s_[:n_side])
+                    else:
+                        Comm.exchange(self, s_, r_)
+                    return 0
+                except Exception:
+                    return 1
+            self._cb = (N.HostAllreduceFn(ar), N.HostExchangeFn(ex))     # keep the thunks alive
+            N.check(ctx.lib.emhd_comm_init_host(ctx.h, L.size, L.rank, L.lo_neighbor, L.hi_neighbor,
+                                                self._cb[0], self._cb[1], None), "comm_init_host")
+        self.ctx = ctx
+
+    def _c(self, t, op):
+        from . import _native as N
+        if self.ctx is None or not t.is_cuda:
+            return None
+        N.check(self.ctx.lib.emhd_allreduce(self.ctx.sync_stream(), t.data_ptr(), t.numel(), op),
+                "allreduce")
+        return t
+
+    def allreduce_sum(self, t):
+        from . import _native as N
+        return self._c(t, N.OP_SUM) if t.is_cuda and self.ctx is not None else super().allreduce_sum(t)
+
+    def allreduce_max(self, t):
+        from . import _native as N
+        return self._c(t, N.OP_MAX) if t.is_cuda and self.ctx is not None else super().allreduce_max(t)
+
+    def allreduce_min(self, t):
+        from . import _native as N
+        return self._c(t, N.OP_MIN) if t.is_cuda and self.ctx is not None else super().allreduce_min(t)
+
+    def barrier(self):
+        if self.layout.size > 1:
+            dist.barrier(group=self.group)

@@ -54,7 +54,7 @@ def phi_residual_bench():
     from paper_1604_02614_b200.fdjac import _generic_ctx
     rng = np.random.default_rng(1)
     out = []
-    for m in (20, 40, 60, 84, 100):
+    for m in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else "10,20,30,40,60,84,100".split(","))]:
         for scale in (1.0, 30.0):
             H = np.triu(rng.standard_normal((m + 1, m)), -1) * scale / np.sqrt(m)
             Hd = D.to_device(H)
