@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--quick", action="store_true", help="timed region only (for ncu)")
     p.add_argument("--no-trajectory", action="store_true", help="skip the config-1 trajectory")
     p.add_argument("--no-two-pass", action="store_true", help="skip the always-two-pass record")
+    p.add_argument("--comm", default="native", choices=["native", "python"],
+                   help="slab collectives: inside libemhd (C driver) or torch.distributed")
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the config-3 trajectory and the config-4 4096^2 Arnoldi line")
     return p.parse_args()
@@ -84,6 +86,9 @@ def config_dict(args, world):
         "grid": [args.n, args.n], "krylov_dim": args.m, "jv_products": args.jv,
         "fields": 8, "mu": 1e-3, "eta": 1e-3, "kappa": 1e-3, "bc": "periodic/periodic",
         "decomposition": f"x-slabs x{world}", "parallelism": f"slab{world}",
+        "slab_collectives": ("libemhd NCCL (C driver, halo exchange overlapped with interior rows)"
+                             if getattr(args, "comm", "native") == "native" else "torch.distributed")
+                            if world > 1 else None,
         "l2": "inputs larger than L2 (64 MiB vectors, 2.7 GB basis); no flush needed",
         "orthogonalisation": "classical Gram-Schmidt, second pass when ||w1|| < eta ||w|| "
                              "(selective re-orthogonalisation, eta = %.4g; 0 = always two passes; "
@@ -215,12 +220,14 @@ def run_ours(args):
     import paper_1604_02614_b200 as P
     from paper_1604_02614_b200 import _native as N
     from paper_1604_02614_b200.mhd import local_rows
-    from paper_1604_02614_b200.slab import Comm, make_layout
+    from paper_1604_02614_b200.slab import Comm, NativeComm, make_layout
 
     g, prm, U, v = make_inputs(args)
     bc = P.BoundaryPolicy("periodic", "periodic")
     layout = make_layout(g.nx, g.ny, bc.x, rank, world)
-    comm = Comm(layout)
+    # slab ranks: collectives inside the library (C driver, stream-ordered NCCL all-reduces,
+    # halo exchange overlapped with the interior rows); --comm python: torch.distributed calls
+    comm = NativeComm(layout) if (world > 1 and args.comm == "native") else Comm(layout)
     f = P.make_rhs(prm, g, bc, layout=layout, comm=comm)
     a_host = local_rows(U.reshape(-1), g, layout)
     v_host = local_rows(v, g, layout)

@@ -44,6 +44,7 @@ struct emhd_ctx {
   cudaEvent_t ev_x = nullptr, ev_halo = nullptr;
   double* hsend = nullptr;                    // [2][8][2][ny] edge rows of the exchanged array
   double* hrecv = nullptr;                    // [2][8][2][ny] halo the stencil reads
+  double* red = nullptr;                      // [max_vectors + 8] reduction scratch (slab path)
   // per-launch profiling (emhd_profile): CUDA events around every launch of the Arnoldi path
   struct ProfRec { int kind; cudaEvent_t e0, e1; double bytes; const double* gate[2]; };
   bool prof = false;
@@ -179,6 +180,7 @@ extern "C" int emhd_ctx_destroy(emhd_ctx* c) {
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   cudaFree(c->hsend);
   cudaFree(c->hrecv);
+  cudaFree(c->red);
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->cancel_host) cudaFreeHost(c->cancel_host);
   delete c;
@@ -317,6 +319,7 @@ static int comm_buffers(emhd_ctx* c) {
   const size_t n = (size_t)2 * NF * 2 * c->g.ny;
   int rc = cerr(cudaMalloc(&c->hsend, n * sizeof(double)));
   if (!rc) rc = cerr(cudaMalloc(&c->hrecv, n * sizeof(double)));
+  if (!rc) rc = cerr(cudaMalloc(&c->red, (size_t)(c->max_vectors + 8) * sizeof(double)));
   if (!rc) rc = cerr(cudaMemset(c->hrecv, 0, n * sizeof(double)));
   if (!rc) rc = cerr(cudaStreamCreateWithFlags(&c->halo_stream, cudaStreamNonBlocking));
   if (!rc) rc = cerr(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
@@ -905,7 +908,14 @@ struct emhd_arnoldi_args_s {
 // perturbs exchanged while the stencil's interior rows run.  The selective re-orthogonalisation
 // decision is taken by a one-CTA kernel from the all-reduced sums, so every rank takes the same
 // branch; the pass-2 launches test its gate, the pass-2 norm all-reduce is issued regardless
-// (unused when skipped).  No prediction of the re-projection dots (pass 1 always computes them).
+// (unused when skipped).  The re-projection dots are predicted as on one rank (args.md2): pass 1
+// skips them after two iterations without a second pass, and a gated multi-dot (plus its
+// all-reduce, issued regardless) supplies them on a misprediction.
+__global__ void gated_copy_kernel(const double* src, double* dst, int n, const double* gate) {
+  if (*gate != 0.0) return;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
 static int arnoldi_iter_slab(emhd_ctx* c, const emhd_arnoldi_args_s* A, int j) {
   double* out = (j % 2 == 0) ? A->w0 : A->w1;
   const double W = 8.0 * (double)A->n_top;
@@ -948,18 +958,39 @@ static int arnoldi_iter_slab(emhd_ctx* c, const emhd_arnoldi_args_s* A, int j) {
     rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream));
   }
   if (!rc) rc = comm_rc(slabcomm_allreduce(c->comm, A->d1, nv + 1, EMHD_OP_SUM, c->stream));
-  // w -= V h1 with the re-projection dots h2 = V^T w1, ||w1||^2 (SUM) and max|w1_top| (MAX)
+  // w -= V h1 with the re-projection dots h2 = V^T w1 (unless predicted away), ||w1||^2 (SUM) and
+  // max|w1_top| (MAX)
+  Reorth r1{};
+  double* md2 = nullptr;
+  const double* predict = nullptr;
+  if (selective && A->md2) {
+    md2 = A->md2 + j;
+    predict = j > 1 ? A->reorth + (j - 2) : nullptr;
+    r1.predict = predict;
+  }
   if (!rc) {
     ProfScope ps(c, EMHD_K_UPDATE, (nv + 2) * vb);
     rc = cerr(launch_update(out, A->V, A->ldv, nv, A->d1, A->len_upd, A->len_dot, A->n_top, 0, k,
-                            A->d2, c->stream, F, nullptr, Reorth{}));
+                            A->d2, c->stream, F, nullptr, r1));
   }
   if (!rc) rc = comm_rc(slabcomm_allreduce_sum_max(c->comm, A->d2, nv + 1, 1, c->stream));
   if (rc) return rc;
   const double* gate = nullptr;
   if (selective) {
     gate = A->reorth + j;
-    rc = cerr(launch_reorth_decide(F, A->d2, nv, A->eta * A->eta, A->reorth + j, c->stream));
+    rc = cerr(launch_reorth_decide(F, A->d2, nv, A->eta * A->eta, A->reorth + j, c->stream, md2, predict));
+    if (!rc && md2) {
+      // misprediction: pass 2 needed but its dots were not computed (gate md2 == 0): a gated
+      // multi-dot into scratch, its all-reduce (issued on every rank regardless of the gate),
+      // then the gated copy into h2 (the all-reduced d2 must not be reduced twice)
+      ProfScope ps(c, EMHD_K_MULTIDOT2, (nv + 1) * vb, md2);
+      rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 0, k, c->red, c->stream, nullptr, md2));
+      if (!rc) rc = comm_rc(slabcomm_allreduce(c->comm, c->red, nv, EMHD_OP_SUM, c->stream));
+      if (!rc) {
+        gated_copy_kernel<<<1, 128, 0, c->stream>>>(c->red, A->d2, nv, md2);
+        rc = cerr(cudaGetLastError());
+      }
+    }
     if (rc) return rc;
   }
   // pass 2 (gated): w -= V h2 ; {||w||^2, max|w_top|} all-reduced ; column bookkeeping

@@ -375,8 +375,10 @@ cudaError_t launch_push_edges(const double* w, const HaloPush& H, const double* 
 }
 
 __global__ void reorth_decide_kernel(const FinishArgs F, const double* r, int nvec, double eta2,
-                                     double* gate) {
-  reorth_decide(F, r, nvec, eta2, gate);
+                                     double* gate, double* gate_md2, const double* predict) {
+  // reprojected: the pass-1 update computed the re-projection dots (same test as its kernel)
+  const bool reproj = !(predict && predict[0] != 0.0 && predict[1] != 0.0);
+  reorth_decide(F, r, nvec, eta2, gate, gate_md2, reproj);
 }
 
 // out = {sum x^2 over len_sum, max|x| over len_max}
@@ -556,8 +558,8 @@ cudaError_t launch_arnoldi_finish(const double* h1, const double* h2, const doub
 }
 
 cudaError_t launch_reorth_decide(FinishArgs fin, const double* r, int nvec, double eta2, double* gate,
-                                 cudaStream_t s) {
-  reorth_decide_kernel<<<1, 128, 0, s>>>(fin, r, nvec, eta2, gate);
+                                 cudaStream_t s, double* gate_md2, const double* predict) {
+  reorth_decide_kernel<<<1, 128, 0, s>>>(fin, r, nvec, eta2, gate, gate_md2, predict);
   return cudaGetLastError();
 }
 

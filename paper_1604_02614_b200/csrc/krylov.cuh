@@ -57,7 +57,7 @@ cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, c
                           const double* skip = nullptr, Reorth ro = Reorth{});
 cudaError_t launch_push_edges(const double* w, const HaloPush& H, const double* gate, cudaStream_t s);
 cudaError_t launch_reorth_decide(FinishArgs fin, const double* r, int nvec, double eta2, double* gate,
-                                 cudaStream_t s);
+                                 cudaStream_t s, double* gate_md2 = nullptr, const double* predict = nullptr);
 cudaError_t launch_gate(const unsigned long long* cancel, unsigned gen, int j, double* gate, cudaStream_t s);
 cudaError_t launch_evals_discount(const double* evals, int count, DevStatus* st, cudaStream_t s);
 cudaError_t launch_update_push(double* w, const double* V, long long ldv, int nvec, const double* h,

@@ -17,7 +17,7 @@ struct UniqueId { char internal[128]; };
 typedef void* Comm;
 typedef int Result;
 enum { Float64 = 8 };
-enum { Sum = 0, Max = 2 };
+enum { Sum = 0, Max = 2, Min = 3 };
 
 struct Api {
   bool ok = false;
@@ -153,18 +153,14 @@ static int host_allreduce(SlabComm* c, double* buf, int n, int op, cudaStream_t 
 
 int slabcomm_allreduce(SlabComm* c, double* buf, int n, int op, cudaStream_t s) {
   if (!c || n <= 0) return 0;
-  if (c->nranks == 1 && !c->host) {
-    // one rank: the reduction is the identity (NCCL would copy in place)
-    return 0;
-  }
   if (c->host) return host_allreduce(c, buf, n, op, s);
   nccl::Api& a = nccl::api();
-  return nccl::check(a.allReduce(buf, buf, (size_t)n, nccl::Float64, op == 2 ? nccl::Max : nccl::Sum,
-                                 c->reduce, s), "AllReduce");
+  const int nop = op == 2 ? nccl::Max : (op == 3 ? nccl::Min : nccl::Sum);
+  return nccl::check(a.allReduce(buf, buf, (size_t)n, nccl::Float64, nop, c->reduce, s), "AllReduce");
 }
 
 int slabcomm_allreduce_sum_max(SlabComm* c, double* buf, int n_sum, int n_max, cudaStream_t s) {
-  if (!c || c->nranks == 1) return 0;
+  if (!c) return 0;
   if (c->host) {
     int rc = n_sum > 0 ? host_allreduce(c, buf, n_sum, 0, s) : 0;
     if (!rc && n_max > 0) rc = host_allreduce(c, buf + n_sum, n_max, 2, s);

@@ -1016,8 +1016,10 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
     P.tma = sel.bulk && (P.ny % 2 == 0) && al(P.a) && al(P.a_halo) &&
             (MODE == MODE_RHS || (al(P.v) && al(P.v_halo)));
   }
-  if (sel.kernel == 2) {
-    if (used) { *used = sel; used->kernel = 2; used->rows_per_cta = 0; used->strip = 0; used->bulk = 0; }
+  // the edge-row launch of a halo-overlapped slab stencil (4 output rows) always takes 2D tiles:
+  // a marching CTA would spend 6 dependent row steps on 2 output rows
+  if (sel.kernel == 2 || (P.rows_mode == 2 && sel.kernel == 0)) {
+    if (used) { *used = sel; used->kernel = 2; used->rows_per_cta = P.rows_mode == 2 ? 2 : 0; used->strip = 0; used->bulk = 0; }
     return launch_tile<MODE, AUG, FXY>(P, s);
   }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

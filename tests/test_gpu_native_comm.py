@@ -69,8 +69,9 @@ def test_ring_of_one_matches_single_domain(P, transport):
                 assert f.ctx.last_stencil()["rows_per_cta"] == 2     # the edge-row launch ran last
         f.ctx.stencil_path(kernel=0)
 
-    # Arnoldi through the C slab driver == the Python per-kernel slab path (same kernels, same
-    # collectives) bit for bit, and the reference fixture to the FD bar
+    # Arnoldi through the C slab driver == the single-domain C driver bit for bit (same kernels,
+    # same predicted re-projection, 1-rank reductions), the Python per-kernel slab path and the
+    # reference fixture to the FD bar
     zk = golden("krylov_mhd.npz")
     gt, pt = zk["grid"], zk["params"]
     g = P.Grid2D(int(gt[0]), int(gt[1]), gt[2], gt[3], gt[4], gt[5])
@@ -79,8 +80,9 @@ def test_ring_of_one_matches_single_domain(P, transport):
     ring = make_ring_layout(g.nx, g.ny)
     fn = P.make_rhs(prm, g, bc, layout=ring, comm=NativeComm(ring, transport=transport))
     fp = P.make_rhs(prm, g, bc, layout=ring, comm=Comm(ring))
+    fs = P.make_rhs(prm, g, bc)
     out = []
-    for f in (fn, fp):
+    for f in (fn, fs, fp):
         op = P.FdJacobianOperator(f, zk["a"], zk["fa"])
         b = P.arnoldi(op, zk["v"], 12)
         out.append(b)
@@ -190,3 +192,26 @@ def test_host_transport_ranks_on_one_gpu_match_reference(size):
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (one NCCL rank per GPU)")
 def test_nccl_ranks_on_two_gpus_match_reference():
     mp.spawn(_worker, args=(2, _port(), "nccl", torch.cuda.device_count()), nprocs=2, join=True)
+
+
+def test_ring_of_one_predicted_reprojection_both_branches(P):
+    """Config 0's state drives both selective re-orthogonalisation branches (and mispredicted
+    re-projections): the slab C driver on a ring of one equals the single-domain C driver bit
+    for bit over 40 iterations (decision taken by a separate kernel from the all-reduced sums,
+    gated multi-dot into scratch + all-reduce + gated copy on a misprediction)."""
+    from paper_1604_02614_b200.slab import NativeComm, make_ring_layout
+    g = P.ReconnectionSpec().grid(64, 64)
+    prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    bc = P.default_bc("reconnection")
+    y0 = P.reconnection_ic(g, params=prm).reshape(-1)
+    ring = make_ring_layout(64, 64)
+    res = []
+    for f in (P.make_rhs(prm, g, bc), P.make_rhs(prm, g, bc, layout=ring, comm=NativeComm(ring))):
+        yd = dev(y0)
+        op = P.FdJacobianOperator(f, yd)
+        b = P.arnoldi(op, f(yd), 40)
+        res.append((b.H.cpu().numpy(), b.V.cpu().numpy(), b.second_pass.cpu().numpy()))
+    sp = res[0][2]
+    assert 0 < sp.sum() < len(sp)
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][2], res[1][2])
