@@ -331,20 +331,29 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
 #undef QV
 }
 
+// raw input rows in flight per CTA: row r+NRAW is requested while row r is consumed.  Two for
+// the Arnoldi-loop stencil (MODE_JVN: 2 CTAs/SM with one more row of prefetch beat 3 CTAs/SM
+// with one, 82.7 vs 89.4 us at 1024^2; three rows: 93.6 us), one for RHS / Jv (3 CTAs/SM; Jv
+// 69 us with one, 72 with two)
+template <int MODE>
+constexpr int nraw() { return MODE == MODE_JVN ? 2 : 1; }
+
 template <int TY, int MODE, bool AUG, int FXY>
 __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilParams P) {
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
   extern __shared__ double smem[];
   // rings sized so ONE barrier per row step suffices (see the loop): primitives 4 rows,
-  // y-fluxes 2 rows, thread-private centre quantities 2 rows, one raw row in flight;
-  // x-fluxes live in registers of the column's own thread.  ~72 KB at TY=128: 3 CTAs/SM
+  // y-fluxes 2 rows, thread-private centre quantities 2 rows, NRAW raw rows in flight;
+  // x-fluxes live in registers of the column's own thread.  ~72 KB at TY=128 with one raw
+  // row (3 CTAs/SM), ~90 KB with two (2 CTAs/SM)
   double* qring = smem;                             // [4][NQ][QW]
   double* gyring = qring + 4 * NQ * QW;             // [2][NF][GYW]
   double* cring = gyring + 2 * NF * GYW;            // [2][NC][QW]
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  double* rawring = cring + 2 * NC * QW;            // [NARR*NF][QW] raw row in flight
-  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NARR * NF * QW);
+  constexpr int NRAW = nraw<MODE>();
+  double* rawring = cring + 2 * NC * QW;            // [NRAW][NARR*NF][QW] raw rows in flight
+  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NRAW * NARR * NF * QW);
 
   pdl_sync();
   const int t = threadIdx.x;
@@ -479,24 +488,31 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
     // interior strips (no y-ghost columns) stream whole row segments with bulk async copies
     // issued by thread 0 (tracked by one mbarrier); edge strips keep per-thread cp.async
     const bool bulk = P.tma && j0 >= 2 && j0 + TY + 2 <= P.ny;
+    constexpr int SLOT = NARR * NF * QW;     // doubles per raw row slot
     if (bulk) {
       if (t == 0) {
-        mbar_init(rbar, 1);
+        for (int k = 0; k < NRAW; ++k) mbar_init(rbar + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        fetch_row_bulk<MODE, QW>(P, row_ref(P, i0), j0 - 2, rawring, rbar);
+        for (int k = 0; k < NRAW && i0 + k <= i1 + 1; ++k)
+          fetch_row_bulk<MODE, QW>(P, row_ref(P, i0 + k), j0 - 2, rawring + k * SLOT, rbar + k);
       }
       __syncthreads();
     } else {
       // per-thread cp.async: every thread consumes only the cells it copied itself
-      const RowRef R = row_ref(P, i0);
-      if (okm) fetch_async<MODE, QW>(P, R, jm, cmain, rawring);
-      if (oke) fetch_async<MODE, QW>(P, R, je, cextra, rawring);
-      cp_commit();
+      for (int k = 0; k < NRAW; ++k) {
+        if (i0 + k <= i1 + 1) {
+          const RowRef R = row_ref(P, i0 + k);
+          if (okm) fetch_async<MODE, QW>(P, R, jm, cmain, rawring + k * SLOT);
+          if (oke) fetch_async<MODE, QW>(P, R, je, cextra, rawring + k * SLOT);
+        }
+        cp_commit();
+      }
     }
     for (int r = i0; r <= i1 + 1; ++r) {
-      double* sraw = rawring;
-      if (bulk) mbar_wait(rbar, (r - i0) & 1);
-      else cp_wait<0>();                     // row r has landed
+      const int rk = r - i0;
+      double* sraw = rawring + (rk % NRAW) * SLOT;
+      if (bulk) mbar_wait(rbar + rk % NRAW, (unsigned)((rk / NRAW) & 1));
+      else cp_wait<NRAW - 1>();              // row r has landed (later rows may be in flight)
       // ---- primitives of row r
       {
         const RowRef Rr = row_ref(P, r);
@@ -528,8 +544,8 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
       // refill the consumed raw row with row r+1 (each thread its own cells; the bulk path
       // refills after the barrier below, once every thread has consumed the row)
       if (!bulk) {
-        if (r + 1 <= i1 + 1) {
-          const RowRef R1 = row_ref(P, r + 1);
+        if (r + NRAW <= i1 + 1) {
+          const RowRef R1 = row_ref(P, r + NRAW);
           if (okm) fetch_async<MODE, QW>(P, R1, jm, cmain, sraw);
           if (oke) fetch_async<MODE, QW>(P, R1, je, cextra, sraw);
         }
@@ -542,10 +558,10 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
       // row r-3 (last read by the outputs of row r-3, previous step); centre quantities
       // are private to their thread.
       __syncthreads();
-      if (bulk && t == 0 && r + 1 <= i1 + 1) {
+      if (bulk && t == 0 && r + NRAW <= i1 + 1) {
         // generic-proxy reads of the row (before the barrier) precede the async-proxy refill
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        fetch_row_bulk<MODE, QW>(P, row_ref(P, r + 1), j0 - 2, sraw, rbar);
+        fetch_row_bulk<MODE, QW>(P, row_ref(P, r + NRAW), j0 - 2, sraw, rbar + rk % NRAW);
       }
       // ---- fluxes of row rf = r - 1
       const int rf = r - 1;
@@ -1006,8 +1022,9 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
                             StencilPath* used) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NARR * NF * QW) +
-                    sizeof(unsigned long long);
+  constexpr int NRAW = nraw<MODE>();
+  const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NRAW * NARR * NF * QW) +
+                    NRAW * sizeof(unsigned long long);
   auto k = stencil_kernel<TY, MODE, AUG, FXY>;
   if ((long long)NF * P.nx * P.ny >= (1LL << 32)) return cudaErrorInvalidValue;   // 32-bit offsets
   {
