@@ -45,7 +45,7 @@ class ArnoldiArgs(ctypes.Structure):
 
 class StencilPath(ctypes.Structure):
     _fields_ = [("kernel", c_int), ("rows_per_cta", c_int), ("strip", c_int), ("bulk", c_int),
-                ("min_rows", c_int), ("tile_rows", c_int)]
+                ("min_rows", c_int), ("tile_rows", c_int), ("raw_rows", c_int)]
 
 
 STENCIL_AUTO, STENCIL_MARCHING, STENCIL_TILE = 0, 1, 2

@@ -229,15 +229,17 @@ extern "C" int emhd_l2_window(emhd_ctx* c, const void* base, long long bytes) {
 
 static void to_c(const StencilPath& a, emhd_stencil_path* b) {
   b->kernel = a.kernel; b->rows_per_cta = a.rows_per_cta; b->strip = a.strip; b->bulk = a.bulk;
-  b->min_rows = a.min_rows; b->tile_rows = a.tile_rows;
+  b->min_rows = a.min_rows; b->tile_rows = a.tile_rows; b->raw_rows = a.raw_rows;
 }
 
 extern "C" int emhd_set_stencil_path(emhd_ctx* c, const emhd_stencil_path* sel) {
   if (!c || !sel || sel->kernel < 0 || sel->kernel > 2 || sel->rows_per_cta < 0 || sel->min_rows < 1 ||
+      sel->raw_rows < 0 || sel->raw_rows > 2 ||
       (sel->strip != 0 && sel->strip != 32 && sel->strip != 64 && sel->strip != 128))
     return EMHD_ERR_ARG;
   c->path.kernel = sel->kernel; c->path.rows_per_cta = sel->rows_per_cta; c->path.strip = sel->strip;
   c->path.bulk = sel->bulk != 0; c->path.min_rows = sel->min_rows; c->path.tile_rows = sel->tile_rows;
+  c->path.raw_rows = sel->raw_rows;
   return EMHD_OK;
 }
 

@@ -331,14 +331,18 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
 #undef QV
 }
 
-// raw input rows in flight per CTA: row r+NRAW is requested while row r is consumed.  Two for
-// the Arnoldi-loop stencil (MODE_JVN: 2 CTAs/SM with one more row of prefetch beat 3 CTAs/SM
-// with one, 82.7 vs 89.4 us at 1024^2; three rows: 93.6 us), one for RHS / Jv (3 CTAs/SM; Jv
-// 69 us with one, 72 with two)
-template <int MODE>
-constexpr int nraw() { return MODE == MODE_JVN ? 2 : 1; }
+// raw input rows in flight per CTA (NR): row r+NR is requested while row r is consumed.  Two
+// (2 CTAs/SM, one more row of prefetch) pay for the Arnoldi-loop stencil (MODE_JVN) on grids of
+// up to ~1.5 M cells, where a CTA marches few rows: 1024^2 82.4 us vs 87.5 with one; from 2048^2
+// on one row at 3 CTAs/SM is faster (2048^2 303 vs 311 us, 4096^2 1233 vs 1348 us); three rows:
+// 1024^2 93.6 us.  RHS / Jv always one (Jv 1024^2 69 us vs 72).
+static bool two_raw_rows(int mode, const StencilParams& P, const StencilPath& sel) {
+  if (mode != MODE_JVN) return false;
+  if (sel.raw_rows == 1 || sel.raw_rows == 2) return sel.raw_rows == 2;
+  return (long long)P.nx * P.ny <= 1536LL * 1024;
+}
 
-template <int TY, int MODE, bool AUG, int FXY>
+template <int TY, int MODE, bool AUG, int FXY, int NR>
 __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilParams P) {
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
   double* gyring = qring + 4 * NQ * QW;             // [2][NF][GYW]
   double* cring = gyring + 2 * NF * GYW;            // [2][NC][QW]
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  constexpr int NRAW = nraw<MODE>();
+  constexpr int NRAW = NR;
   double* rawring = cring + 2 * NC * QW;            // [NRAW][NARR*NF][QW] raw rows in flight
   unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NRAW * NARR * NF * QW);
 
@@ -1017,15 +1021,14 @@ cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* 
   return cudaGetLastError();
 }
 
-template <int TY, int MODE, bool AUG, int FXY>
+template <int TY, int MODE, bool AUG, int FXY, int NRAW = 1>
 static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const StencilPath& sel,
                             StencilPath* used) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  constexpr int NRAW = nraw<MODE>();
   const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NRAW * NARR * NF * QW) +
                     NRAW * sizeof(unsigned long long);
-  auto k = stencil_kernel<TY, MODE, AUG, FXY>;
+  auto k = stencil_kernel<TY, MODE, AUG, FXY, NRAW>;
   if ((long long)NF * P.nx * P.ny >= (1LL << 32)) return cudaErrorInvalidValue;   // 32-bit offsets
   {
     // bulk copies need 16-byte aligned sources and sizes: even ny and aligned buffers
@@ -1080,6 +1083,9 @@ static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, int ns, 
   if (mode == MODE_JV)
     return aug ? launch_t<TY, MODE_JV, true, FXY>(P, ns, s, sel, used)
                : launch_t<TY, MODE_JV, false, FXY>(P, ns, s, sel, used);
+  if (two_raw_rows(mode, P, sel))
+    return aug ? launch_t<TY, MODE_JVN, true, FXY, 2>(P, ns, s, sel, used)
+               : launch_t<TY, MODE_JVN, false, FXY, 2>(P, ns, s, sel, used);
   return aug ? launch_t<TY, MODE_JVN, true, FXY>(P, ns, s, sel, used)
              : launch_t<TY, MODE_JVN, false, FXY>(P, ns, s, sel, used);
 }
@@ -1115,6 +1121,7 @@ StencilPath stencil_path_defaults() {
   p.bulk = env_int("EMHD_STENCIL_TMA", 1) != 0;
   p.min_rows = env_int("EMHD_MIN_ROWS", 2);
   p.tile_rows = env_int("EMHD_STENCIL_TILE_ROWS", 6);
+  p.raw_rows = env_int("EMHD_STENCIL_RAW_ROWS", 0);
   return p;
 }
 

@@ -215,9 +215,11 @@ def test_marching_kernel_all_modes_all_bcs(P, mi, spacing):
     rng = np.random.default_rng(100 + mi)
     U = rand_state(rng, nx, ny)
     prm = P.MhdParams(mu=2e-2, eta=1e-2, kappa=3e-2, b_half=bool(mi % 2))
-    for bx, by in itertools.product(BCS, BCS):
+    for k, (bx, by) in enumerate(itertools.product(BCS, BCS)):
         case = Case(P, g, prm, P.BoundaryPolicy(bx, by), U, seed=mi)
-        case.force(kernel=1, strip=m["strip"], rows_per_cta=m["rows_per_cta"], bulk=int(m["bulk"]))
+        # the normalised-Jv stencil with one and with two input rows staged ahead
+        case.force(kernel=1, strip=m["strip"], rows_per_cta=m["rows_per_cta"], bulk=int(m["bulk"]),
+                   raw_rows=1 + (k + mi) % 2)
         check_all_modes(case, (m, spacing, bx, by), expect_kernel=1)
         r = case.ran()
         assert r["strip"] == m["strip"] and r["rows_per_cta"] == m["rows_per_cta"]
