@@ -1,3 +1,5 @@
+#!/bin/bash
+# config-2 step (arnoldi m=40) at several grid sizes with the per-kernel table: bash tools/ab_sizes.sh
 for n in 4096 2048 1024 512; do
   echo "== n=$n"
   python bench.py --n $n --steps 3 --warmup 2 --jv 5 --no-two-pass --no-secondary --no-cpu-baseline --no-trajectory --no-e2e 2>/dev/null | python -c "
