@@ -196,6 +196,27 @@ __device__ __forceinline__ void fetch_row_bulk(const StencilParams& P, const Row
   }
 }
 
+// q[bidx[k]] for the augmented epilogue's B columns, selected with compile-time indices so the
+// coefficients stay in registers (a runtime index into q[] would put q in local memory)
+__device__ __forceinline__ void aug_coefs(const StencilParams& P, const double qv[5], double qb[5]) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double c = 0.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) c = (k < P.nb && P.bidx[k] == i) ? qv[i] : c;
+    qb[k] = c;
+  }
+}
+
+// top += sum_k B_k[idx] q[bidx[k]], k = 0 .. nb-1 in order (krylov.py:268-270, exact order)
+__device__ __forceinline__ double aug_add(const StencilParams& P, const double qb[5], unsigned long long idx,
+                                          double top) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    if (k < P.nb) top = __dadd_rn(top, __dmul_rn(__ldg(P.bcol[k] + idx), qb[k]));
+  return top;
+}
+
 // raw ring layout: [slot][array (a, v)][field][column slot]
 template <int MODE, int QW>
 __device__ __forceinline__ void fetch_async(const StencilParams& P, const RowRef& R, int jsrc, int c,
@@ -343,7 +364,7 @@ static bool two_raw_rows(int mode, const StencilParams& P, const StencilPath& se
 }
 
 template <int TY, int MODE, bool AUG, int FXY, int NR>
-__global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilParams P) {
+__global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(const StencilParams P) {
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
   extern __shared__ double smem[];
@@ -423,6 +444,8 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
       }
     }
   }
+  double qb[5];
+  aug_coefs(P, qv, qb);
 
   const int ncols_out = min(TY, P.ny - j0);
   const unsigned plane = (unsigned)P.nx * (unsigned)P.ny;   // field stride of out / fa / vout
@@ -438,11 +461,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
         for (int f = 0; f < NF; ++f) {
           const long long idx = o + (long long)f * P.nx * P.ny;
           double val = 0.0;
-          if (AUG) {
-            val = __dmul_rn(P.ch, 0.0);
-            for (int k = 0; k < P.nb; ++k)
-              val = __dadd_rn(val, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
-          }
+          if (AUG) val = aug_add(P, qb, (unsigned long long)idx, __dmul_rn(P.ch, 0.0));
           P.out[idx] = val;
           if (MODE == MODE_JVN) P.vout[idx] = div_const(__ldg(P.v + idx), hnext, rh);
         }
@@ -619,11 +638,7 @@ __global__ void __launch_bounds__(TY, 384 / TY) stencil_kernel(const StencilPara
             nfmask |= (((unsigned)__double2hiint(F) & 0x7ff00000u) + 0x00100000u) >> (31 - f) & (1u << f);
             const double df = __dsub_rn(F, fa_pre[f]);
             double jv = fsig ? div_const1(df, sigma, rsig) : div_const(df, sigma, rsig);   // fdjac.py:49
-            if (AUG) {
-              jv = __dmul_rn(P.ch, jv);
-              for (int k = 0; k < P.nb; ++k)
-                jv = __dadd_rn(jv, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
-            }
+            if (AUG) jv = aug_add(P, qb, idx, __dmul_rn(P.ch, jv));
             P.out[idx] = jv;
           }
         }
@@ -754,6 +769,8 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
     for (int k = 0; k < 5; ++k)
       if (k < P.p) qv[k] = MODE == MODE_JVN ? div_const(P.v[P.n_top + k], hnext, rh) : P.qsrc[k];
   }
+  double qb[5];
+  aug_coefs(P, qv, qb);
   int flag = 0;
   unsigned long long bad = ~0ull;
   const int ro = t / TT_C, co = t % TT_C;              // this thread's output cell
@@ -766,10 +783,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
       for (int f = 0; f < NF; ++f) {
         const unsigned idx = o + f * plane;
         double val = 0.0;
-        if (AUG) {
-          val = __dmul_rn(P.ch, 0.0);
-          for (int k = 0; k < P.nb; ++k) val = __dadd_rn(val, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
-        }
+        if (AUG) val = aug_add(P, qb, idx, __dmul_rn(P.ch, 0.0));
         P.out[idx] = val;
         if (MODE == MODE_JVN) P.vout[idx] = div_const(__ldg(P.v + idx), hnext, rh);
       }
@@ -837,10 +851,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
           nfmask |= (((unsigned)__double2hiint(F) & 0x7ff00000u) + 0x00100000u) >> (31 - f) & (1u << f);
           const double df = __dsub_rn(F, __ldg(P.fa + idx));
           double jv = fsig ? div_const1(df, sigma, rsig) : div_const(df, sigma, rsig);
-          if (AUG) {
-            jv = __dmul_rn(P.ch, jv);
-            for (int k = 0; k < P.nb; ++k) jv = __dadd_rn(jv, __dmul_rn(__ldg(P.bcol[k] + idx), qv[P.bidx[k]]));
-          }
+          if (AUG) jv = aug_add(P, qb, idx, __dmul_rn(P.ch, jv));
           P.out[idx] = jv;
         }
       }
