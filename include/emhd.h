@@ -207,6 +207,11 @@ int emhd_phi_small_batch(emhd_ctx* ctx, const double* H, long long ldh, const in
                          const double* host_scales, const double* brk_hist, const double* beta,
                          double* Y, long long ldy, double* res);
 
+/* Small dense exponentials of dimension >= n run on a thread-block cluster of 8 CTAs (products,
+ * norms and ell split by row blocks; 0 = never, every one on one CTA); process-wide; returns
+ * the previous threshold (default: EMHD_DENSE_CLUSTER_N, else 56). */
+int emhd_set_dense_cluster(int n);
+
 /* E = expm(A), n x n row-major device matrices; work: device scratch of n + 4 doubles.
  * Synchronous.  (scipy.linalg.expm as called by phi_dense, phifuncs.py:97,104) */
 int emhd_expm(emhd_ctx* ctx, const double* A, int n, double* E, double* work);

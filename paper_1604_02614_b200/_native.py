@@ -124,6 +124,7 @@ _SIGS = {
                                     c_vp]),
     "emhd_allreduce": (c_int, [c_vp, P, c_int, c_int]),
     "emhd_halo_exchange": (c_int, [c_vp, P, P]),
+    "emhd_set_dense_cluster": (c_int, [c_int]),
 }
 
 _lib = None

@@ -35,6 +35,9 @@ struct emhd_ctx {
   unsigned long long* cancel_host = nullptr;  // pinned source of its async updates
   const double* skip_next = nullptr;          // emhd_skip_next: gate of the next pass-2 launch
   bool l2win = false;                         // emhd_l2_window set on this context's stream
+  cudaStream_t l2win_stream = nullptr;        // the stream carrying the window
+  bool l2_limit_changed = false;              // this context raised the persisting-L2 limit
+  size_t l2_limit_prev = 0;                   // ... from this value (restored on destroy)
   StencilPath path{};                         // stencil launch selection (emhd_set_stencil_path)
   StencilPath last{};                         // what the last stencil launch ran
   // slab-rank collectives (emhd_comm_init_*): all-reduces on `stream`, halo exchange on
@@ -168,6 +171,16 @@ extern "C" int emhd_ctx_create(emhd_ctx** out, const emhd_geometry* g, const emh
 
 extern "C" int emhd_ctx_destroy(emhd_ctx* c) {
   if (!c) return EMHD_OK;
+  if (c->l2win) {
+    // remove the persisting window from the stream, release the persisting lines and give the
+    // device back its previous persisting-L2 limit: nothing outlives the context
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(c->l2win_stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+  }
+  if (c->l2_limit_changed) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->l2_limit_prev);
+  cudaGetLastError();
   cudaFree(c->partials);
   cudaFree(c->ticket);
   cudaFree(c->st);
@@ -211,7 +224,10 @@ extern "C" int emhd_l2_window(emhd_ctx* c, const void* base, long long bytes) {
     const size_t lim = (size_t)(bytes < maxpers ? bytes : maxpers);
     size_t cur = 0;
     rc = cerr(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-    if (!rc && cur != lim) rc = cerr(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+    if (!rc && cur != lim) {
+      if (!c->l2_limit_changed) { c->l2_limit_changed = true; c->l2_limit_prev = cur; }
+      rc = cerr(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+    }
     if (rc) return rc;
     v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
     v.accessPolicyWindow.num_bytes = (size_t)bytes;
@@ -222,7 +238,10 @@ extern "C" int emhd_l2_window(emhd_ctx* c, const void* base, long long bytes) {
     v.accessPolicyWindow.num_bytes = 0;
   }
   rc = cerr(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-  if (!rc) c->l2win = v.accessPolicyWindow.num_bytes > 0;
+  if (!rc) {
+    c->l2win = v.accessPolicyWindow.num_bytes > 0;
+    c->l2win_stream = c->stream;
+  }
   if (!rc && bytes == 0) rc = cerr(cudaCtxResetPersistingL2Cache());
   return rc;
 }
@@ -609,7 +628,7 @@ static int ensure_dense(emhd_ctx* c, size_t need) {
 }
 
 static void carve_dense(emhd_ctx* c, PhiSmallArgs& P, int S, size_t n) {
-  const size_t per = 11 * n * n + 5 * n + 64;
+  const size_t per = dense_per(n);
   for (int s = 0; s < S; ++s) {
     double* b = c->dense + per * s;
     size_t nn = n * n;
@@ -618,6 +637,7 @@ static void carve_dense(emhd_ctx* c, PhiSmallArgs& P, int S, size_t n) {
     for (int k = 0; k < 7; ++k) P.work[s].m[k] = b + (2 + k) * nn;
     P.work[s].m[7] = b + 9 * nn;     // n x 2n
     P.work[s].vec = b + 11 * nn;
+    P.work[s].part = b + 11 * nn + 5 * n + 64;
   }
 }
 
@@ -629,7 +649,7 @@ static int phi_small_impl(emhd_ctx* c, const double* H, long long ldh, int m, in
       (!host_scales && (!scales || !res_scale)) || !beta || !Y || !res)
     return EMHD_ERR_ARG;
   const size_t n = (size_t)m + order;
-  const size_t per = 11 * n * n + 5 * n + 64;
+  const size_t per = dense_per(n);
   int rc = ensure_dense(c, per * S);
   if (rc) return rc;
   PhiSmallArgs P;
@@ -659,7 +679,7 @@ extern "C" int emhd_phi_small_batch(emhd_ctx* c, const double* H, long long ldh,
     mmax = ms[s] > mmax ? ms[s] : mmax;
   }
   const size_t n = (size_t)mmax + order;
-  const size_t per = 11 * n * n + 5 * n + 64;
+  const size_t per = dense_per(n);
   int rc = ensure_dense(c, per * S);
   if (rc) return rc;
   PhiSmallArgs P;
@@ -684,6 +704,14 @@ extern "C" int emhd_phi_small_h(emhd_ctx* c, const double* H, long long ldh, int
   if (!host_scales) return EMHD_ERR_ARG;
   return phi_small_impl(c, H, ldh, m, order, S, nullptr, nullptr, scal, beta, Y, res, nullptr,
                         host_scales);
+}
+
+// Exponentials of dimension >= n run on a cluster of DENSE_CLUSTER CTAs (0: never); returns
+// the previous setting.  Process-wide (default EMHD_DENSE_CLUSTER_N, else 56).
+extern "C" int emhd_set_dense_cluster(int n) {
+  const int prev = dense_cluster_min_n();
+  set_dense_cluster_min_n(n);
+  return prev;
 }
 
 // E = expm(A) for an n x n device matrix (scratch: 4 doubles + n doubles in `work`)

@@ -85,27 +85,41 @@ __device__ void mm(double* C, const double* A, const double* B, int n, double* s
   else mm_tile<8, 4>(C, A, B, n, sA, sB);    // n > 128 loops over 128 x 128 tiles
 }
 
-// Column sums y[c] = sum_r w(r) |A[r][c]| (w = 1 or x[r]) with all threads: 16 row groups x
-// 32 column lanes (coalesced rows), per-lane partials combined in a fixed order.
+// Column sums y[c] = sum_r w(r) |A[r][c]| (w = 1 or x[r]) with all threads in ONE pass: the
+// DT threads cover (column, row group) pairs — G = DT / ceil32(n) row groups of coalesced
+// column lanes — and the per-group partials are combined in a fixed order (two barriers per
+// call instead of two per 32-column chunk: ell's 2m+1 dependent |A|-products are barrier-bound)
 __device__ void abs_colsums(const double* A, int n, const double* x, double* y, double* part) {
-  const int l = threadIdx.x & 31, g = threadIdx.x >> 5;
-  for (int c0 = 0; c0 < n; c0 += 32) {
-    const int c = c0 + l;
-    double s = 0.0;
-    if (c < n) {
-      if (x) for (int r = g; r < n; r += DT / 32) s += x[r] * fabs(A[r * n + c]);
-      else for (int r = g; r < n; r += DT / 32) s += fabs(A[r * n + c]);
-    }
-    part[g * 32 + l] = s;
-    __syncthreads();
-    if (g == 0 && c < n) {
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < DT / 32; ++q) t += part[q * 32 + l];
-      y[c] = t;
+  const int nc = (n + 31) & ~31;                  // columns padded to whole warps
+  if (nc > DT) {
+    // n > DT: chunks of DT columns, one row group each
+    for (int c0 = 0; c0 < n; c0 += DT) {
+      const int c = c0 + threadIdx.x;
+      if (c < n) {
+        double s = 0.0;
+        if (x) for (int r = 0; r < n; ++r) s += x[r] * fabs(A[r * n + c]);
+        else for (int r = 0; r < n; ++r) s += fabs(A[r * n + c]);
+        y[c] = s;
+      }
     }
     __syncthreads();
+    return;
   }
+  const int G = DT / nc;                          // row groups
+  const int c = threadIdx.x % nc, g = threadIdx.x / nc;
+  double s = 0.0;
+  if (g < G && c < n) {
+    if (x) for (int r = g; r < n; r += G) s += x[r] * fabs(A[r * n + c]);
+    else for (int r = g; r < n; r += G) s += fabs(A[r * n + c]);
+  }
+  if (g < G) part[g * nc + c] = s;
+  __syncthreads();
+  for (int cc = threadIdx.x; cc < n; cc += DT) {
+    double t = 0.0;
+    for (int q = 0; q < G; ++q) t += part[q * nc + cc];
+    y[cc] = t;
+  }
+  __syncthreads();
 }
 
 __device__ double max_of(const double* y, int n, double* red) {
@@ -186,9 +200,11 @@ __device__ __noinline__ bool gj_solve(double* M, int n, double* red, int* ired, 
     if (lane == 0) { red[warp] = best; ired[warp] = bi; }
     __syncthreads();
     // every thread combines the warp results itself (same order, same answer), so no second
-    // barrier; red/ired are rewritten only after this step's two later barriers
+    // barrier; red/ired are rewritten only after this step's two later barriers.  Only warps
+    // that saw a candidate row (rows k .. n-1) take part
     double bb = -1.0; int piv = n;
-    for (int w = 0; w < NWD; ++w)
+    const int nwd = min(NWD, (n - k + 31) / 32);
+    for (int w = 0; w < nwd; ++w)
       if (red[w] > bb || (red[w] == bb && ired[w] < piv)) { bb = red[w]; piv = ired[w]; }
     if (!(bb > 0.0)) return false;
     const double d = M[piv * w2 + k];
@@ -205,11 +221,27 @@ __device__ __noinline__ bool gj_solve(double* M, int n, double* red, int* ired, 
     }
     __syncthreads();
     if (piv != k && threadIdx.x == 0) M[piv * w2 + k] = M[k * w2 + k];
-    for (int i = warp; i < n; i += NWD) {
-      const double f = fac[i];
-      if (i == k || f == 0.0) continue;
-      double* row = M + (size_t)i * w2;
-      for (int c = k + 1 + lane; c < w2; c += 32) row[c] = fma(-f, prow[c], row[c]);
+    // elimination: warp w owns rows w, w + NWD, ...; for each column its lanes update all of
+    // the warp's rows at once — RPW independent FMAs per column instead of one dependent
+    // load-FMA-store chain per row (the same operation per element, so the same bits)
+    constexpr int RPW = 8;
+    for (int base = warp; base < n; base += NWD * RPW) {
+      double fr[RPW];
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        const int i = base + q * NWD;
+        fr[q] = (i < n) ? fac[i] : 0.0;          // fac[k] = 0: the pivot row is left alone
+      }
+      for (int c = k + 1 + lane; c < w2; c += 32) {
+        const double pc = prow[c];
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+          if (fr[q] != 0.0) {
+            double* a = M + (size_t)(base + q * NWD) * w2 + c;
+            *a = fma(-fr[q], pc, *a);
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -220,7 +252,7 @@ __device__ __noinline__ bool gj_solve(double* M, int n, double* red, int* ired, 
 // E = exp(A) (vcol < 0), or only vout = exp(A) e_vcol (vcol >= 0; E then holds a scaled factor)
 // sM: shared-memory home of the n x 2n Gauss-Jordan system when it fits (else null: global)
 __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA, double* sB, double* red,
-                          int* ired, double* prow, int vcol, double* vout, double* sM) {
+                          int* ired, double* prow, int vcol, double* vout, double* sM, double* fac) {
   double* A2 = W.m[0];
   double* A4 = W.m[1];
   double* A6 = W.m[2];
@@ -231,7 +263,6 @@ __device__ bool expm_block(double* A, int n, double* E, DenseWork W, double* sA,
   double* M = sM ? sM : W.m[7];      // n x 2n: n dependent elimination steps, keep on chip
   double* x = prow;        // norm scratch on chip (prow is free until the solve)
   double* y = prow + n;
-  double* fac = W.vec + 2 * n;
 
   // ell() runs 2m+1 dependent |A|-matvecs: read A from shared memory when the (not yet
   // used) Gauss-Jordan area is on chip
@@ -384,7 +415,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   __shared__ double sB[16 * MM_MAXR];
   __shared__ double red[DT / 32 + 1];
   __shared__ int ired[DT / 32 + 1];
-  extern __shared__ double prow[];                 // [2n] staged pivot row (+ [n][2n] M)
+  extern __shared__ double prow[];                 // [2n] pivot row, [n] GJ factors (+ [n][2n] M)
   const int sidx = blockIdx.x;
   // phi_order(X) e1 from the (m + order)-dimensional augmentation
   //   [[X, e1, 0 ..], [0, 0, 1 ..], .., [0 .. 0]]   (exp top-right column = phi_order(X) e1),
@@ -400,7 +431,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
     // small n: every work matrix lives in shared memory (the same code, generic pointers):
     // the ~100 dependent steps of an exponential (products, norms, the 2m+1 |A|-products of
     // ell, the elimination) then wait on shared-memory latency instead of L2 round trips
-    double* b = prow + 2 * n;
+    double* b = prow + 3 * n;
     const size_t nn = (size_t)n * n;
     W.a = b;
     W.e = b + nn;
@@ -435,8 +466,8 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   for (int e = threadIdx.x; e < m * m; e += DT) if (!isfinite(A[(e / m) * n + e % m])) finite = false;
   finite = __syncthreads_and(finite);
   double* ycol = W.vec + 3 * n;                    // [2n] column result / ping-pong
-  double* sM = (!P.smem_work && n <= P.smem_n) ? prow + 2 * n : nullptr;
-  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol, sM);
+  double* sM = (!P.smem_work && n <= P.smem_n) ? prow + 3 * n : nullptr;
+  bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol, sM, prow + 2 * n);
   if (ok) {
     bool fin2 = true;
     if (P.E_out) {
@@ -473,6 +504,395 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   }
 }
 
+// ============================================================================================
+// Cluster version (n >= DENSE_CLUSTER_MIN_N): one exponential per thread-block cluster of
+// DENSE_CLUSTER CTAs on as many SMs.  The same algorithm as expm_block (same degree / scaling
+// decisions from the same exact 1-norms, same Pade, Gauss-Jordan and squarings), with the
+// O(n^3) products, the elementwise updates and the column sums of the norms and of ell's
+// |A|-products split by row blocks across the cluster; work matrices stay in the (L2-resident)
+// global workspace and the phases are ordered by cluster barriers (release / acquire at cluster
+// scope).  The Gauss-Jordan solve and the 2^s vector products run on rank 0 (one CTA), whose
+// n dependent steps would otherwise each cost a cluster barrier.
+struct Team {
+  int rank, size;
+  __device__ __forceinline__ void sync() const {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
+  __device__ __forceinline__ int r0(int n) const { const int b = (n + size - 1) / size; return min(n, rank * b); }
+  __device__ __forceinline__ int r1(int n) const { const int b = (n + size - 1) / size; return min(n, (rank + 1) * b); }
+};
+
+// rows [r0, r1) of C = A * B (n x n, row-major), the k sums in order 0 .. n-1 per element (the
+// same chains as mm_tile); 16 row lanes x 32 column lanes, RN columns per thread
+template <int RN>
+__device__ void mm_rows_t(double* C, const double* A, const double* B, int n, int r0, int r1, double* sA,
+                          double* sB) {
+  constexpr int TC = 32 * RN;
+  const int t = threadIdx.x;
+  const int tr = t / 32;
+  const int tc = (t % 32) * RN;
+  for (int bi = r0; bi < r1; bi += 16) {
+    for (int bj = 0; bj < n; bj += TC) {
+      double acc[RN];
+#pragma unroll
+      for (int v = 0; v < RN; ++v) acc[v] = 0.0;
+      for (int bk = 0; bk < n; bk += 16) {
+        for (int q = t; q < 16 * 16; q += DT) {
+          const int r = q / 16, c = q % 16;
+          const int gr = bi + r, gc = bk + c;
+          sA[r * 17 + c] = (gr < r1 && gc < n) ? A[gr * n + gc] : 0.0;
+        }
+        for (int q = t; q < 16 * TC; q += DT) {
+          const int r2 = q / TC, c2 = q % TC;
+          const int gr2 = bk + r2, gc2 = bj + c2;
+          sB[r2 * TC + c2] = (gr2 < n && gc2 < n) ? B[gr2 * n + gc2] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const double av = sA[tr * 17 + k];
+#pragma unroll
+          for (int v = 0; v < RN; ++v) acc[v] = fma(av, sB[k * TC + tc + v], acc[v]);
+        }
+        __syncthreads();
+      }
+      const int gr = bi + tr;
+#pragma unroll
+      for (int v = 0; v < RN; ++v) {
+        const int gc = bj + tc + v;
+        if (gr < r1 && gc < n) C[gr * n + gc] = acc[v];
+      }
+    }
+  }
+}
+
+__device__ void mm_team(const Team& T, double* C, const double* A, const double* B, int n, double* sA,
+                        double* sB) {
+  const int r0 = T.r0(n), r1 = T.r1(n);
+  if (n <= 32) mm_rows_t<1>(C, A, B, n, r0, r1, sA, sB);
+  else if (n <= 64) mm_rows_t<2>(C, A, B, n, r0, r1, sA, sB);
+  else if (n <= 96) mm_rows_t<3>(C, A, B, n, r0, r1, sA, sB);
+  else mm_rows_t<4>(C, A, B, n, r0, r1, sA, sB);     // n > 128: loops over 128-column tiles
+  T.sync();
+}
+
+// y[c] = sum_r w(r) |A[r][c]| over ALL rows: each CTA sums its row block into the step's
+// partial buffer, then (after the cluster barrier) every CTA adds the size partials in rank
+// order — identical y on every CTA.  `par` alternates between the two partial buffers.
+__device__ void colsums_team(const Team& T, const double* A, int n, const double* x, double* y,
+                             double* part_g, int& par) {
+  const int r0 = T.r0(n), r1 = T.r1(n);
+  double* mine = part_g + ((size_t)par * T.size + T.rank) * n;
+  for (int c = threadIdx.x; c < n; c += DT) {
+    double s = 0.0;
+    if (x) for (int r = r0; r < r1; ++r) s += x[r] * fabs(A[r * n + c]);
+    else for (int r = r0; r < r1; ++r) s += fabs(A[r * n + c]);
+    mine[c] = s;
+  }
+  T.sync();
+  const double* all = part_g + (size_t)par * T.size * n;
+  for (int c = threadIdx.x; c < n; c += DT) {
+    double s = 0.0;
+    for (int q = 0; q < T.size; ++q) s += __ldcg(all + (size_t)q * n + c);
+    y[c] = s;
+  }
+  __syncthreads();
+  par ^= 1;
+}
+
+__device__ double norm1_team(const Team& T, const double* A, int n, double* red, double* y, double* part_g,
+                             int& par) {
+  colsums_team(T, A, n, nullptr, y, part_g, par);
+  return max_of(y, n, red);
+}
+
+__device__ int ell_team(const Team& T, const double* A, int n, int m, double a1, double* x, double* y,
+                        double* red, double* part_g, int& par) {
+  const int p = 2 * m + 1;
+  const double lg = lgamma(2.0 * p + 1.0) - 2.0 * lgamma((double)p + 1.0) + lgamma(2.0 * p + 2.0);
+  for (int i = threadIdx.x; i < n; i += DT) x[i] = 1.0;
+  __syncthreads();
+  for (int k = 0; k < p; ++k) {
+    colsums_team(T, A, n, x, y, part_g, par);
+    for (int i = threadIdx.x; i < n; i += DT) x[i] = y[i];
+    __syncthreads();
+  }
+  const double nap = max_of(x, n, red);
+  if (nap == 0.0 || a1 == 0.0) return 0;
+  const double log2_alpha = log2(nap) - log2(a1) - lg / log(2.0);
+  const double v = ceil((log2_alpha + 53.0) / (2.0 * m));
+  return v > 0.0 ? (int)v : 0;
+}
+
+__device__ void axpby_team(const Team& T, double* out, const double* const* terms, const double* coefs,
+                           int nterms, int n, double diag) {
+  const int r0 = T.r0(n), r1 = T.r1(n);
+  for (int e = r0 * n + threadIdx.x; e < r1 * n; e += DT) {
+    double s = ((e / n) == (e % n)) ? diag : 0.0;
+    for (int k = 0; k < nterms; ++k) s = fma(coefs[k], terms[k][e], s);
+    out[e] = s;
+  }
+  T.sync();
+}
+
+__device__ void scale_rows_team(const Team& T, double* X, int n, double f) {
+  const int r0 = T.r0(n), r1 = T.r1(n);
+  for (int e = r0 * n + threadIdx.x; e < r1 * n; e += DT) X[e] *= f;
+}
+
+// expm_block on a cluster (see above); rank 0 leaves the result as expm_block does
+__device__ bool expm_cluster(const Team& T, double* A, int n, double* E, DenseWork W, double* sA, double* sB,
+                             double* red, int* ired, double* prow, int vcol, double* vout, double* sM,
+                             double* fac) {
+  double* A2 = W.m[0];
+  double* A4 = W.m[1];
+  double* A6 = W.m[2];
+  double* A8 = W.m[3];
+  double* U = W.m[4];
+  double* Vm = W.m[5];
+  double* Tm = W.m[6];
+  double* M = sM ? sM : W.m[7];
+  double* x = prow;
+  double* y = prow + n;
+  int par = 0;
+  mm_team(T, A2, A, A, n, sA, sB);
+  mm_team(T, A4, A2, A2, n, sA, sB);
+  mm_team(T, A6, A4, A2, n, sA, sB);
+  const double a1 = norm1_team(T, A, n, red, y, W.part, par);
+  const double d4 = pow(norm1_team(T, A4, n, red, y, W.part, par), 0.25);
+  const double d6 = pow(norm1_team(T, A6, n, red, y, W.part, par), 1.0 / 6.0);
+  const double eta1 = fmax(d4, d6);
+  int mdeg = 0, s = 0;
+  if (eta1 <= 1.495585217958292e-002 && ell_team(T, A, n, 3, a1, x, y, red, W.part, par) == 0) mdeg = 3;
+  else if (eta1 <= 2.539398330063230e-001 && ell_team(T, A, n, 5, a1, x, y, red, W.part, par) == 0) mdeg = 5;
+  double d8 = 0.0, eta3 = 0.0;
+  if (mdeg == 0) {
+    mm_team(T, A8, A4, A4, n, sA, sB);
+    d8 = pow(norm1_team(T, A8, n, red, y, W.part, par), 0.125);
+    eta3 = fmax(d6, d8);
+    if (eta3 <= 9.504178996162932e-001 && ell_team(T, A, n, 7, a1, x, y, red, W.part, par) == 0) mdeg = 7;
+    else if (eta3 <= 2.097847961257068e+000 && ell_team(T, A, n, 9, a1, x, y, red, W.part, par) == 0) mdeg = 9;
+  }
+  if (mdeg == 0) {
+    mm_team(T, Tm, A4, A6, n, sA, sB);           // A^10
+    const double d10 = pow(norm1_team(T, Tm, n, red, y, W.part, par), 0.1);
+    const double eta4 = fmax(d8, d10);
+    const double eta5 = fmin(eta3, eta4);
+    s = (eta5 == 0.0) ? 0 : (int)fmax(ceil(log2(eta5 / 4.25)), 0.0);
+    const double sc = ldexp(1.0, -s);
+    scale_rows_team(T, A, n, sc);
+    T.sync();
+    const double a1s = norm1_team(T, A, n, red, y, W.part, par);
+    s += ell_team(T, A, n, 13, a1s, x, y, red, W.part, par);
+    const double sc2 = ldexp(1.0, -s);
+    scale_rows_team(T, A, n, sc2 / sc);
+    scale_rows_team(T, A2, n, ldexp(1.0, -2 * s));
+    scale_rows_team(T, A4, n, ldexp(1.0, -4 * s));
+    scale_rows_team(T, A6, n, ldexp(1.0, -6 * s));
+    T.sync();
+    mdeg = 13;
+  }
+  if (mdeg == 13) {
+    const double b[14] = {64764752532480000., 32382376266240000., 7771770303897600.,
+                          1187353796428800., 129060195264000., 10559470521600.,
+                          670442572800., 33522128640., 1323241920., 40840800., 960960.,
+                          16380., 182., 1.};
+    {
+      const double* tt[3] = {A6, A4, A2};
+      const double cc[3] = {b[13], b[11], b[9]};
+      axpby_team(T, Tm, tt, cc, 3, n, 0.0);
+      mm_team(T, U, A6, Tm, n, sA, sB);
+      const double* t2[4] = {U, A6, A4, A2};
+      const double c2[4] = {1.0, b[7], b[5], b[3]};
+      axpby_team(T, Tm, t2, c2, 4, n, b[1]);
+      mm_team(T, U, A, Tm, n, sA, sB);
+    }
+    {
+      const double* tt[3] = {A6, A4, A2};
+      const double cc[3] = {b[12], b[10], b[8]};
+      axpby_team(T, Tm, tt, cc, 3, n, 0.0);
+      mm_team(T, Vm, A6, Tm, n, sA, sB);
+      const double* t2[4] = {Vm, A6, A4, A2};
+      const double c2[4] = {1.0, b[6], b[4], b[2]};
+      axpby_team(T, Vm, t2, c2, 4, n, b[0]);      // in place per element: reads Vm[e] first
+    }
+  } else {
+    double b[10];
+    if (mdeg == 3) { const double c[] = {120., 60., 12., 1.}; for (int k = 0; k < 4; ++k) b[k] = c[k]; }
+    if (mdeg == 5) { const double c[] = {30240., 15120., 3360., 420., 30., 1.}; for (int k = 0; k < 6; ++k) b[k] = c[k]; }
+    if (mdeg == 7) { const double c[] = {17297280., 8648640., 1995840., 277200., 25200., 1512., 56., 1.}; for (int k = 0; k < 8; ++k) b[k] = c[k]; }
+    if (mdeg == 9) { const double c[] = {17643225600., 8821612800., 2075673600., 302702400., 30270240., 2162160., 110880., 3960., 90., 1.}; for (int k = 0; k < 10; ++k) b[k] = c[k]; }
+    const double* pw[4] = {A2, A4, A6, A8};
+    const int nt = mdeg / 2;
+    double co[4], ce[4];
+    for (int k = 0; k < nt; ++k) { co[k] = b[2 * k + 3]; ce[k] = b[2 * k + 2]; }
+    axpby_team(T, Tm, pw, co, nt, n, b[1]);
+    mm_team(T, U, A, Tm, n, sA, sB);
+    axpby_team(T, Vm, pw, ce, nt, n, b[0]);
+  }
+  // rank 0: M = [V - U | V + U], Gauss-Jordan, E; the others wait at the next barrier
+  bool ok = true;
+  if (T.rank == 0) {
+    for (int e = threadIdx.x; e < n * n; e += DT) {
+      const int r = e / n, c = e % n;
+      const double v = __ldcg(Vm + e), u = __ldcg(U + e);
+      M[r * 2 * n + c] = v - u;
+      M[r * 2 * n + n + c] = v + u;
+    }
+    __syncthreads();
+    ok = gj_solve(M, n, red, ired, fac, prow);
+    if (ok)
+      for (int e = threadIdx.x; e < n * n; e += DT) E[e] = M[(e / n) * 2 * n + n + e % n];
+    __syncthreads();
+    if (threadIdx.x == 0) red[DT / 32] = ok ? 1.0 : 0.0;
+  }
+  // share the solve's verdict: rank 0 writes it into the partial buffer before the barrier
+  if (T.rank == 0 && threadIdx.x == 0) W.part[0] = ok ? 1.0 : 0.0;
+  T.sync();
+  ok = __ldcg(W.part) != 0.0;
+  if (!ok) return false;
+  if (vcol >= 0 && s <= 7) {
+    // 2^s matrix-vector products on rank 0 (dependent, each O(n^2)); result in vout
+    if (T.rank == 0) {
+      double* xa = vout;
+      double* xb = vout + n;
+      for (int i = threadIdx.x; i < n; i += DT) xa[i] = E[(size_t)i * n + vcol];
+      __syncthreads();
+      for (int k = 1; k < (1 << s); ++k) {
+        for (int i = threadIdx.x; i < n; i += DT) {
+          double acc = 0.0;
+          const double* row = E + (size_t)i * n;
+          for (int c = 0; c < n; ++c) acc = fma(row[c], xa[c], acc);
+          xb[i] = acc;
+        }
+        __syncthreads();
+        double* tmp = xa; xa = xb; xb = tmp;
+      }
+      if (xa != vout)
+        for (int i = threadIdx.x; i < n; i += DT) vout[i] = xa[i];
+      __syncthreads();
+    }
+    return true;
+  }
+  for (int k = 0; k < s; ++k) {
+    mm_team(T, Tm, E, E, n, sA, sB);
+    const int r0 = T.r0(n), r1 = T.r1(n);
+    for (int e = r0 * n + threadIdx.x; e < r1 * n; e += DT) E[e] = Tm[e];
+    T.sync();
+  }
+  if (vcol >= 0 && T.rank == 0) {
+    for (int i = threadIdx.x; i < n; i += DT) vout[i] = E[(size_t)i * n + vcol];
+    __syncthreads();
+  }
+  return true;
+}
+
+// phi_small_kernel on a cluster: cluster q serves problem q (a scale / basis size); rank 0 of
+// the cluster writes the outputs
+__global__ void __launch_bounds__(DT) phi_cluster_kernel(PhiSmallArgs P) {
+  __shared__ double sA[16 * 17];
+  __shared__ double sB[16 * MM_MAXR];
+  __shared__ double red[DT / 32 + 1];
+  __shared__ int ired[DT / 32 + 1];
+  extern __shared__ double prow[];                 // [2n] pivot row, [n] GJ factors (+ [n][2n] M on rank 0)
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  Team T{(int)rank, DENSE_CLUSTER};
+  const int sidx = blockIdx.x / DENSE_CLUSTER;
+  const int m = P.batch ? P.mb[sidx] : P.m, n = m + P.order;
+  const int col = (P.order == 0) ? 0 : m + P.order - 1;
+  DenseWork W = P.work[sidx];
+  double* A = W.a;
+  double* E = W.e;
+  double* Yrow = P.Y + (size_t)sidx * (P.batch ? P.ldy : P.m);
+  const double sc = P.scales_by_value ? P.sv[sidx] : P.scales[sidx];
+  double hn;
+  bool brk;
+  if (P.batch) {
+    brk = P.brk_hist[m - 1] != 0.0;
+    hn = brk ? 0.0 : P.H[(size_t)m * P.ldh + (m - 1)];
+  } else {
+    hn = P.scal ? P.scal[0] : 0.0;
+    brk = P.scal ? (P.scal[2] != 0.0) : true;
+  }
+  const double beta = P.beta[0];
+  {
+    // this rank's rows of the augmented matrix, and its verdict on their finiteness
+    const int r0 = T.r0(n), r1 = T.r1(n);
+    bool fin = true;
+    for (int e = r0 * n + threadIdx.x; e < r1 * n; e += DT) {
+      const int r = e / n, c = e % n;
+      double v = 0.0;
+      if (r < m && c < m) {
+        v = sc * P.H[(size_t)r * P.ldh + c];
+        if (!isfinite(v)) fin = false;
+      } else if (r == 0 && c == m) v = 1.0;
+      else if (r >= m && c == r + 1) v = 1.0;
+      A[e] = v;
+    }
+    fin = __syncthreads_and(fin);
+    if (threadIdx.x == 0) W.part[(size_t)DENSE_CLUSTER * n + rank] = fin ? 1.0 : 0.0;
+  }
+  T.sync();
+  bool finite = true;
+  for (int q = 0; q < DENSE_CLUSTER; ++q)
+    finite = finite && __ldcg(W.part + (size_t)DENSE_CLUSTER * n + q) != 0.0;
+  T.sync();                                        // the partial buffer is reused below
+  double* ycol = W.vec + 3 * n;
+  double* sM = (rank == 0 && n <= P.smem_n) ? prow + 3 * n : nullptr;
+  bool ok = finite && expm_cluster(T, A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol, sM,
+                                   prow + 2 * n);
+  if (rank != 0) return;
+  if (ok) {
+    bool fin2 = true;
+    if (P.E_out) {
+      for (int e = threadIdx.x; e < n * n; e += DT) if (!isfinite(E[e])) fin2 = false;
+    } else {
+      for (int i = threadIdx.x; i < n; i += DT) if (!isfinite(ycol[i])) fin2 = false;
+    }
+    ok = __syncthreads_and(fin2);
+  }
+  if (!ok) {
+    if (threadIdx.x == 0) { atomicOr(&P.st->flags, (int)ST_DENSE); P.res[sidx] = INFINITY; }
+    return;
+  }
+  if (P.E_out) {
+    for (int e = threadIdx.x; e < n * n; e += DT) P.E_out[e] = E[e];
+  }
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < m; i += DT) {
+    const double yv = ycol[i] * beta;
+    Yrow[i] = yv;
+    ss += yv * yv;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < DT / 32; ++w) t += red[w];
+    const double nrm = sqrt(t);
+    const double ylast = ycol[m - 1] * beta;
+    const double hnext = brk ? 0.0 : hn;
+    double r = (nrm == 0.0) ? 0.0 : fabs(hnext) * fabs(ylast) / nrm;
+    P.res[sidx] = r * (P.scales_by_value ? P.rv[sidx] : P.res_scale[sidx]);
+  }
+}
+
+// smallest n served by the cluster kernel (0: never); EMHD_DENSE_CLUSTER_N, emhd_set_dense_cluster
+static int g_cluster_min_n = -1;
+
+int dense_cluster_min_n() {
+  if (g_cluster_min_n < 0) {
+    const char* e = getenv("EMHD_DENSE_CLUSTER_N");
+    g_cluster_min_n = e ? atoi(e) : 56;
+  }
+  return g_cluster_min_n;
+}
+
+void set_dense_cluster_min_n(int n) { g_cluster_min_n = n < 0 ? 0 : n; }
+
 cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t s) {
   PhiSmallArgs P = Pin;
   const int n = P.m + P.order;              // the largest m of a batch
@@ -497,17 +917,45 @@ cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t 
     const char* env = getenv("EMHD_DENSE_SMEM");
     use_smem = env ? atoi(env) != 0 : 1;
   }
-  size_t dyn = sizeof(double) * 2 * n;
+  // dynamic shared memory: [2n] pivot row + [n] elimination factors, then the [n][2n]
+  // Gauss-Jordan system when it fits (or, for small n on one CTA, the whole workspace)
+  size_t dyn = sizeof(double) * 3 * n;
   P.smem_n = 0;
   P.smem_work = 0;
-  const size_t whole = sizeof(double) * (2 * (size_t)n + 11 * (size_t)n * n + 5 * (size_t)n + 64);
-  if (use_smem && whole <= (size_t)max_dyn) {
+  const int cmin = dense_cluster_min_n();
+  const bool cluster = cmin > 0 && n >= cmin;
+  const size_t whole = sizeof(double) * (3 * (size_t)n + 11 * (size_t)n * n + 5 * (size_t)n + 64);
+  if (use_smem && !cluster && whole <= (size_t)max_dyn) {
     dyn = whole;                        // n <= ~42: the whole exponential on chip
     P.smem_work = 1;
-  } else if (use_smem && sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
-    dyn = sizeof(double) * (2 * (size_t)n + 2 * (size_t)n * n);
+  } else if (use_smem && sizeof(double) * (3 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
+    dyn = sizeof(double) * (3 * (size_t)n + 2 * (size_t)n * n);
     P.smem_n = n;
   }
+  if (cluster) {
+    // one cluster of DENSE_CLUSTER CTAs per problem; rank 0 keeps the on-chip M when it fits
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(phi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+      cudaGetLastError();
+      attr = true;
+    }
+    P.cluster = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nscales * DENSE_CLUSTER);
+    cfg.blockDim = dim3(DT);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = DENSE_CLUSTER;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, phi_cluster_kernel, P);
+  }
+  P.cluster = 0;
   phi_small_kernel<<<nscales, DT, dyn, s>>>(P);
   return cudaGetLastError();
 }

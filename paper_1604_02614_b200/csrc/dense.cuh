@@ -10,8 +10,14 @@ struct DenseWork {
   double* a;        // n x n input (scaled in place)
   double* e;        // n x n exponential
   double* m[8];     // 7 n x n work matrices + one n x 2n
-  double* vec;      // 3 n
+  double* vec;      // 5 n + 64
+  double* part;     // [2][CLUSTER][n] column-sum partials of the cluster kernel
 };
+
+constexpr int DENSE_CLUSTER = 8;     // CTAs (SMs) per exponential in the cluster kernel
+
+// doubles of dense workspace per problem of dimension n (see carve in capi.cu)
+inline size_t dense_per(size_t n) { return 11 * n * n + 5 * n + 64 + 2 * DENSE_CLUSTER * n; }
 
 struct PhiSmallArgs {
   const double* H;          // Hessenberg (device), leading m x m block used
@@ -36,8 +42,11 @@ struct PhiSmallArgs {
   int smem_n;               // set by the launcher: largest n whose [n][2n] system is on chip
   int smem_work;            // set by the launcher: the whole workspace (11 n^2 + 5 n doubles) is
                             // carved from dynamic shared memory instead of the global work[]
+  int cluster;              // set by the launcher: DENSE_CLUSTER CTAs per problem (large n)
 };
 
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s);
+int dense_cluster_min_n();
+void set_dense_cluster_min_n(int n);
 
 }  // namespace emhd

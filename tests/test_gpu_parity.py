@@ -826,3 +826,30 @@ def test_selective_reorth_stress_m120_near_dependent(P):
         assert drift(H, k_rep) <= 1e-8, (name, k_rep, drift(H, k_rep))
         for k in (40, 60, 80):
             assert drift(H, k) <= 4.0 * floor[k] + 1e-9, (name, k, drift(H, k), floor[k])
+
+
+def test_l2_window_released_with_the_context(P):
+    """emhd_l2_window raises the device's persisting-L2 limit and sets a window on the stream;
+    destroying the context removes the window and restores the limit it found (ADVICE r1:
+    nothing outlives the context)."""
+    cudart = pytest.importorskip("cuda.bindings.runtime")
+    from paper_1604_02614_b200 import _native as N
+    from paper_1604_02614_b200 import device as D
+    from paper_1604_02614_b200.fdjac import _generic_ctx
+
+    def limit():
+        err, v = cudart.cudaDeviceGetLimit(cudart.cudaLimit.cudaLimitPersistingL2CacheSize)
+        assert err == cudart.cudaError_t.cudaSuccess
+        return v
+
+    g = _generic_ctx()
+    buf = torch.empty(1 << 20, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    lim0 = limit()
+    ctx = D.Ctx(g.geometry, g.physics, 16)
+    want = 4 << 20 if lim0 != 4 << 20 else 6 << 20
+    N.check(ctx.lib.emhd_l2_window(ctx.sync_stream(), buf.data_ptr(), want), "l2_window")
+    assert limit() != lim0
+    del ctx                          # emhd_ctx_destroy
+    torch.cuda.synchronize()
+    assert limit() == lim0
