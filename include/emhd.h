@@ -76,6 +76,7 @@ typedef struct emhd_status {
   unsigned long long first_nonfinite;  /* flat index of the first non-finite F(a+sigma v) */
   int breakdown;                       /* Arnoldi lucky breakdown seen */
   int fail_iter;                       /* epoch (emhd_set_epoch) of the first flagging stencil */
+  int rhs_evals_mark;                  /* rhs_evals at the last emhd_evals_mark (stream-ordered) */
 } emhd_status;
 
 /* ---- context -------------------------------------------------------- */
@@ -85,14 +86,20 @@ int emhd_ctx_create(emhd_ctx** ctx, const emhd_geometry* g, const emhd_physics* 
 int emhd_ctx_destroy(emhd_ctx* ctx);
 int emhd_set_stream(emhd_ctx* ctx, void* cuda_stream);
 int emhd_num_sms(emhd_ctx* ctx);
-/* tag recorded (atomic min) in emhd_status.fail_iter by stencil launches that flag an error */
+/* tag recorded (atomic min) in emhd_status.fail_iter by stencil launches that flag an error;
+ * -1 (the default) for launches outside the Arnoldi driver, whose iterations carry their index */
 int emhd_set_epoch(emhd_ctx* ctx, int epoch);
 /* synchronous read of the device status word (stream-ordered) */
 int emhd_status_read(emhd_ctx* ctx, emhd_status* out);
 int emhd_status_reset(emhd_ctx* ctx);
+/* stream-ordered snapshot of rhs_evals into rhs_evals_mark (no sync): a step's RHS count is
+ * then read in the step's one final status read instead of a read at its start */
+int emhd_evals_mark(emhd_ctx* ctx);
 /* stream-ordered: clear RHO/PRESSURE/NONFINITE flags whose fail_iter >= epoch_min (discarded
  * speculative Arnoldi iterations; no reference counterpart — they never run there) */
 int emhd_status_scrub(emhd_ctx* ctx, int epoch_min);
+/* stream-ordered: clear every error flag and first-failure record, keep rhs_evals (and its mark) */
+int emhd_status_clear_errors(emhd_ctx* ctx);
 
 /* ---- stencil launch selection (per context) ------------------------- */
 /* Which kernel variant evaluates the fused RHS / Jv stencil.  All variants issue the same

@@ -31,7 +31,7 @@ class Physics(ctypes.Structure):
 
 class Status(ctypes.Structure):
     _fields_ = [("flags", c_int), ("rhs_evals", c_int), ("first_nonfinite", ctypes.c_ulonglong),
-                ("breakdown", c_int), ("fail_iter", c_int)]
+                ("breakdown", c_int), ("fail_iter", c_int), ("rhs_evals_mark", c_int)]
 
 
 class ArnoldiArgs(ctypes.Structure):
@@ -72,6 +72,8 @@ _SIGS = {
     "emhd_status_read": (c_int, [c_vp, ctypes.POINTER(Status)]),
     "emhd_status_reset": (c_int, [c_vp]),
     "emhd_status_scrub": (c_int, [c_vp, c_int]),
+    "emhd_evals_mark": (c_int, [c_vp]),
+    "emhd_status_clear_errors": (c_int, [c_vp]),
     "emhd_set_stencil_path": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
     "emhd_get_stencil_path": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
     "emhd_last_stencil": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),

@@ -30,7 +30,8 @@ struct emhd_ctx {
   double* dense = nullptr;            // dense workspace
   size_t dense_len = 0;
   StencilParams base{};
-  int epoch = 0;
+  int epoch = -1;                             // tag of stencil launches outside the Arnoldi
+                                              // driver (-1: never a discarded speculative one)
   unsigned long long* cancel = nullptr;       // look-ahead cancel word {generation, epoch}
   unsigned long long* cancel_host = nullptr;  // pinned source of its async updates
   const double* skip_next = nullptr;          // emhd_skip_next: gate of the next pass-2 launch
@@ -303,9 +304,31 @@ __global__ void status_scrub_kernel(DevStatus* st, int epoch_min) {
   }
 }
 
+__global__ void status_clear_errors_kernel(DevStatus* st) {
+  st->flags &= ~(ST_RHO | ST_PRESSURE | ST_NONFINITE | ST_DENSE);
+  st->fail_iter = 0x7fffffff;
+  st->first_nonfinite = ~0ull;
+}
+
+// Stream-ordered: clear the error flags (and their first-failure records) but keep the RHS
+// count and its mark — errors of discarded speculative work are forgotten, counting goes on
+extern "C" int emhd_status_clear_errors(emhd_ctx* c) {
+  if (!c) return EMHD_ERR_ARG;
+  status_clear_errors_kernel<<<1, 1, 0, c->stream>>>(c->st);
+  return cerr(cudaGetLastError());
+}
+
 extern "C" int emhd_status_scrub(emhd_ctx* c, int epoch_min) {
   if (!c) return EMHD_ERR_ARG;
   status_scrub_kernel<<<1, 1, 0, c->stream>>>(c->st, epoch_min);
+  return cerr(cudaGetLastError());
+}
+
+__global__ void evals_mark_kernel(DevStatus* st) { st->rhs_evals_mark = st->rhs_evals; }
+
+extern "C" int emhd_evals_mark(emhd_ctx* c) {
+  if (!c) return EMHD_ERR_ARG;
+  evals_mark_kernel<<<1, 1, 0, c->stream>>>(c->st);
   return cerr(cudaGetLastError());
 }
 
@@ -316,6 +339,7 @@ extern "C" int emhd_status_read(emhd_ctx* c, emhd_status* out) {
   if (rc) return rc;
   out->flags = c->st_host->flags;
   out->rhs_evals = c->st_host->rhs_evals;
+  out->rhs_evals_mark = c->st_host->rhs_evals_mark;
   out->first_nonfinite = c->st_host->first_nonfinite;
   out->breakdown = c->st_host->breakdown;
   out->fail_iter = c->st_host->fail_iter;
@@ -1041,7 +1065,8 @@ static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
   if (!c || !args || j < 0) return EMHD_ERR_ARG;
   const emhd_arnoldi_args_s* A = (const emhd_arnoldi_args_s*)args;
   if (j + 1 > c->max_vectors || (gated && !A->gate)) return EMHD_ERR_ARG;
-  c->epoch = j;
+  // the iteration's stencil carries epoch j (P.epoch below); the context's own epoch is left
+  // alone, so later RHS / Jv launches are never mistaken for a discarded speculative iteration
   if (c->comm) {
     // slab ranks: no look-ahead (a device-side cancellation could differ between ranks while
     // their collectives must match one to one)

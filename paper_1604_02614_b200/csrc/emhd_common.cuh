@@ -21,6 +21,7 @@ struct DevStatus {
   unsigned long long first_nonfinite;   // flat index of first non-finite Jv entry
   int breakdown;
   int fail_iter;                        // epoch of the first stencil launch that flagged
+  int rhs_evals_mark;                   // rhs_evals when emhd_evals_mark last ran (stream order)
 };
 
 // Correctly rounded x / d for a constant divisor d with r = RN(1/d), using

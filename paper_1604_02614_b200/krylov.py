@@ -210,7 +210,7 @@ class _Process:
     """Device Arnoldi factorisation (reference _ArnoldiProcess, krylov.py:127-188)."""
 
     def __init__(self, engine, seed, m_cap, n_top, p=0, layout=None, comm=None, persistent=False,
-                 reorthogonalize=True):
+                 reorthogonalize=True, seed_norms=None):
         self.eng = engine
         self.ctx = engine.ctx
         self.lib = self.ctx.lib
@@ -289,9 +289,15 @@ class _Process:
         sd = seed.reshape(-1)
         h = self.ctx.sync_stream()
         _l2_window(self.ctx, h, self.V, self.ld * 8)
-        N.check(self.lib.emhd_norms(h, D.ptr(sd), self.len_dot, n_top, D.ptr(self.nb)), "norms")
-        self._allreduce_norms(self.nb)
-        b2 = float(self.nb[0].item())
+        if seed_norms is not None:
+            # {sum seed^2, max|seed|} already all-reduced and read by the caller (its zero test):
+            # one host sync for both
+            dev2, b2 = seed_norms
+            self.nb[0:2].copy_(dev2)
+        else:
+            N.check(self.lib.emhd_norms(h, D.ptr(sd), self.len_dot, n_top, D.ptr(self.nb)), "norms")
+            self._allreduce_norms(self.nb)
+            b2 = float(self.nb[0].item())
         self.beta = math.sqrt(b2)
         if self.beta == 0.0:
             raise ValueError("Arnoldi seed vector must be nonzero")
@@ -432,6 +438,7 @@ class _Process:
             return self.settle()
         self.lib.emhd_set_epoch(self.ctx.sync_stream(), j)
         wi = self._apply(j)
+        self.lib.emhd_set_epoch(self.ctx.sync_stream(), -1)   # later launches: not speculative
         self.applies += 1
         w = self.w[wi]
         h = self.ctx.sync_stream()
@@ -585,6 +592,9 @@ class _Process:
     def check_status(self, st):
         E = self.eng
         if st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE):
+            if st.fail_iter < 0:
+                # flagged by a launch outside this factorisation (a step's RHS / remainder)
+                raise_status(self.ctx, st, None, self.comm)
             j = min(st.fail_iter, self.m - 1)
             a, ah = E.jop.a, E.jop.a_halo
             # the failing state is a + sigma V[j] with V[j] materialised
@@ -757,7 +767,8 @@ class _Process:
         elif self._pending and self.m > m_keep:
             return
         elif st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE | N.ST_DENSE):
-            self.ctx.reset_status()
+            # errors of discarded speculative work only: forget them, keep the RHS count
+            N.check(self.lib.emhd_status_clear_errors(self.ctx.sync_stream()), "status_clear_errors")
 
     def account_passes(self):
         """Reporting only (COUNT_PASSES): add this projection's kept iterations and second
@@ -834,6 +845,22 @@ def residual_estimate(basis, h, c, small_phi_seed):
     return abs(basis.h_next) * abs(y[-1]) / nrm
 
 
+def _seed_norms(ctx, v, len_dot, n_top, layout, comm):
+    """{sum v^2 over len_dot, max|v| over n_top} on the device, all-reduced across slabs, and
+    their host values — the zero test of a projection and its beta in ONE host sync."""
+    t = torch.zeros(2, dtype=D.F64, device=D.device())
+    N.check(ctx.lib.emhd_norms(ctx.sync_stream(), D.ptr(v), len_dot, n_top, D.ptr(t)), "norms")
+    if comm is not None and layout is not None and layout.distributed:
+        slots = torch.zeros(layout.size + 1, dtype=D.F64, device=D.device())
+        N.check(ctx.lib.emhd_slot_norms(ctx.sync_stream(), D.ptr(t), layout.rank, layout.size, D.ptr(slots)),
+                "slot_norms")
+        comm.allreduce_sum(slots)
+        N.check(ctx.lib.emhd_unslot_norms(ctx.sync_stream(), D.ptr(slots), layout.size, D.ptr(t)),
+                "unslot_norms")
+    host = t.cpu().numpy()
+    return t, float(host[0]), float(host[1])
+
+
 def _maxabs_many(ctx, vecs):
     out = torch.zeros(2 * len(vecs), dtype=D.F64, device=D.device())
     h = ctx.sync_stream()
@@ -857,10 +884,8 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
     vd = D.to_device(v).reshape(-1)
     eng, layout, comm = _engine_for(op, vd.numel())
     n_top = vd.numel()
-    mx = _maxabs_many(eng.ctx, [vd])
-    if comm is not None:
-        comm.allreduce_max(mx)
-    if float(mx[0].item()) == 0.0:
+    norms_dev, b2, vmax = _seed_norms(eng.ctx, vd, n_top, n_top, layout, comm)
+    if vmax == 0.0:
         outs = [torch.zeros(n_top, dtype=D.F64, device=D.device()) for _ in scales]
         if _into:
             for (base, coef, out), o in zip(_into, outs):
@@ -872,11 +897,12 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
         return ([D.to_host(o) for o in outs] if host else outs), stats
     c_big = max(scales)
     proc = _Process(eng, vd, cfg.m_max, n_top, 0, layout, comm, persistent=True,
-                    reorthogonalize=cfg.reorthogonalize)
+                    reorthogonalize=cfg.reorthogonalize, seed_norms=(norms_dev, b2))
     m_target = min(cfg.m_init, proc.n)
+    # the m_init burst is queued together with the first batch of residual checks: one host
+    # sync resolves both (a breakdown inside the burst is caught by that settle, below)
     proc.extend_many(m_target)
-    proc.settle()
-    nxt = proc.m                                  # smallest basis size not yet checked
+    nxt = m_target                                # smallest basis size not yet checked
     look = proc.lookahead()
     while True:
         # speculative batch: the residual at the current m plus up to B-1 further iterations,
@@ -893,6 +919,12 @@ def multi_scale_eval(op, h, v, scales, tol, cfg=None, order=1, _into=None):
         if look:
             proc.extend_many(look, lookahead=True)
         raw = proc.settle(res_raw, check=False, upto=hi, side=look > 0)
+        if proc.breakdown and proc.m < ms[0]:
+            # the burst broke down before m_init: the reference checks the residual at that m
+            # (rare: one more launch and sync)
+            ms = [proc.m]
+            _, res_raw = proc.phi_batch(order, c_big * h, ms)
+            raw = proc.settle(res_raw, check=False, upto=proc.m)
         chosen, res = None, None
         for k, mk in enumerate(ms):
             if mk > proc.m:                       # beyond a breakdown found by settle
@@ -981,13 +1013,17 @@ def phi_comb(req, cfg=None, _zero=None):
         q = np.array([t ** (p - 1 - i) / math.factorial(p - 1 - i) for i in range(p)])
         seed[:n_top].copy_(u)
         seed[n_top:n_top + p].copy_(torch.from_numpy(q))
+        # first substep: u = 0 and q = e_p, so ||seed||^2 = 1 exactly — no device norm or sync
+        known = None
+        if t == 0.0:
+            known = (torch.tensor([1.0, 0.0], dtype=D.F64).to(D.device(), non_blocking=True), 1.0)
         proc = _Process(eng, seed[:n_top + p], min(cfg.m_max, naug_glob), n_top, p, layout, comm,
                         reorthogonalize=cfg.reorthogonalize,
-                        persistent=True)
+                        persistent=True, seed_norms=known)
         m_target = min(cfg.m_init, naug_glob)
+        # burst queued together with the first batch of residual checks (one host sync)
         proc.extend_many(m_target)
-        proc.settle()
-        nxt = proc.m
+        nxt = m_target
         look = proc.lookahead()
         while True:
             # speculative batch of residual checks (see multi_scale_eval); extensions stop
@@ -1003,6 +1039,11 @@ def phi_comb(req, cfg=None, _zero=None):
             if look and proc.m < limit:
                 proc.extend_many(min(look, limit - proc.m), lookahead=True)
             raw = proc.settle(res_raw, check=False, upto=ms[-1], side=look > 0)
+            if proc.breakdown and proc.m < ms[0]:
+                # breakdown inside the burst: the reference checks the residual at that m
+                ms = [proc.m]
+                Yb, res_raw = proc.phi_batch(0, delta, ms)
+                raw = proc.settle(res_raw, check=False, upto=proc.m)
             tol_sub = req.tol * max(delta, 1e-2)
             action, res = None, None
             for k, mk in enumerate(ms):

@@ -131,6 +131,7 @@ def agree_status(st, comm):
         sum(int(b) for b in bits)
     mnv = mn.cpu().numpy()
     out.rhs_evals = st.rhs_evals
+    out.rhs_evals_mark = st.rhs_evals_mark
     out.first_nonfinite = int(mnv[0])
     out.breakdown = st.breakdown
     out.fail_iter = int(mnv[1])
