@@ -102,6 +102,10 @@ class Ctx:
         # RHS evaluations the device counted for speculative Arnoldi iterations that were
         # discarded (the reference never performs them); subtracted from StepStats.rhs_evals
         self.rhs_discount = 0
+        # stencil launches whose status is checked later (a step's RHS / remainder Jv): each is
+        # tagged with its own epoch DEFER_BASE + k, so the first one that failed is known and
+        # its admissibility report names the reference's cell (mhd.py:111-131)
+        self.deferred = []
 
     def sync_stream(self):
         s = stream_handle()
@@ -131,6 +135,24 @@ class Ctx:
         sp = N.StencilPath()
         N.check(self.lib.emhd_last_stencil(self.h, ctypes_byref(sp)), "last_stencil")
         return {k: getattr(sp, k) for k, _ in N.StencilPath._fields_}
+
+    DEFER_BASE = -(2 ** 31)
+
+    def defer(self, report_args, keep=()):
+        """Tag the next stencil launch as deferred (status read later); keep its inputs alive."""
+        k = len(self.deferred)
+        self.deferred.append((report_args, keep))
+        N.check(self.lib.emhd_set_epoch(self.sync_stream(), self.DEFER_BASE + k), "set_epoch")
+
+    def undefer(self):
+        N.check(self.lib.emhd_set_epoch(self.sync_stream(), -1), "set_epoch")
+
+    def deferred_report(self, st):
+        """Report arguments of the deferred launch that flagged first, or None."""
+        k = st.fail_iter - self.DEFER_BASE
+        if 0 <= k < len(self.deferred):
+            return self.deferred[k][0]
+        return None
 
     def reset_status(self):
         N.check(self.lib.emhd_status_reset(self.sync_stream()), "status_reset")

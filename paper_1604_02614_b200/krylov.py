@@ -593,8 +593,9 @@ class _Process:
         E = self.eng
         if st.flags & (N.ST_RHO | N.ST_PRESSURE | N.ST_NONFINITE):
             if st.fail_iter < 0:
-                # flagged by a launch outside this factorisation (a step's RHS / remainder)
-                raise_status(self.ctx, st, None, self.comm)
+                # flagged by a launch outside this factorisation (a step's RHS / remainder Jv,
+                # tagged by Ctx.defer: its report names the reference's cell)
+                raise_status(self.ctx, st, self.ctx.deferred_report(st), self.comm)
             j = min(st.fail_iter, self.m - 1)
             a, ah = E.jop.a, E.jop.a_halo
             # the failing state is a + sigma V[j] with V[j] materialised

@@ -853,3 +853,32 @@ def test_l2_window_released_with_the_context(P):
     del ctx                          # emhd_ctx_destroy
     torch.cuda.synchronize()
     assert limit() == lim0
+
+
+def test_step_rhs_admissibility_names_the_reference_cell(P):
+    """An EpiRK5P1 trial step whose stage state is inadmissible: the failing launch is one of
+    the step's deferred RHS / remainder launches (status read later, not an Arnoldi iteration);
+    the raised AdmissibilityError carries the reference's message — the first failing launch's
+    ghost-padded argmin cell and value (mhd.py:111-131) — as the oracle's step raises it."""
+    from oracle import epirk_cpu, stencil
+    g = P.ReconnectionSpec().grid(32, 32)
+    prm = P.MhdParams(mu=1e-3, eta=1e-3, kappa=1e-3)
+    U = P.reconnection_ic(g, params=prm)
+    rho = U[0]
+    U[7] = P.energy_from(rho, U[1:4] / rho, U[4:7], 1e-3 * 0.5 * rho, prm)
+    bc = P.default_bc("reconnection")
+    y0 = U.reshape(-1)
+    for h in (8.0, 1.6, 0.32):
+        with pytest.raises(stencil.InadmissibleState) as want:
+            epirk_cpu.step5p1(stencil.rhs_closure(prm, g, bc), y0, h, 1e-6)
+        with pytest.raises(P.AdmissibilityError) as got:
+            P.epirk5p1_step(P.make_rhs(prm, g, bc), y0, h, 1e-6)
+        # same kind and cell; the value of a stage state agrees to the trajectory bar (the stage
+        # comes out of an FD-Krylov projection, 1e-8 relative, not bitwise)
+        gk, gv = str(got.value).rsplit(":", 1)
+        wk, wv = str(want.value).rsplit(":", 1)
+        assert gk.split(" at ")[0] == wk.split(" at ")[0], (h, str(got.value), str(want.value))
+        assert abs(float(gv) - float(wv)) <= 1e-6 * abs(float(wv)), (h, gv, wv)
+        if gk != wk:
+            # a different cell only on a round-off tie of this x-symmetric state's minimum
+            assert abs(float(gv) - float(wv)) <= 1e-12 * abs(float(wv)), (h, gv, wv)
