@@ -363,8 +363,13 @@ static bool two_raw_rows(int mode, const StencilParams& P, const StencilPath& se
   return (long long)P.nx * P.ny <= 1536LL * 1024;
 }
 
+// HW (with two staged rows, 2 CTAs/SM): one extra warp per CTA does the strip's halo work (the
+// four halo columns' primitives and the two halo y-fluxes) beside the TY column threads, so no
+// column warp carries extra work into the per-row barrier
 template <int TY, int MODE, bool AUG, int FXY, int NR>
-__global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(const StencilParams P) {
+__global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY)
+    stencil_kernel(const StencilParams P) {
+  constexpr bool HW = NR == 2;
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
   extern __shared__ double smem[];
@@ -381,7 +386,8 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
   unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NRAW * NARR * NF * QW);
 
   pdl_sync();
-  const int t = threadIdx.x;
+  const int tid = threadIdx.x;
+  const int t = HW ? tid - 32 : tid;               // column thread index (< 0: the halo warp)
   const int j0 = blockIdx.x * TY;
   // output rows [i0, i1) of this CTA: a chunk of [row_lo, row_hi) (rows_mode 0/1), or the
   // two edge row pairs {0, 1} / {nx-2, nx-1} (rows_mode 2, the launch that waits for the halo)
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
   }
   // the launch's bookkeeping (RHS count, evals, augmented tail) is done by the counting launch
   const bool head = P.count && blockIdx.x == 0 && blockIdx.y == 0;
-  const bool lead = head && t == 0;
+  const bool lead = head && tid == 0;
   if (P.skip && *P.skip != 0.0) {
     // cancelled look-ahead iteration (its gate was written by an earlier launch)
     if (lead && P.evals) *P.evals = 0.0;
@@ -416,10 +422,10 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
       // the previous iteration broke down: this launch was queued ahead of the host's
       // breakdown check; leave no trace (zero output, no flags, no RHS count)
       for (long long r = i0; r < i1; ++r)
-        if (t < min(TY, P.ny - j0))
+        if (t >= 0 && t < min(TY, P.ny - j0))
 #pragma unroll
           for (int f = 0; f < NF; ++f) P.out[r * P.ny + j0 + t + (long long)f * P.nx * P.ny] = 0.0;
-      if (head && t < P.p) P.out[P.n_top + t] = 0.0;
+      if (head && t >= 0 && t < P.p) P.out[P.n_top + t] = 0.0;
       if (lead && P.evals) *P.evals = 0.0;
       return;
     }
@@ -455,7 +461,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
   if (skip_stencil) {
     // zero direction: Jv = 0 without an RHS evaluation (fdjac.py:41-42)
     for (int r = i0; r < i1; ++r) {
-      if (t < ncols_out) {
+      if (t >= 0 && t < ncols_out) {
         const long long o = (long long)r * P.ny + j0 + t;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
@@ -474,13 +480,14 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
     // that compute the halo y-fluxes (slots 1 and TY+2: threads 0 and 3) own those columns'
     // centre quantities
     const int cmain = t + 2;
-    const int cextra = t == 0 ? 1 : t == 1 ? 0 : t == 2 ? TY + 3 : t == 3 ? TY + 2 : -1;
+    const int cextra = HW ? (tid == 0 ? 1 : tid == 1 ? 0 : tid == 2 ? TY + 3 : tid == 3 ? TY + 2 : -1)
+                          : (t == 0 ? 1 : t == 1 ? 0 : t == 2 ? TY + 3 : t == 3 ? TY + 2 : -1);
     auto col_ok = [&](int c) { int j = j0 - 2 + c; return j >= -2 && j <= P.ny + 1; };
     bool fm, fe = false;
     const int jm = map_ghost(j0 - 2 + cmain, P.ny, P.bcy, fm);
     const int je = cextra >= 0 ? map_ghost(j0 - 2 + cextra, P.ny, P.bcy, fe) : 0;
     const unsigned ymm = fm ? 0x80000000u : 0u, yme = fe ? 0x80000000u : 0u;
-    const bool okm = col_ok(cmain), oke = cextra >= 0 && col_ok(cextra);
+    const bool okm = t >= 0 && col_ok(cmain), oke = cextra >= 0 && col_ok(cextra);
 
     // prologue: primitives of rows i0-2 and i0-1
     for (int r = i0 - 2; r < i0; ++r) {
@@ -500,7 +507,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
     // software pipeline: the raw inputs of row r+1 stream into the shared raw row while the
     // fluxes of row r-1 and outputs of row r-2 are computed
     double fa_pre[NF];                       // F(a) of the next output row, one step ahead
-    if (MODE != MODE_RHS && t < ncols_out) {
+    if (MODE != MODE_RHS && t >= 0 && t < ncols_out) {
       const unsigned o = (unsigned)i0 * P.ny + j0 + t;
 #pragma unroll
       for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + (o + f * plane));
@@ -513,7 +520,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
     const bool bulk = P.tma && j0 >= 2 && j0 + TY + 2 <= P.ny;
     constexpr int SLOT = NARR * NF * QW;     // doubles per raw row slot
     if (bulk) {
-      if (t == 0) {
+      if (tid == 0) {
         for (int k = 0; k < NRAW; ++k) mbar_init(rbar + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         for (int k = 0; k < NRAW && i0 + k <= i1 + 1; ++k)
@@ -581,7 +588,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
       // row r-3 (last read by the outputs of row r-3, previous step); centre quantities
       // are private to their thread.
       __syncthreads();
-      if (bulk && t == 0 && r + NRAW <= i1 + 1) {
+      if (bulk && tid == 0 && r + NRAW <= i1 + 1) {
         // generic-proxy reads of the row (before the barrier) precede the async-proxy refill
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         fetch_row_bulk<MODE, QW>(P, row_ref(P, r + NRAW), j0 - 2, sraw, rbar + rk % NRAW);
@@ -596,7 +603,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
         double* gyr = gyring + ((rf + 2) % 2) * NF * GYW;
         const bool out_row = (rf >= i0 && rf < i1);
         double gy[NF];
-        if (t < ncols_out) {
+        if (t >= 0 && t < ncols_out) {
           flux_cell<FXY>(P, qm, q0, qp, c0, cmain, QW, true, out_row, gxC, gy);
           if (out_row) {
 #pragma unroll
@@ -608,8 +615,13 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
           // j0+ncols (thread 3's extra slot TY+2 on a full strip, else the main slot of
           // thread ncols): each computed by the owner of that column's centre quantities
           int cs = -1, gslot = 0;
-          if (t == 0) { cs = 1; gslot = 0; }
-          if (t == (ncols_out == TY ? 3 : ncols_out)) { cs = ncols_out + 2; gslot = ncols_out + 1; }
+          // (HW: the halo warp's lanes 0 and 3 own slots 1 and TY+2; a ragged strip's right
+          // halo column is column thread ncols's main slot)
+          if ((HW ? tid : t) == 0) { cs = 1; gslot = 0; }
+          if (ncols_out == TY ? (HW ? tid == 3 : t == 3) : t == ncols_out) {
+            cs = ncols_out + 2;
+            gslot = ncols_out + 1;
+          }
           if (cs >= 0) {
             double gdummy[NF];
             flux_cell<FXY>(P, qm, q0, qp, c0, cs, QW, false, true, gdummy, gy);
@@ -621,7 +633,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
       // ---- output row ro = r - 2: x-fluxes of rows ro+1 (gxC) and ro-1 (gxA) are this
       // thread's own registers; y-fluxes of row ro come from the ring (previous step)
       const int ro = r - 2;
-      if (ro >= i0 && t < ncols_out) {
+      if (ro >= i0 && t >= 0 && t < ncols_out) {
         const double* gyr = gyring + ((ro + 2) % 2) * NF * GYW;
         const unsigned o = (unsigned)ro * P.ny + j0 + t;
         unsigned nfmask = 0;                 // bit f: F of field f is inf / nan
@@ -660,7 +672,7 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
   }
 
   // tail of the augmented output: bottom = upshift(q) (krylov.py:271-272); v_j tail
-  if (AUG && head && t < P.p) {
+  if (AUG && head && t >= 0 && t < P.p) {
     double nxt = 0.0;
 #pragma unroll
     for (int k = 1; k < 5; ++k) if (k == t + 1 && k < P.p) nxt = qv[k];
@@ -676,12 +688,12 @@ __global__ void __launch_bounds__(TY, NR == 2 ? 2 : 384 / TY) stencil_kernel(con
   // status aggregation: one atomic per CTA
   __shared__ int s_flag;
   __shared__ unsigned long long s_bad;
-  if (t == 0) { s_flag = 0; s_bad = ~0ull; }
+  if (tid == 0) { s_flag = 0; s_bad = ~0ull; }
   __syncthreads();
   if (flag) atomicOr(&s_flag, flag);
   if (bad != ~0ull) atomicMin(&s_bad, bad);
   __syncthreads();
-  if (t == 0) {
+  if (tid == 0) {
     if (s_flag) {
       atomicOr(&P.st->flags, s_flag);
       atomicMin(&P.st->fail_iter, P.epoch);
@@ -1060,7 +1072,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
   if (P.rows_per_cta <= 0) {
     // exactly one wave of resident CTAs (all CTAs carry equal work)
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, TY, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NRAW == 2 ? TY + 32 : TY, sm);
     const int strips = (P.ny + TY - 1) / TY;
     const int target = (occ < 1 ? 1 : occ) * num_sms;
     // floor: strips x chunks must not exceed one wave of resident CTAs
@@ -1084,7 +1096,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
     used->bulk = P.tma && P.ny >= 2 * TY + 2;
   }
   dim3 grid((P.ny + TY - 1) / TY, P.rows_mode == 2 ? 2 : (nrows + P.rows_per_cta - 1) / P.rows_per_cta);
-  return launch_pdl(k, grid, dim3(TY), sm, s, P);
+  return launch_pdl(k, grid, dim3(NRAW == 2 ? TY + 32 : TY), sm, s, P);
 }
 
 template <int TY, int FXY>
