@@ -117,7 +117,7 @@ typedef struct emhd_stencil_path {
                         when 16-byte aligned; 0 = per-thread cp.async everywhere */
   int min_rows;      /* >= 1 */
   int tile_rows;
-  int raw_rows;      /* marching normalised Jv: input rows staged ahead, 1 or 2 (0 = by grid size) */
+  int raw_rows;      /* marching normalised Jv: input rows staged ahead, 1 or 2 (0 = 2) */
 } emhd_stencil_path;
 int emhd_set_stencil_path(emhd_ctx* ctx, const emhd_stencil_path* sel);
 int emhd_get_stencil_path(emhd_ctx* ctx, emhd_stencil_path* out);

@@ -352,15 +352,14 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
 #undef QV
 }
 
-// raw input rows in flight per CTA (NR): row r+NR is requested while row r is consumed.  Two
-// (2 CTAs/SM, one more row of prefetch) pay for the Arnoldi-loop stencil (MODE_JVN) on grids of
-// up to ~1.5 M cells, where a CTA marches few rows: 1024^2 82.4 us vs 87.5 with one; from 2048^2
-// on one row at 3 CTAs/SM is faster (2048^2 303 vs 311 us, 4096^2 1233 vs 1348 us); three rows:
-// 1024^2 93.6 us.  RHS / Jv always one (Jv 1024^2 69 us vs 72).
+// raw input rows in flight per CTA (NR): row r+NR is requested while row r is consumed.  The
+// Arnoldi-loop stencil (MODE_JVN) takes two (2 CTAs/SM, one more row of prefetch, plus the
+// halo warp): 1024^2 78.9 us vs 87.5 with one row at 3 CTAs/SM, 2048^2 301.5 vs 312.9,
+// 4096^2 1224 vs 1218 (three rows: 1024^2 93.6 us).  RHS / Jv keep one (Jv 1024^2 69 us vs 72).
 static bool two_raw_rows(int mode, const StencilParams& P, const StencilPath& sel) {
+  (void)P;
   if (mode != MODE_JVN) return false;
-  if (sel.raw_rows == 1 || sel.raw_rows == 2) return sel.raw_rows == 2;
-  return (long long)P.nx * P.ny <= 1536LL * 1024;
+  return sel.raw_rows != 1;
 }
 
 // HW (with two staged rows, 2 CTAs/SM): one extra warp per CTA does the strip's halo work (the

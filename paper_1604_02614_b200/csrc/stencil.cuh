@@ -50,7 +50,7 @@ struct StencilPath {
   int bulk;          // marching: interior strips stage raw rows with bulk async copies (when aligned)
   int min_rows;      // auto: floor of rows per CTA
   int tile_rows;     // auto: 2D tiles when a marching CTA would get fewer rows than this
-  int raw_rows;      // marching MODE_JVN: raw rows staged ahead (0 auto by grid size, 1, 2)
+  int raw_rows;      // marching MODE_JVN: raw rows staged ahead (0 auto = 2, 1, 2)
 };
 
 StencilPath stencil_path_defaults();   // EMHD_STENCIL_TY / _TMA / _TILE_ROWS, EMHD_MIN_ROWS
