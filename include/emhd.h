@@ -121,6 +121,12 @@ typedef struct emhd_stencil_path {
 } emhd_stencil_path;
 int emhd_set_stencil_path(emhd_ctx* ctx, const emhd_stencil_path* sel);
 int emhd_get_stencil_path(emhd_ctx* ctx, emhd_stencil_path* out);
+/* Small grids (every CTA of the streaming kernels co-resident: up to ~128^2 cells x 8 fields):
+ * emhd_arnoldi_iter runs the orthogonalisation of krylov.py:151-166 — dots, update, the
+ * selective re-orthogonalisation decision and, when needed, the second pass — as ONE launch
+ * with grid barriers instead of four, bit-identical to the separate launches.  on = 0 turns it
+ * off for this context (default: EMHD_FUSED_ORTH, 1). */
+int emhd_set_fused_orth(emhd_ctx* ctx, int on);
 /* what the last stencil launch on ctx ran: kernel (1 marching / 2 tile), rows_per_cta and strip
  * of a marching launch, bulk = 1 when some interior strip staged its rows by bulk copies */
 int emhd_last_stencil(emhd_ctx* ctx, emhd_stencil_path* out);

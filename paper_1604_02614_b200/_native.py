@@ -76,6 +76,7 @@ _SIGS = {
     "emhd_status_clear_errors": (c_int, [c_vp]),
     "emhd_set_stencil_path": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
     "emhd_get_stencil_path": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
+    "emhd_set_fused_orth": (c_int, [c_vp, c_int]),
     "emhd_last_stencil": (c_int, [c_vp, ctypes.POINTER(StencilPath)]),
     "emhd_rhs": (c_int, [c_vp, P, P, P]),
     "emhd_jv": (c_int, [c_vp, P, P, P, P, P, P, P]),

@@ -41,6 +41,8 @@ struct emhd_ctx {
   size_t l2_limit_prev = 0;                   // ... from this value (restored on destroy)
   StencilPath path{};                         // stencil launch selection (emhd_set_stencil_path)
   StencilPath last{};                         // what the last stencil launch ran
+  bool fused_orth = true;                     // small grids: one-launch orthogonalisation
+                                              // (emhd_set_fused_orth; default EMHD_FUSED_ORTH)
   // slab-rank collectives (emhd_comm_init_*): all-reduces on `stream`, halo exchange on
   // halo_stream into hrecv, overlapped with the interior rows of the stencil that needs it
   SlabComm* comm = nullptr;
@@ -164,6 +166,10 @@ extern "C" int emhd_ctx_create(emhd_ctx** out, const emhd_geometry* g, const emh
   if (rc) { emhd_ctx_destroy(c); return rc; }
   fill_base(c);
   c->path = stencil_path_defaults();
+  {
+    const char* e = getenv("EMHD_FUSED_ORTH");
+    c->fused_orth = e ? atoi(e) != 0 : true;
+  }
   emhd_status_reset(c);
   rc = cerr(cudaStreamSynchronize(0));
   *out = c;
@@ -260,6 +266,12 @@ extern "C" int emhd_set_stencil_path(emhd_ctx* c, const emhd_stencil_path* sel) 
   c->path.kernel = sel->kernel; c->path.rows_per_cta = sel->rows_per_cta; c->path.strip = sel->strip;
   c->path.bulk = sel->bulk != 0; c->path.min_rows = sel->min_rows; c->path.tile_rows = sel->tile_rows;
   c->path.raw_rows = sel->raw_rows;
+  return EMHD_OK;
+}
+
+extern "C" int emhd_set_fused_orth(emhd_ctx* c, int on) {
+  if (!c) return EMHD_ERR_ARG;
+  c->fused_orth = on != 0;
   return EMHD_OK;
 }
 
@@ -1132,6 +1144,15 @@ static int arnoldi_iter(emhd_ctx* c, const void* args, int j, bool gated) {
     }
   }
   const double vb = 8.0 * (double)A->len_upd;
+  if (c->fused_orth && orth_small_fits(A->len_upd, c->num_sms)) {
+    // small grids: multi-dot, update, decision and (when needed) the second pass in ONE launch
+    // (grid barriers between the phases; bit-identical to the separate launches below)
+    Reorth r = r1;
+    ProfScope ps(c, EMHD_K_MULTIDOT, (2 * nv + 3) * vb, skip);
+    return cerr(launch_orth_small(out, A->V, A->ldv, nv, A->len_upd, A->len_dot, A->n_top, k,
+                                  c->partials + c->partials_len / 2, c->ticket + 4, A->d1, A->d2,
+                                  A->nrm, c->stream, F, skip, r));
+  }
   {
     ProfScope ps(c, EMHD_K_MULTIDOT, (nv + 1) * vb, skip);
     rc = cerr(launch_multidot(out, A->V, A->ldv, nv, A->len_dot, 1, k, A->d1, c->stream, skip));

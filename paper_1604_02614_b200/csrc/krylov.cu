@@ -32,6 +32,8 @@ constexpr int EPT = 2;           // elements per double2
 constexpr int TILE = KT * EPT;   // 512 elements per combine tile
 constexpr int NWARP = KT / 32;
 
+static int grid_for_len(long long len, int tile, int num_sms);
+
 // Last-CTA deterministic reduction of partials[nval][G] -> out[nval].
 // kind[v]: 0 = sum, 1 = max.  Returns true in the CTA that did it.
 __device__ bool finish_partials(const double* partials, int nval, int G, const int* kinds,
@@ -353,6 +355,309 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
   }
 }
 
+// ---- small grids: the whole orthogonalisation of one Arnoldi iteration in ONE launch --------
+// On a 64^2 .. 128^2 grid the four launches above (multi-dot, update, gated multi-dot, gated
+// update) are 2-7 us of launch ramp, partial reduction and tail each against ~1 us of memory
+// traffic.  Here the same phases run in one kernel separated by a grid barrier; every CTA sums
+// the per-CTA partials itself (in CTA order, exactly as the last CTA of the separate kernels
+// does) and therefore takes the selective re-orthogonalisation decision without another
+// launch.  Tile ownership, partial layout and summation order are those of multidot_kernel /
+// update_kernel for the same length, so H, w and every scalar are BIT-IDENTICAL to the
+// four-launch path (tested).  The launcher only uses it when all CTAs are co-resident
+// (grid <= 2 CTAs per SM), which the barrier needs.
+//
+// Grid barrier: arrival counter + generation word, self-resetting (no host bookkeeping, and a
+// gated launch that returns early never touches it).
+// Release / acquire at gpu scope on the two words instead of full memory fences: the CTA's
+// stores are ordered before thread 0's arrival by the CTA barrier (cumulativity), the
+// consumers' loads after its acquire of the new generation.
+__device__ __forceinline__ void grid_bar(unsigned int* bar, unsigned int G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int gen, prev;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(gen) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(bar) : "memory");
+    if (prev == G - 1u) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;\n" ::"l"(bar), "r"(0u) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar + 1) : "memory");
+    } else {
+      unsigned int now;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(now) : "l"(bar + 1) : "memory");
+      } while (now == gen);
+    }
+  }
+  __syncthreads();
+}
+
+// the last-CTA sums of finish_partials / finish_partials_maxidx, done by every CTA into shared
+// memory: dst[v] = sum (or max for v == max_idx) over c < G of partials[v][c], lanes striding
+// the CTAs and a warp butterfly on top (the same association as the separate kernels)
+__device__ __forceinline__ void reduce_partials_all(const double* partials, int nval, int G, int max_idx,
+                                                    double* dst) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int v = warp; v < nval; v += NWARP) {
+    const bool mx = v == max_idx;
+    double acc = 0.0;
+    for (int c = lane; c < G; c += 32) {
+      const double x = __ldcg(partials + (size_t)v * G + c);
+      acc = mx ? fmax(acc, x) : acc + x;
+    }
+    acc = mx ? warp_max(acc) : warp_sum(acc);
+    if (lane == 0) dst[v] = acc;
+  }
+  __syncthreads();
+}
+
+struct OrthSmallArgs {
+  double* w;
+  const double* V;
+  long long ldv;
+  int nvec;
+  long long len_upd, len_dot, len_max;
+  int Gm, Gu;                 // grids of the separate multi-dot / update kernels for these lengths
+  double* partials;           // per-CTA partials of the dot phases
+  double* partials_b;         // ... of the update phases (alternating buffers: one barrier per phase)
+  unsigned int* bar;          // {arrivals, generation}
+  double* d1;                 // out: h1[0:nvec], ||w||^2
+  double* d2;                 // out: re-projection dots, ||w1||^2, max|w1_top|
+  double* nrm;                // out (pass 2): ||w||^2, max|w_top|
+  const double* skip;         // cancelled look-ahead iteration
+  FinishArgs fin;
+  Reorth ro;                  // eta2 > 0 and gate_out set: selective; else always two passes
+};
+
+// <w, V_i> partials of this CTA (multidot_kernel<2, 4>'s loop; COH: w was written by other CTAs
+// of this launch, so it is read through L2)
+template <bool COH>
+__device__ __forceinline__ void orth_dots(const OrthSmallArgs& A, int self, double* s_acc) {
+  constexpr int VEC = 2, U = 4;
+  constexpr int TL = KT * 2 * VEC;
+  const int nvec = A.nvec, nval = nvec + self;
+  for (int k = threadIdx.x; k < nval * NWARP; k += KT) s_acc[k] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double selfacc = 0.0;
+  const long long ntiles = (A.len_dot + TL - 1) / TL;
+  if ((int)blockIdx.x < A.Gm) {
+    for (long long tl = blockIdx.x; tl < ntiles; tl += A.Gm) {
+      const long long e0 = tl * TL + 2LL * threadIdx.x;
+      double2 wv[VEC];
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        const long long e = e0 + (long long)q * 2 * KT;
+        if (COH) {
+          wv[q] = make_double2(0.0, 0.0);
+          if (e + 1 < A.len_dot) wv[q] = __ldcg(reinterpret_cast<const double2*>(A.w + e));
+          else if (e < A.len_dot) wv[q].x = __ldcg(A.w + e);
+        } else {
+          wv[q] = ld2_stream(A.w, e, A.len_dot);
+        }
+        selfacc = fma(wv[q].x, wv[q].x, fma(wv[q].y, wv[q].y, selfacc));
+      }
+      for (int i = 0; i < nvec; i += U) {
+        double2 x[U][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < VEC; ++q)
+            x[u][q] = (i + u < nvec) ? ld2_stream(A.V + (size_t)(i + u) * A.ldv, e0 + (long long)q * 2 * KT, A.len_dot)
+                                     : make_double2(0.0, 0.0);
+        double d[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          d[u] = 0.0;
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) d[u] = fma(wv[q].x, x[u][q].x, fma(wv[q].y, x[u][q].y, d[u]));
+        }
+        warp_reduce_multi<U>(d, lane);
+        if ((lane & (32 / U - 1)) == 0) {
+          const int u = multi_index<U>(lane);
+          if (i + u < nvec) s_acc[(i + u) * NWARP + warp] += d[0];
+        }
+      }
+    }
+    if (self) {
+      selfacc = warp_sum(selfacc);
+      if (lane == 0) s_acc[nvec * NWARP + warp] = selfacc;
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nval; v += KT) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < NWARP; ++q) acc += s_acc[v * NWARP + q];
+      A.partials[(size_t)v * A.Gm + blockIdx.x] = acc;
+    }
+  }
+}
+
+// w -= V h on this CTA's tiles (update_kernel<MODE, 8>'s loop).  MODE 0: optional re-projection
+// dots, ||w1||^2, max|w1_top| partials; MODE 1: ||w||^2, max|w_top| partials (w is this
+// thread's own pass-1 result: a plain load, never the read-only path)
+template <int MODE>
+__device__ __forceinline__ void orth_update(const OrthSmallArgs& A, const double* s_h, bool reproj,
+                                            double* s_acc) {
+  constexpr int U = 8;
+  constexpr int TL = KT * 2;
+  const int nvec = A.nvec;
+  const int nval = MODE == 0 ? nvec + 2 : 2;
+  for (int k = threadIdx.x; k < nval * NWARP; k += KT) s_acc[k] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double ss = 0.0, mx = 0.0;
+  const long long ntiles = (A.len_upd + TL - 1) / TL;
+  for (long long k = blockIdx.x; k < ntiles; k += A.Gu) {
+    const long long tl = ntiles - 1 - k;
+    const long long e = tl * TL + 2LL * threadIdx.x;
+    const bool full = e + 1 < A.len_upd;
+    double2 wv = make_double2(0.0, 0.0);
+    if (MODE == 0) wv = ld2(A.w, e, A.len_upd);
+    else if (full) wv = *reinterpret_cast<const double2*>(A.w + e);
+    else if (e < A.len_upd) wv.x = A.w[e];
+    for (int i = 0; i < nvec; i += U) {
+      double2 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        x[u] = (i + u < nvec) ? ld2(A.V + (size_t)(i + u) * A.ldv, e, A.len_upd) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i + u < nvec) {
+          const double hh = s_h[i + u];
+          wv.x = fma(-hh, x[u].x, wv.x);
+          wv.y = fma(-hh, x[u].y, wv.y);
+        }
+      }
+    }
+    if (full) *reinterpret_cast<double2*>(A.w + e) = wv;
+    else if (e < A.len_upd) A.w[e] = wv.x;
+    const double dx = (e < A.len_dot) ? wv.x : 0.0, dy = (e + 1 < A.len_dot) ? wv.y : 0.0;
+    if (MODE == 0 && reproj) {
+      for (int i = (nvec - 1) / U * U; i >= 0; i -= U) {
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          x[u] = (i + u < nvec) ? ld2_stream(A.V + (size_t)(i + u) * A.ldv, e, A.len_upd) : make_double2(0.0, 0.0);
+        double d[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d[u] = fma(dx, x[u].x, dy * x[u].y);
+        warp_reduce_multi<U>(d, lane);
+        if ((lane & (32 / U - 1)) == 0) {
+          const int u = multi_index<U>(lane);
+          if (i + u < nvec) s_acc[(i + u) * NWARP + warp] += d[0];
+        }
+      }
+    }
+    ss = fma(dx, dx, fma(dy, dy, ss));
+    const double mxx = (e < A.len_max) ? fabs(wv.x) : 0.0;
+    const double mxy = (e + 1 < A.len_max) ? fabs(wv.y) : 0.0;
+    mx = fmax(mx, fmax(mxx, mxy));
+  }
+  ss = warp_sum(ss);
+  mx = warp_max(mx);
+  if (MODE == 1) {
+    if (lane == 0) { s_acc[0 * NWARP + warp] = ss; s_acc[1 * NWARP + warp] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int q = 0; q < NWARP; ++q) { a += s_acc[q]; b = fmax(b, s_acc[NWARP + q]); }
+      A.partials_b[blockIdx.x] = a;
+      A.partials_b[(size_t)A.Gu + blockIdx.x] = b;
+    }
+  } else {
+    if (lane == 0) { s_acc[nvec * NWARP + warp] = ss; s_acc[(nvec + 1) * NWARP + warp] = mx; }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nval; v += KT) {
+      double acc = 0.0;
+      if (v == nvec + 1) {
+#pragma unroll
+        for (int q = 0; q < NWARP; ++q) acc = fmax(acc, s_acc[v * NWARP + q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NWARP; ++q) acc += s_acc[v * NWARP + q];
+      }
+      A.partials_b[(size_t)v * A.Gu + blockIdx.x] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(KT, 2) orth_small_kernel(const OrthSmallArgs A) {
+  pdl_sync();
+  if (A.skip && *A.skip != 0.0) return;          // cancelled look-ahead iteration (all CTAs agree)
+  extern __shared__ double sm[];
+  const int nvec = A.nvec;
+  double* s_h = sm;                                // [nvec + 2] reduced values of the current phase
+  double* s_acc = sm + ((nvec + 3) & ~1);          // [(nvec + 2)][NWARP]
+  const unsigned int G = gridDim.x;
+  // pass 1 dots: h1 = V^T w, ||w||^2
+  orth_dots<false>(A, 1, s_acc);
+  grid_bar(A.bar, G);
+  reduce_partials_all(A.partials, nvec + 1, A.Gm, -1, s_h);
+  const double selfdot = s_h[nvec];
+  if (blockIdx.x == 0)
+    for (int v = threadIdx.x; v <= nvec; v += KT) A.d1[v] = s_h[v];
+  // pass 1 update (+ re-projection dots unless predicted unnecessary), ||w1||^2, max|w1_top|
+  const bool selective = A.ro.eta2 > 0.0 && A.ro.gate_out;
+  const bool reproj = !(A.ro.predict && A.ro.predict[0] != 0.0 && A.ro.predict[1] != 0.0);
+  orth_update<0>(A, s_h, reproj, s_acc);
+  grid_bar(A.bar, G);
+  reduce_partials_all(A.partials_b, nvec + 2, A.Gu, nvec + 1, s_h);   // s_h: h2 (or zeros), r
+  const bool skip2 = selective && s_h[nvec] >= A.ro.eta2 * selfdot;
+  if (blockIdx.x == 0) {
+    for (int v = threadIdx.x; v < nvec + 2; v += KT) A.d2[v] = s_h[v];
+    if (selective && threadIdx.x == 0) {
+      *A.ro.gate_out = skip2 ? 1.0 : 0.0;
+      if (A.ro.gate_md2) *A.ro.gate_md2 = (skip2 || reproj) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (skip2) {
+      FinishArgs F1 = A.fin;
+      F1.h2 = nullptr;
+      finish_column(F1, A.d2 + nvec);
+    }
+  }
+  if (skip2) return;
+  // (each phase's partials are read only between its own barrier and the next one, and the dot
+  // and update phases alternate between two buffers: one barrier per phase)
+  if (!reproj) {
+    // mispredicted: the re-projection dots h2 = V^T w1 were not computed by the update
+    orth_dots<true>(A, 0, s_acc);
+    grid_bar(A.bar, G);
+    reduce_partials_all(A.partials, nvec, A.Gm, -1, s_h);
+    if (blockIdx.x == 0)
+      for (int v = threadIdx.x; v < nvec; v += KT) A.d2[v] = s_h[v];
+  }
+  // pass 2: w -= V h2, ||w||^2, max|w_top|, column bookkeeping
+  orth_update<1>(A, s_h, false, s_acc);
+  grid_bar(A.bar, G);
+  if (blockIdx.x == 0) {
+    reduce_partials_all(A.partials_b, 2, A.Gu, 1, s_h);
+    if (threadIdx.x < 2) A.nrm[threadIdx.x] = s_h[threadIdx.x];
+    __syncthreads();
+    if (A.fin.H) finish_column(A.fin, A.nrm);
+  }
+}
+
+bool orth_small_fits(long long len_upd, int num_sms) {
+  return grid_for_len(len_upd, KT * 2, num_sms) <= 2 * num_sms;
+}
+
+cudaError_t launch_orth_small(double* w, const double* V, long long ldv, int nvec, long long len_upd,
+                              long long len_dot, long long len_max, KWork& wk, double* partials_b,
+                              unsigned int* bar, double* d1, double* d2, double* nrm, cudaStream_t s,
+                              FinishArgs fin, const double* skip, Reorth ro) {
+  OrthSmallArgs A;
+  A.w = w; A.V = V; A.ldv = ldv; A.nvec = nvec;
+  A.len_upd = len_upd; A.len_dot = len_dot; A.len_max = len_max;
+  A.Gm = grid_for_len(len_dot, KT * 4, wk.num_sms);
+  A.Gu = grid_for_len(len_upd, KT * 2, wk.num_sms);
+  A.partials = wk.partials; A.partials_b = partials_b; A.bar = bar;
+  A.d1 = d1; A.d2 = d2; A.nrm = nrm; A.skip = skip; A.fin = fin; A.ro = ro;
+  const int G = A.Gu > A.Gm ? A.Gu : A.Gm;
+  if (G > 2 * wk.num_sms) return cudaErrorInvalidConfiguration;   // the grid barrier needs co-residency
+  const size_t sm = sizeof(double) * ((size_t)((nvec + 3) & ~1) + (size_t)(nvec + 2) * NWARP);
+  return launch_pdl(orth_small_kernel, dim3(G), dim3(KT), sm, s, A);
+}
+
 // slab ranks, pass 2 skipped: w1 is final, so its edge rows go to the neighbours' halo buffers
 // here (otherwise emhd_update_push stores the edges of the final w)
 __global__ void push_edges_kernel(const double* __restrict__ w, const HaloPush H, const double* gate) {
@@ -495,7 +800,7 @@ cudaError_t launch_evals_discount(const double* evals, int count, DevStatus* st,
 
 // Up to 4 CTAs per SM, every CTA the same number of tiles (1024 tiles on 592 CTAs would leave
 // 160 CTAs with one tile while the rest do two: 512 CTAs of two tiles finish at the same time)
-static int grid_for(long long len, int tile, int num_sms) {
+static int grid_for_len(long long len, int tile, int num_sms) {
   long long tiles = (len + tile - 1) / tile;
   if (tiles < 1) tiles = 1;
   const long long g = 4LL * num_sms;
@@ -503,6 +808,7 @@ static int grid_for(long long len, int tile, int num_sms) {
   const long long per = (tiles + g - 1) / g;
   return (int)((tiles + per - 1) / per);
 }
+static int grid_for(long long len, int tile, int num_sms) { return grid_for_len(len, tile, num_sms); }
 
 cudaError_t launch_multidot(const double* w, const double* V, long long ldv, int nvec, long long len_dot,
                             int self, KWork& wk, double* out, cudaStream_t s, const double* skip,

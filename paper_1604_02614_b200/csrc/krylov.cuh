@@ -55,6 +55,14 @@ cudaError_t launch_update(double* w, const double* V, long long ldv, int nvec, c
                           long long len_upd, long long len_dot, long long len_max, int mode,
                           KWork& wk, double* out, cudaStream_t s, FinishArgs fin = FinishArgs{},
                           const double* skip = nullptr, Reorth ro = Reorth{});
+// one-launch orthogonalisation of an Arnoldi iteration on small grids (bit-identical to
+// launch_multidot + launch_update (+ gated second pass)); partials_b: a second partials buffer
+// ((nvec + 2) * 2 * num_sms doubles); bar: {arrivals, generation}, zeroed once
+bool orth_small_fits(long long len_upd, int num_sms);
+cudaError_t launch_orth_small(double* w, const double* V, long long ldv, int nvec, long long len_upd,
+                              long long len_dot, long long len_max, KWork& wk, double* partials_b,
+                              unsigned int* bar, double* d1, double* d2, double* nrm, cudaStream_t s,
+                              FinishArgs fin, const double* skip, Reorth ro);
 cudaError_t launch_push_edges(const double* w, const HaloPush& H, const double* gate, cudaStream_t s);
 cudaError_t launch_reorth_decide(FinishArgs fin, const double* r, int nvec, double eta2, double* gate,
                                  cudaStream_t s, double* gate_md2 = nullptr, const double* predict = nullptr);

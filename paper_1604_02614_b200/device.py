@@ -130,6 +130,11 @@ class Ctx:
             N.check(self.lib.emhd_set_stencil_path(self.h, ctypes_byref(sp)), "set_stencil_path")
         return {k: getattr(sp, k) for k, _ in N.StencilPath._fields_}
 
+    def fused_orth(self, on):
+        """Small grids: run an Arnoldi iteration's orthogonalisation as one launch (default on;
+        off: the separate multi-dot / update launches, bit-identical)."""
+        N.check(self.lib.emhd_set_fused_orth(self.h, int(bool(on))), "set_fused_orth")
+
     def last_stencil(self):
         """What the last stencil launch on this context ran (kernel 1 marching / 2 tile, ...)."""
         sp = N.StencilPath()
