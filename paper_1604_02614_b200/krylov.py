@@ -236,12 +236,28 @@ class _Process:
         else:
             self.ld = _ld(self.naug)
             self.V = torch.empty((self.m_cap + 1, self.ld), dtype=D.F64, device=D.device())
-        self.w = [torch.empty(self.ld, dtype=D.F64, device=D.device()) for _ in range(2)]
         k = self.m_cap + 4
         hw = max(self.m_cap, 1)
-        # one zero-filled block for H and every small scalar area (a single fill launch)
-        self._small = torch.zeros((self.m_cap + 1) * hw + 3 * k + 2 + 5 * (self.m_cap + 1) + 4,
-                                  dtype=D.F64, device=D.device())
+        nsmall = (self.m_cap + 1) * hw + 3 * k + 2 + 5 * (self.m_cap + 1) + 4
+        # projections inside a step run one after the other on the context's stream: their work
+        # vectors, small device block and pinned readback buffers are allocated once per
+        # (cap, ld) and reused (stream order protects the device side, every host read follows
+        # a sync) — a dozen tensor constructions per projection otherwise, on host-bound grids
+        pool = None
+        if persistent:
+            cache = self.ctx.__dict__.setdefault("_proc_pool", {})
+            pool = cache.get((self.m_cap, self.ld, D.device().index))
+            if pool is None:
+                pool = cache[(self.m_cap, self.ld, D.device().index)] = {}
+        self._pool = pool
+        if pool:
+            self.w = pool["w"]
+            self._small = pool["small"]
+            self._small.zero_()
+        else:
+            self.w = [torch.empty(self.ld, dtype=D.F64, device=D.device()) for _ in range(2)]
+            # one zero-filled block for H and every small scalar area (a single fill launch)
+            self._small = torch.zeros(nsmall, dtype=D.F64, device=D.device())
         o = (self.m_cap + 1) * hw
         self.H = self._small[:o].view(self.m_cap + 1, hw)
         self.d1 = self._small[o:o + k]
@@ -260,16 +276,26 @@ class _Process:
         # and always runs the re-orthogonalisation pass (`if True:`, krylov.py:156-160)
         del reorthogonalize
         self.eta = REORTH_ETA if engine.fused else 0.0
-        self.scal = D.Scratch(4)
-        self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
-        self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
         self._settled = 0
         self._pending = False
         self._brk_seen = {}
         self._depth = 2
-        self.Ybuf = torch.empty(8 * (self.m_cap + 1), dtype=D.F64, device=D.device())
-        self.resbuf = torch.empty(8, dtype=D.F64, device=D.device())
-        self.host_rb = torch.zeros(self.m_cap + 16, dtype=D.F64, pin_memory=True)
+        if pool:
+            self.scal = pool["scal"]
+            self.scal.dev.zero_()
+            self.res_host, self.brk_host, self.host_rb = pool["res_host"], pool["brk_host"], pool["host_rb"]
+            self.Ybuf, self.resbuf = pool["Ybuf"], pool["resbuf"]
+        else:
+            self.scal = D.Scratch(4)
+            self.res_host = torch.zeros(8, dtype=D.F64, pin_memory=True)
+            self.brk_host = torch.zeros(self.m_cap + 1, dtype=D.F64, pin_memory=True)
+            self.Ybuf = torch.empty(8 * (self.m_cap + 1), dtype=D.F64, device=D.device())
+            self.resbuf = torch.empty(8, dtype=D.F64, device=D.device())
+            self.host_rb = torch.zeros(self.m_cap + 16, dtype=D.F64, pin_memory=True)
+            if pool is not None:
+                pool.update(w=self.w, small=self._small, scal=self.scal, res_host=self.res_host,
+                            brk_host=self.brk_host, host_rb=self.host_rb, Ybuf=self.Ybuf,
+                            resbuf=self.resbuf)
         self.beta_dev = self.nb[2:3]
         # slab ranks with symmetric memory: w's edge rows are pushed into the neighbours'
         # halo buffers by the update pass itself (emhd_update_push), no P2P exchange per Jv
@@ -546,10 +572,15 @@ class _Process:
         if self.fast:
             st = N.Status()
             nb = upto - first
-            with torch.cuda.stream(self.side_stream() if side else torch.cuda.current_stream()):
+            def _readback():
                 N.check(self.lib.emhd_readback(self.ctx.sync_stream(), D.ptr(self.brk) + 8 * first, nb,
                                                D.ptr(res_dev) if nres else None, nres,
                                                D.ptr(self.host_rb), D.ctypes_byref(st)), "readback")
+            if side:
+                with torch.cuda.stream(self.side_stream()):
+                    _readback()
+            else:
+                _readback()           # no stream context on the common path (host-bound grids)
             hb = self.host_rb.numpy()
             flags = hb[:nb]
             if nres:
@@ -684,17 +715,21 @@ class _Process:
         S = len(ms)
         Y = self.Ybuf[:S * (self.m_cap + 1)].view(S, self.m_cap + 1)
         res = self.resbuf[:S]
-        stream = torch.cuda.current_stream()
-        if side:
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            stream = self.side_stream()
-            stream.wait_event(ev)
-        with torch.cuda.stream(stream):
+        def _launch():
             N.check(self.lib.emhd_phi_small_batch(self.ctx.sync_stream(), D.ptr(self.H), self.H.shape[1],
                                                   N.int_array(ms), order, S, N.dbl_array([scale] * S),
                                                   D.ptr(self.brk), D.ptr(self.beta_dev), D.ptr(Y),
                                                   self.m_cap + 1, D.ptr(res)), "phi_small_batch")
+        if side:
+            stream = torch.cuda.current_stream()
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            stream = self.side_stream()
+            stream.wait_event(ev)
+            with torch.cuda.stream(stream):
+                _launch()
+        else:
+            _launch()
         return Y, res
 
     def side_stream(self):
