@@ -12,6 +12,7 @@ struct DenseWork {
   double* m[8];     // 7 n x n work matrices + one n x 2n
   double* vec;      // 5 n + 64
   double* part;     // [2][CLUSTER][n] column-sum partials of the cluster kernel
+  int gj_blocked;   // set by the kernels from PhiSmallArgs: blocked Gauss-Jordan solve
 };
 
 constexpr int DENSE_CLUSTER = 8;     // CTAs (SMs) per exponential in the cluster kernel
@@ -43,6 +44,7 @@ struct PhiSmallArgs {
   int smem_work;            // set by the launcher: the whole workspace (11 n^2 + 5 n doubles) is
                             // carved from dynamic shared memory instead of the global work[]
   int cluster;              // set by the launcher: DENSE_CLUSTER CTAs per problem (large n)
+  int gj_blocked;           // set by the launcher: blocked Gauss-Jordan solve (EMHD_DENSE_GJ_BLOCKED, 1)
 };
 
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s);
