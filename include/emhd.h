@@ -225,6 +225,12 @@ int emhd_phi_small_batch(emhd_ctx* ctx, const double* H, long long ldh, const in
  * the previous threshold (default: EMHD_DENSE_CLUSTER_N, else 56). */
 int emhd_set_dense_cluster(int n);
 
+/* The (V - U) X = (V + U) solve of the Pade approximant (scipy.linalg.expm's LAPACK solve behind
+ * phifuncs.py:65-107): blocked Gauss-Jordan with partial pivoting, eight pivot columns per step,
+ * for 24 <= n <= 128 (on != 0, default), or the unblocked solve for every n; process-wide;
+ * returns the previous setting (default: EMHD_DENSE_GJ_BLOCKED, else 1). */
+int emhd_set_dense_gj_blocked(int on);
+
 /* E = expm(A), n x n row-major device matrices; work: device scratch of n + 4 doubles.
  * Synchronous.  (scipy.linalg.expm as called by phi_dense, phifuncs.py:97,104) */
 int emhd_expm(emhd_ctx* ctx, const double* A, int n, double* E, double* work);

@@ -128,6 +128,7 @@ _SIGS = {
     "emhd_allreduce": (c_int, [c_vp, P, c_int, c_int]),
     "emhd_halo_exchange": (c_int, [c_vp, P, P]),
     "emhd_set_dense_cluster": (c_int, [c_int]),
+    "emhd_set_dense_gj_blocked": (c_int, [c_int]),
 }
 
 _lib = None

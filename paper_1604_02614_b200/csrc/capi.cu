@@ -750,6 +750,15 @@ extern "C" int emhd_set_dense_cluster(int n) {
   return prev;
 }
 
+// The linear solve of the Pade approximant: blocked Gauss-Jordan (8 pivot columns per step) for
+// 24 <= n <= 128, or the unblocked solve everywhere (on = 0); returns the previous setting.
+// Process-wide (default EMHD_DENSE_GJ_BLOCKED, else 1).
+extern "C" int emhd_set_dense_gj_blocked(int on) {
+  const int prev = dense_gj_blocked();
+  set_dense_gj_blocked(on);
+  return prev;
+}
+
 // E = expm(A) for an n x n device matrix (scratch: 4 doubles + n doubles in `work`)
 extern "C" int emhd_expm(emhd_ctx* c, const double* A, int n, double* E, double* work) {
   if (!c || !A || !E || !work || n < 1) return EMHD_ERR_ARG;

@@ -1110,6 +1110,16 @@ int dense_cluster_min_n() {
 
 void set_dense_cluster_min_n(int n) { g_cluster_min_n = n < 0 ? 0 : n; }
 
+static int g_gj_blocked = -1;
+int dense_gj_blocked() {
+  if (g_gj_blocked < 0) {
+    const char* e = getenv("EMHD_DENSE_GJ_BLOCKED");
+    g_gj_blocked = e ? (atoi(e) != 0 ? 1 : 0) : 1;
+  }
+  return g_gj_blocked;
+}
+void set_dense_gj_blocked(int on) { g_gj_blocked = on ? 1 : 0; }
+
 cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t s) {
   PhiSmallArgs P = Pin;
   const int n = P.m + P.order;              // the largest m of a batch
@@ -1129,11 +1139,7 @@ cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t 
       max_dyn = 48 * 1024 - (int)fa.sharedSizeBytes;
     }
   }
-  static int gj_blocked = -1;
-  if (gj_blocked < 0) {
-    const char* env = getenv("EMHD_DENSE_GJ_BLOCKED");
-    gj_blocked = env ? atoi(env) != 0 : 1;
-  }
+  const int gj_blocked = dense_gj_blocked();
   static int use_smem = -1;
   if (use_smem < 0) {
     const char* env = getenv("EMHD_DENSE_SMEM");

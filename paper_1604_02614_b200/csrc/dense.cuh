@@ -50,5 +50,7 @@ struct PhiSmallArgs {
 cudaError_t launch_phi_small(const PhiSmallArgs& P, int nscales, cudaStream_t s);
 int dense_cluster_min_n();
 void set_dense_cluster_min_n(int n);
+int dense_gj_blocked();
+void set_dense_gj_blocked(int on);
 
 }  // namespace emhd

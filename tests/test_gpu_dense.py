@@ -73,3 +73,28 @@ def test_cluster_residual_batch_matches_one_cta(ctx):
             ctx.lib.emhd_set_dense_cluster(prev)
     assert np.max(np.abs(out[0][0] - out[1][0])) <= 1e-14 * np.max(np.abs(out[0][0]))
     assert np.allclose(out[0][1], out[1][1], rtol=1e-12, atol=0.0)
+
+
+@pytest.mark.parametrize("n", [24, 31, 57, 96, 110, 128])
+def test_blocked_solve_matches_unblocked_and_scipy(ctx, n):
+    """The Pade solve by blocked Gauss-Jordan (eight pivot columns per step, rows not moved)
+    against the unblocked solve and scipy, on Hessenberg-like and on full matrices whose
+    denominators need row exchanges (large off-diagonal entries), one CTA and cluster."""
+    import scipy.linalg
+    rng = np.random.default_rng(1000 + n)
+    mats = [np.triu(rng.standard_normal((n, n)), -1) * 20.0 / np.sqrt(n),
+            rng.standard_normal((n, n)) * 6.0 / np.sqrt(n) + 4.0 * np.eye(n)[::-1],
+            rng.standard_normal((n, n)) * 60.0 / np.sqrt(n)]
+    for k, H in enumerate(mats):
+        ref = scipy.linalg.expm(H)
+        den = max(1.0, np.max(np.abs(ref)))
+        for cmin in (0, 1):
+            res = {}
+            for on in (1, 0):
+                prev = ctx.lib.emhd_set_dense_gj_blocked(on)
+                try:
+                    res[on] = expm_dev(ctx, H, cmin)
+                finally:
+                    ctx.lib.emhd_set_dense_gj_blocked(prev)
+            assert np.max(np.abs(res[1] - ref)) <= 2e-11 * den, (n, k, cmin)
+            assert np.max(np.abs(res[1] - res[0])) <= 1e-12 * den, (n, k, cmin)
