@@ -182,6 +182,29 @@ def epirk_small():
         json.dump({k: getattr(st, k) for k in keys}, fh, indent=1)
 
 
+def config1_256(t_end=0.03):
+    """BASELINE config 1 at its full size (KH shear 256 x 256, EpiRK5P1 tol 1e-6) for the first
+    few adaptive steps (t <= 0.03: ~1 min of the reference on one core).  The 4 MB state is not
+    committed: the fixture holds every 64th entry of the result, its norm and the counters; the
+    initial condition is rebuilt by the same host builder the test uses."""
+    sys.path.insert(0, os.path.join(OUT, "..", ".."))
+    from paper_1604_02614_b200.problems import kh_shear_grid, kh_shear_ic
+    g0 = kh_shear_grid(256)
+    g = R.Grid2D(g0.nx, g0.ny, g0.x_lo, g0.x_hi, g0.y_lo, g0.y_hi)
+    P = R.MhdParams(mu=1e-4, eta=1e-4, kappa=1e-4)
+    bc = R.BoundaryPolicy("periodic", "reflect")
+    U0 = kh_shear_ic(g0, P)
+    f = R.make_rhs(P, g, bc)
+    y, st = R.integrate_adaptive(f, U0.reshape(-1), 0.0, t_end, R.StepController(tol=1e-6))
+    keys = ["steps_accepted", "steps_rejected", "projections", "rhs_evals", "operator_applies",
+            "substeps", "max_basis_size"]
+    np.savez_compressed(os.path.join(OUT, "config1_kh256_short.npz"), y_sub=y[::64],
+                        y_norm=np.array([np.linalg.norm(y)]), u0_norm=np.array([np.linalg.norm(U0)]),
+                        t_end=np.array([t_end]))
+    with open(os.path.join(OUT, "config1_kh256_short.json"), "w") as fh:
+        json.dump({k: getattr(st, k) for k in keys}, fh, indent=1)
+
+
 def errors():
     out = {}
     g = R.Grid2D(6, 5, 0.0, 1.0, 0.0, 1.0)
@@ -232,12 +255,15 @@ def harness_fixtures():
 if __name__ == "__main__":
     if sys.argv[1:] == ["harness"]:
         harness_fixtures()
+    elif sys.argv[1:] == ["config1"]:
+        config1_256()
     else:
         rhs_cases()
         config0()
         krylov_dense()
         krylov_mhd()
         epirk_small()
+        config1_256()
         errors()
         harness_fixtures()
     print("fixtures written to", OUT)

@@ -405,6 +405,27 @@ def test_epirk5p1_adaptive_kh32(P):
         assert getattr(S, k) == v, k
 
 
+def test_config1_full_size_first_steps(P):
+    """BASELINE config 1 at its own size (KH shear 256^2, EpiRK5P1 tol 1e-6): the first adaptive
+    steps (t <= 0.03) against the unmodified reference's run (fixture: every 64th entry of the
+    result, its norm, the counters) — 1e-8 relative L2, identical StepStats."""
+    z = golden("config1_kh256_short.npz")
+    with open(os.path.join(GOLDEN, "config1_kh256_short.json")) as fh:
+        st = json.load(fh)
+    from paper_1604_02614_b200.problems import kh_shear_grid, kh_shear_ic
+    g = kh_shear_grid(256)
+    prm = P.MhdParams(mu=1e-4, eta=1e-4, kappa=1e-4)
+    U0 = kh_shear_ic(g, prm)
+    assert abs(np.linalg.norm(U0) - float(z["u0_norm"][0])) <= 1e-13 * float(z["u0_norm"][0])
+    f = P.make_rhs(prm, g, P.BoundaryPolicy("periodic", "reflect"))
+    y, S = P.integrate_adaptive(f, U0.reshape(-1), 0.0, float(z["t_end"][0]), P.StepController(tol=1e-6))
+    ys = z["y_sub"]
+    assert np.linalg.norm(y[::64] - ys) <= 1e-8 * np.linalg.norm(ys)
+    assert abs(np.linalg.norm(y) - float(z["y_norm"][0])) <= 1e-9 * float(z["y_norm"][0])
+    for k, v in st.items():
+        assert getattr(S, k) == v, k
+
+
 # ------------------------------------------------ full-size properties (config 2)
 
 def test_config2_full_size_arnoldi_properties(P):

@@ -146,6 +146,25 @@ def test_epirk5p1_adaptive_kh32():
         assert getattr(T, k) == v, k
 
 
+def test_config1_full_size_first_steps():
+    """The oracle on BASELINE config 1 at its own size (KH shear 256^2, EpiRK5P1 tol 1e-6) for
+    the first four adaptive steps, against the unmodified reference's run (~45 s on one core)."""
+    z = golden("config1_kh256_short.npz")
+    with open(os.path.join(GOLDEN, "config1_kh256_short.json")) as fh:
+        st = json.load(fh)
+    from paper_1604_02614_b200.problems import kh_shear_grid, kh_shear_ic
+    from paper_1604_02614_b200.mhd import BoundaryPolicy, MhdParams
+    g = kh_shear_grid(256)
+    prm = MhdParams(mu=1e-4, eta=1e-4, kappa=1e-4)
+    f = stencil.rhs_closure(prm, g, BoundaryPolicy("periodic", "reflect"))
+    U0 = kh_shear_ic(g, prm)
+    y, T = epirk_cpu.run_adaptive(f, U0.reshape(-1), 0.0, float(z["t_end"][0]), epirk_cpu.Controller(tol=1e-6))
+    assert np.linalg.norm(y[::64] - z["y_sub"]) <= 1e-10 * np.linalg.norm(z["y_sub"])
+    assert abs(np.linalg.norm(y) - float(z["y_norm"][0])) <= 1e-11 * float(z["y_norm"][0])
+    for k, v in st.items():
+        assert getattr(T, k) == v, k
+
+
 @pytest.mark.slow
 def test_config0_full_trajectory():
     z = golden("config0_recon64.npz")
