@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Micro-benchmark of the Arnoldi-loop stencil (fused normalise + Jv, MODE_JVN) per kernel
-variant: python tools/bench_jvn.py 1024,2048 [raw_rows,...]   (raw rows staged ahead: 1 or 2)
+variant: python tools/bench_jvn.py 1024,2048 [raw_rows,...] [strip,...]   (raw rows staged ahead: 1 or
+2; strip width 0 = default, 32 / 64 / 128 / 256)
 CUDA-event timed, back-to-back launches on inputs larger than L2 only from 2048^2 up; at 1024^2
 the a / w / F(a) / out set (320 MB) already exceeds the 126 MB L2."""
 import json
@@ -20,6 +21,7 @@ def main():
     from paper_1604_02614_b200.problems import fourier_grid, fourier_state
     sizes = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["1024"])]
     variants = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "2"])]
+    strips = [int(x) for x in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["0"])]
     res = []
     for n in sizes:
         g = fourier_grid(n)
@@ -35,8 +37,8 @@ def main():
         vout = torch.empty_like(a)
         L = f.ctx.lib
         ref = None
-        for rr in variants:
-            f.ctx.stencil_path(kernel=1, raw_rows=rr)
+        for rr, strip in [(r, st) for r in variants for st in strips]:
+            f.ctx.stencil_path(kernel=1, raw_rows=rr, strip=strip)
 
             def go():
                 N.check(L.emhd_jv_normalized(f.ctx.sync_stream(), a.data_ptr(), None, fa.data_ptr(),
