@@ -64,8 +64,9 @@ __device__ bool finish_partials(const double* partials, int nval, int G, const i
 }
 
 // finish_partials with value max_idx reduced by max, all others by sum
+// (values below v_begin are known to be zero in every CTA: written as 0 without reading them)
 __device__ bool finish_partials_maxidx(const double* partials, int nval, int G, int max_idx,
-                                       double* out, unsigned int* ticket) {
+                                       double* out, unsigned int* ticket, int v_begin = 0) {
   __shared__ bool last;
   __threadfence();
   __syncthreads();
@@ -77,7 +78,8 @@ __device__ bool finish_partials_maxidx(const double* partials, int nval, int G, 
   if (!last) return false;
   __threadfence();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int v = warp; v < nval; v += NWARP) {
+  for (int v = threadIdx.x; v < v_begin; v += KT) out[v] = 0.0;
+  for (int v = v_begin + warp; v < nval; v += NWARP) {
     const bool mx = v == max_idx;
     double acc = 0.0;
     for (int c = lane; c < G; c += 32) {
@@ -333,7 +335,10 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     mx = warp_max(mx);
     if (lane == 0) { s_acc[nvec * NWARP + warp] = ss; s_acc[(nvec + 1) * NWARP + warp] = mx; }
     __syncthreads();
-    for (int v = threadIdx.x; v < nval; v += KT) {
+    // without the re-projection the nvec dot partials are zero in every CTA: neither stored
+    // nor summed (the last CTA writes the zeros; (nvec + 2) x G loads less in its tail)
+    const int v0 = reproj ? 0 : nvec;
+    for (int v = v0 + threadIdx.x; v < nval; v += KT) {
       double acc = 0.0;
       if (v == nvec + 1) {
 #pragma unroll
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(KT, 4) update_kernel(double* __restrict__ w,
     __shared__ int max_kind;
     if (threadIdx.x == 0) max_kind = nvec + 1;
     __syncthreads();
-    const bool last = finish_partials_maxidx(partials, nval, gridDim.x, max_kind, out, ticket);
+    const bool last = finish_partials_maxidx(partials, nval, gridDim.x, max_kind, out, ticket, v0);
     if (last && ro.gate_out) {
       __syncthreads();
       reorth_decide(fin, out, nvec, ro.eta2, ro.gate_out, ro.gate_md2, reproj);
@@ -394,9 +399,10 @@ __device__ __forceinline__ void grid_bar(unsigned int* bar, unsigned int G) {
 // memory: dst[v] = sum (or max for v == max_idx) over c < G of partials[v][c], lanes striding
 // the CTAs and a warp butterfly on top (the same association as the separate kernels)
 __device__ __forceinline__ void reduce_partials_all(const double* partials, int nval, int G, int max_idx,
-                                                    double* dst) {
+                                                    double* dst, int v_begin = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int v = warp; v < nval; v += NWARP) {
+  for (int v = threadIdx.x; v < v_begin; v += KT) dst[v] = 0.0;      // known zeros
+  for (int v = v_begin + warp; v < nval; v += NWARP) {
     const bool mx = v == max_idx;
     double acc = 0.0;
     for (int c = lane; c < G; c += 32) {
@@ -566,7 +572,7 @@ __device__ __forceinline__ void orth_update(const OrthSmallArgs& A, const double
   } else {
     if (lane == 0) { s_acc[nvec * NWARP + warp] = ss; s_acc[(nvec + 1) * NWARP + warp] = mx; }
     __syncthreads();
-    for (int v = threadIdx.x; v < nval; v += KT) {
+    for (int v = (reproj ? 0 : nvec) + threadIdx.x; v < nval; v += KT) {
       double acc = 0.0;
       if (v == nvec + 1) {
 #pragma unroll
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(KT, 2) orth_small_kernel(const OrthSmallArgs A
   const bool reproj = !(A.ro.predict && A.ro.predict[0] != 0.0 && A.ro.predict[1] != 0.0);
   orth_update<0>(A, s_h, reproj, s_acc);
   grid_bar(A.bar, G);
-  reduce_partials_all(A.partials_b, nvec + 2, A.Gu, nvec + 1, s_h);   // s_h: h2 (or zeros), r
+  reduce_partials_all(A.partials_b, nvec + 2, A.Gu, nvec + 1, s_h, reproj ? 0 : nvec);   // s_h: h2 (or zeros), r
   const bool skip2 = selective && s_h[nvec] >= A.ro.eta2 * selfdot;
   if (blockIdx.x == 0) {
     for (int v = threadIdx.x; v < nvec + 2; v += KT) A.d2[v] = s_h[v];
