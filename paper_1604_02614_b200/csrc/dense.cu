@@ -263,8 +263,8 @@ __device__ __noinline__ bool gj_solve(double* M, int n, double* red, int* ired, 
 // choice is the same rule (largest magnitude, lowest row on ties) on the same updated entries
 // up to the association of the updates, so results agree with the unblocked solve to round-off.
 // Measured (clock64, n = 110, M on chip): 541 k cycles unblocked -> 447 k (panel warp 182 k,
-// rank-8 update 162 k + 21 k, staging 11 k); exponential 486 -> 409 us at n = 110, 290 -> 245
-// at n = 80, 768 -> 467 at n = 128 (M in global memory there).
+// rank-8 update 142 k + 20 k, staging 8 k); exponential 486 -> 398 us at n = 110, 290 -> 242
+// at n = 80, 768 -> 465 at n = 128 (M in global memory there).
 constexpr int GB = 8, GPB = GB + 1;
 constexpr int GJ_BLOCKED_MIN_N = 24;   // below: the unblocked solve is as fast (n = 12: 65 vs 70 us)
 __device__ __noinline__ bool gj_solve_blocked(double* M, int n, double* pan, double* Wb, int* used,
@@ -383,7 +383,44 @@ __device__ __noinline__ bool gj_solve_blocked(double* M, int n, double* pan, dou
     for (int q = 0; q < GB; ++q) pr_rows[q] = q < bw ? rowof[k + q] : -1;
     const int c_lo = k + bw;
     // (a) non-pivot rows: rows over warps (four at a time: independent FMA chains), columns
-    // over lanes
+    // over lanes — two columns per lane with 16-byte accesses when M is 16-byte aligned (its
+    // rows are: 2n doubles), starting at the even column at or below c_lo (a panel column that
+    // is never read again)
+    if ((reinterpret_cast<uintptr_t>(M) & 15) == 0) {
+      for (int cb = (c_lo & ~1) + 2 * lane; cb < w2; cb += 64) {
+        double2 pv[GB];
+#pragma unroll
+        for (int q = 0; q < GB; ++q)
+          pv[q] = q < bw ? *reinterpret_cast<const double2*>(M + (size_t)pr_rows[q] * w2 + cb) : make_double2(0.0, 0.0);
+        for (int i0 = warp; i0 < n; i0 += 4 * NWD) {
+          double2 acc[4];
+          bool live[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * NWD;
+            bool is_piv = false;
+#pragma unroll
+            for (int q = 0; q < GB; ++q) is_piv |= (i == pr_rows[q]);
+            live[u] = i < n && !is_piv;
+            acc[u] = live[u] ? *reinterpret_cast<const double2*>(M + (size_t)i * w2 + cb) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int q = 0; q < GB; ++q) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (live[u]) {
+                const double wv = Wb[(i0 + u * NWD) * GPB + q];
+                acc[u].x = fma(wv, pv[q].x, acc[u].x);
+                acc[u].y = fma(wv, pv[q].y, acc[u].y);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (live[u]) *reinterpret_cast<double2*>(M + (size_t)(i0 + u * NWD) * w2 + cb) = acc[u];
+        }
+      }
+    } else {
     for (int cb = c_lo + lane; cb < w2; cb += 32) {
       double pv[GB];
 #pragma unroll
@@ -410,6 +447,7 @@ __device__ __noinline__ bool gj_solve_blocked(double* M, int n, double* pan, dou
         for (int u = 0; u < 4; ++u)
           if (live[u]) M[(size_t)(i0 + u * NWD) * w2 + cb] = acc[u];
       }
+    }
     }
     __syncthreads();
     GJT(2)
@@ -680,7 +718,7 @@ __global__ void __launch_bounds__(DT) phi_small_kernel(PhiSmallArgs P) {
   for (int e = threadIdx.x; e < m * m; e += DT) if (!isfinite(A[(e / m) * n + e % m])) finite = false;
   finite = __syncthreads_and(finite);
   double* ycol = W.vec + 3 * n;                    // [2n] column result / ping-pong
-  double* sM = (!P.smem_work && n <= P.smem_n) ? prow + 3 * n : nullptr;
+  double* sM = (!P.smem_work && n <= P.smem_n) ? prow + ((3 * n + 1) & ~1) : nullptr;   // 16-byte aligned
   bool ok = finite && expm_block(A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol, sM, prow + 2 * n);
   if (ok) {
     bool fin2 = true;
@@ -1057,7 +1095,7 @@ __global__ void __launch_bounds__(DT) phi_cluster_kernel(PhiSmallArgs P) {
     finite = finite && __ldcg(W.part + (size_t)DENSE_CLUSTER * n + q) != 0.0;
   T.sync();                                        // the partial buffer is reused below
   double* ycol = W.vec + 3 * n;
-  double* sM = (rank == 0 && n <= P.smem_n) ? prow + 3 * n : nullptr;
+  double* sM = (rank == 0 && n <= P.smem_n) ? prow + ((3 * n + 1) & ~1) : nullptr;   // 16-byte aligned
   bool ok = finite && expm_cluster(T, A, n, E, W, sA, sB, red, ired, prow, P.E_out ? -1 : col, ycol, sM,
                                    prow + 2 * n);
   if (rank != 0) return;
@@ -1157,8 +1195,8 @@ cudaError_t launch_phi_small(const PhiSmallArgs& Pin, int nscales, cudaStream_t 
   if (use_smem && !cluster && whole <= (size_t)max_dyn) {
     dyn = whole;                        // n <= ~42: the whole exponential on chip
     P.smem_work = 1;
-  } else if (use_smem && sizeof(double) * (3 * (size_t)n + 2 * (size_t)n * n) <= (size_t)max_dyn) {
-    dyn = sizeof(double) * (3 * (size_t)n + 2 * (size_t)n * n);
+  } else if (use_smem && sizeof(double) * (3 * (size_t)n + 1 + 2 * (size_t)n * n) <= (size_t)max_dyn) {
+    dyn = sizeof(double) * (3 * (size_t)n + 1 + 2 * (size_t)n * n);
     P.smem_n = n;
   }
   if (cluster) {
