@@ -262,142 +262,127 @@ __device__ __noinline__ bool gj_solve(double* M, int n, double* red, int* ired, 
 // first (they only read the pivot rows), then the pivot rows, one thread per column.  Pivot
 // choice is the same rule (largest magnitude, lowest row on ties) on the same updated entries
 // up to the association of the updates, so results agree with the unblocked solve to round-off.
-// Measured (clock64, n = 110, M on chip): 541 k cycles unblocked -> 447 k (panel warp 182 k,
-// rank-8 update 142 k + 20 k, staging 8 k); exponential 486 -> 398 us at n = 110, 290 -> 242
-// at n = 80, 768 -> 465 at n = 128 (M in global memory there).
+// Measured (clock64, n = 110, M on chip): 541 k cycles unblocked -> 403 k blocked (panel warp
+// 162 k, rank-8 update 142 k + 20 k, staging 8 k) -> 360 k with the panel look-ahead below;
+// exponential 486 -> 394 us at n = 110, 290 -> 245 at n = 80, 768 -> 455 at n = 128.
 constexpr int GB = 8, GPB = GB + 1;
 constexpr int GJ_BLOCKED_MIN_N = 24;   // below: the unblocked solve is as fast (n = 12: 65 vs 70 us)
-__device__ __noinline__ bool gj_solve_blocked(double* M, int n, double* pan, double* Wb, int* used,
-                                              int* rowof, double* red) {
-  const int w2 = 2 * n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NWD = DT / 32;
-  for (int i = threadIdx.x; i < n; i += DT) used[i] = 0;
-  if (threadIdx.x == 0) red[0] = 1.0;              // cleared by the panel warp on a zero pivot
-  __syncthreads();
-#ifdef DENSE_DBG
-  long long tp[4] = {0, 0, 0, 0};
-#define GJT(i) { const long long tn = clock64(); tp[i] += tn - tlast; tlast = tn; }
-  long long tlast = clock64();
-#else
-#define GJT(i)
-#endif
-  for (int k = 0; k < n; k += GB) {
-    const int bw = min(GB, n - k);
-    for (int e = threadIdx.x; e < n * GB; e += DT) {
-      const int i = e / GB, t = e % GB;
-      pan[i * GPB + t] = t < bw ? M[(size_t)i * w2 + k + t] : 0.0;
-      Wb[i * GPB + t] = 0.0;
+// One warp: in-place Gauss-Jordan of the n x bw panel M[:, k : k+bw) held in registers (lane l:
+// rows l + 32 q, q < 4), rows already used as pivots excluded from the search; writes the
+// composite transform Wout[n][GPB], the pivot rows rowof[k + t] and used[]; clears red[0] on a
+// zero pivot column.  Reads M only in its own panel columns and writes nothing to M.
+__device__ __forceinline__ void gj_panel_warp(const double* M, int w2, int n, int k, int bw, int* used,
+                                              int* rowof, double* Wout, double* red, int lane) {
+  double X[4][GB];
+  unsigned usedmask = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = lane + 32 * q;
+    if (i < n) {
+#pragma unroll
+      for (int c = 0; c < GB; ++c) X[q][c] = c < bw ? M[(size_t)i * w2 + k + c] : 0.0;
+      usedmask |= (used[i] ? 1u : 0u) << q;
+    } else {
+#pragma unroll
+      for (int c = 0; c < GB; ++c) X[q][c] = 0.0;
+      usedmask |= 1u << q;
     }
-    __syncthreads();
-    GJT(0)
-    if (warp == 0) {
-      // lane l holds rows l + 32 q (q < 4) of the panel in registers; in-place Gauss-Jordan:
-      // at step t column t of X turns from panel entries into the transform's column t
-      double X[4][GB];
-      unsigned usedmask = 0;
+  }
+  double* pbuf = red + 1;                    // the pivot row of the step, published by its owner
+  bool ok = true;
+#pragma unroll
+  for (int t = 0; t < GB; ++t) {
+    if (t < bw && ok) {
+      double best = -1.0; int bi = n;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int i = lane + 32 * q;
-        if (i < n) {
-#pragma unroll
-          for (int c = 0; c < GB; ++c) X[q][c] = pan[i * GPB + c];
-          usedmask |= (used[i] ? 1u : 0u) << q;
-        } else {
-#pragma unroll
-          for (int c = 0; c < GB; ++c) X[q][c] = 0.0;
-          usedmask |= 1u << q;
+        if (!((usedmask >> q) & 1u)) {
+          const double a = fabs(X[q][t]);
+          if (a > best) { best = a; bi = lane + 32 * q; }
         }
       }
-      double* pbuf = red + 1;                    // the pivot row of the step, published by its owner
-      bool ok = true;
-#pragma unroll
-      for (int t = 0; t < GB; ++t) {
-        if (t < bw && ok) {
-          double best = -1.0; int bi = n;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (!((usedmask >> q) & 1u)) {
-              const double a = fabs(X[q][t]);
-              if (a > best) { best = a; bi = lane + 32 * q; }
-            }
-          }
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-          }
-          if (!(best > 0.0)) {
-            if (lane == 0) red[0] = 0.0;
-            ok = false;
-          } else {
-            const int r = bi;
-            const bool owner = lane == (r & 31);
-            if (owner) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (q == (r >> 5)) {
-#pragma unroll
-                  for (int c = 0; c < GB; ++c) pbuf[c] = X[q][c];
-                }
-              usedmask |= 1u << (r >> 5);
-              used[r] = 1;
-              rowof[k + t] = r;
-            }
-            __syncwarp();
-            double prs[GB];
-#pragma unroll
-            for (int c = 0; c < GB; ++c) prs[c] = pbuf[c];
-            __syncwarp();
-            const double rd = 1.0 / prs[t];
-#pragma unroll
-            for (int c = 0; c < GB; ++c) prs[c] = (c == t) ? rd : prs[c] * rd;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const bool isr = owner && q == (r >> 5);
-              const double f = X[q][t];
-#pragma unroll
-              for (int c = 0; c < GB; ++c) {
-                const double v = (c == t) ? -f * prs[t] : fma(-f, prs[c], X[q][c]);
-                X[q][c] = isr ? prs[c] : v;
-              }
-            }
-          }
-        }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
+      if (!(best > 0.0)) {
+        if (lane == 0) red[0] = 0.0;
+        ok = false;
+      } else {
+        const int r = bi;
+        const bool owner = lane == (r & 31);
+        if (owner) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = lane + 32 * q;
-        if (i < n) {
+          for (int q = 0; q < 4; ++q)
+            if (q == (r >> 5)) {
 #pragma unroll
-          for (int c = 0; c < GB; ++c) Wb[i * GPB + c] = X[q][c];
+              for (int c = 0; c < GB; ++c) pbuf[c] = X[q][c];
+            }
+          usedmask |= 1u << (r >> 5);
+          used[r] = 1;
+          rowof[k + t] = r;
+        }
+        __syncwarp();
+        double prs[GB];
+#pragma unroll
+        for (int c = 0; c < GB; ++c) prs[c] = pbuf[c];
+        __syncwarp();
+        const double rd = 1.0 / prs[t];
+#pragma unroll
+        for (int c = 0; c < GB; ++c) prs[c] = (c == t) ? rd : prs[c] * rd;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool isr = owner && q == (r >> 5);
+          const double f = X[q][t];
+#pragma unroll
+          for (int c = 0; c < GB; ++c) {
+            const double v = (c == t) ? -f * prs[t] : fma(-f, prs[c], X[q][c]);
+            X[q][c] = isr ? prs[c] : v;
+          }
         }
       }
     }
-    __syncthreads();
-    GJT(1)
-    if (red[0] == 0.0) return false;
-    // pivot rows of this panel (used[] cannot tell them from earlier ones: compare indices)
-    int pr_rows[GB];
+  }
 #pragma unroll
-    for (int q = 0; q < GB; ++q) pr_rows[q] = q < bw ? rowof[k + q] : -1;
-    const int c_lo = k + bw;
-    // (a) non-pivot rows: rows over warps (four at a time: independent FMA chains), columns
-    // over lanes — two columns per lane with 16-byte accesses when M is 16-byte aligned (its
-    // rows are: 2n doubles), starting at the even column at or below c_lo (a panel column that
-    // is never read again)
+  for (int q = 0; q < 4; ++q) {
+    const int i = lane + 32 * q;
+    if (i < n) {
+#pragma unroll
+      for (int c = 0; c < GB; ++c) Wout[i * GPB + c] = X[q][c];
+    }
+  }
+}
+
+// Rank-bw update of the columns [c_begin, c_end) with the transform Wc of the panel whose pivot
+// rows are pr_rows: C[i] = keep_i C[i] + sum_s Wc[i][s] C[r_s], by the threads [t0, t0 + nt) of the
+// CTA (nt a multiple of 32), synchronised among themselves by barrier `bar_id` (0: the CTA
+// barrier): non-pivot rows first (they only read the pivot rows), then the pivot rows, one
+// thread per column.
+__device__ __forceinline__ void gj_update(double* M, int w2, int n, int c_begin, int c_end,
+                                          const int (&pr_rows)[GB], int bw, const double* Wc, int t0,
+                                          int nt, int bar_id) {
+  const int tl = threadIdx.x - t0;
+  const int lane = tl & 31, warp = tl >> 5, nw = nt >> 5;
+  auto sync = [&]() {
+    if (bar_id == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nt) : "memory");
+  };
+  if (c_begin < c_end) {
     if ((reinterpret_cast<uintptr_t>(M) & 15) == 0) {
-      for (int cb = (c_lo & ~1) + 2 * lane; cb < w2; cb += 64) {
+      // two columns per lane, 16-byte accesses (rows are 2n doubles: aligned), from the even
+      // column at or below c_begin (an already-eliminated column when c_begin is odd)
+      for (int cb = (c_begin & ~1) + 2 * lane; cb < c_end; cb += 64) {
         double2 pv[GB];
 #pragma unroll
         for (int q = 0; q < GB; ++q)
           pv[q] = q < bw ? *reinterpret_cast<const double2*>(M + (size_t)pr_rows[q] * w2 + cb) : make_double2(0.0, 0.0);
-        for (int i0 = warp; i0 < n; i0 += 4 * NWD) {
+        for (int i0 = warp; i0 < n; i0 += 4 * nw) {
           double2 acc[4];
           bool live[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int i = i0 + u * NWD;
+            const int i = i0 + u * nw;
             bool is_piv = false;
 #pragma unroll
             for (int q = 0; q < GB; ++q) is_piv |= (i == pr_rows[q]);
@@ -409,73 +394,113 @@ __device__ __noinline__ bool gj_solve_blocked(double* M, int n, double* pan, dou
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               if (live[u]) {
-                const double wv = Wb[(i0 + u * NWD) * GPB + q];
+                const double wv = Wc[(i0 + u * nw) * GPB + q];
                 acc[u].x = fma(wv, pv[q].x, acc[u].x);
                 acc[u].y = fma(wv, pv[q].y, acc[u].y);
               }
             }
           }
+          // a pair may straddle an odd boundary of [c_begin, c_end): the column outside it
+          // belongs to another phase (or to the panel warp 0 is reading) and is not written
+          const bool ux = cb >= c_begin, uy = cb + 1 < c_end;
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (live[u]) *reinterpret_cast<double2*>(M + (size_t)(i0 + u * NWD) * w2 + cb) = acc[u];
+          for (int u = 0; u < 4; ++u) {
+            if (live[u]) {
+              double* dst = M + (size_t)(i0 + u * nw) * w2 + cb;
+              if (ux && uy) *reinterpret_cast<double2*>(dst) = acc[u];
+              else if (ux) dst[0] = acc[u].x;
+              else if (uy) dst[1] = acc[u].y;
+            }
+          }
         }
       }
     } else {
-    for (int cb = c_lo + lane; cb < w2; cb += 32) {
-      double pv[GB];
+      for (int cb = c_begin + lane; cb < c_end; cb += 32) {
+        double pv[GB];
 #pragma unroll
-      for (int q = 0; q < GB; ++q) pv[q] = q < bw ? M[(size_t)pr_rows[q] * w2 + cb] : 0.0;
-      for (int i0 = warp; i0 < n; i0 += 4 * NWD) {
-        double acc[4];
-        bool live[4];
+        for (int q = 0; q < GB; ++q) pv[q] = q < bw ? M[(size_t)pr_rows[q] * w2 + cb] : 0.0;
+        for (int i0 = warp; i0 < n; i0 += 4 * nw) {
+          double acc[4];
+          bool live[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u * NWD;
-          bool is_piv = false;
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * nw;
+            bool is_piv = false;
 #pragma unroll
-          for (int q = 0; q < GB; ++q) is_piv |= (i == pr_rows[q]);
-          live[u] = i < n && !is_piv;
-          acc[u] = live[u] ? M[(size_t)i * w2 + cb] : 0.0;
-        }
+            for (int q = 0; q < GB; ++q) is_piv |= (i == pr_rows[q]);
+            live[u] = i < n && !is_piv;
+            acc[u] = live[u] ? M[(size_t)i * w2 + cb] : 0.0;
+          }
 #pragma unroll
-        for (int q = 0; q < GB; ++q) {
+          for (int q = 0; q < GB; ++q) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (live[u]) acc[u] = fma(Wc[(i0 + u * nw) * GPB + q], pv[q], acc[u]);
+          }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (live[u]) acc[u] = fma(Wb[(i0 + u * NWD) * GPB + q], pv[q], acc[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (live[u]) M[(size_t)(i0 + u * NWD) * w2 + cb] = acc[u];
-      }
-    }
-    }
-    __syncthreads();
-    GJT(2)
-    // (b) the pivot rows themselves, one thread per column (reads the old values first)
-    for (int cb = c_lo + threadIdx.x; cb < w2; cb += DT) {
-      double pv[GB];
-#pragma unroll
-      for (int q = 0; q < GB; ++q) pv[q] = q < bw ? M[(size_t)pr_rows[q] * w2 + cb] : 0.0;
-#pragma unroll
-      for (int u = 0; u < GB; ++u) {
-        if (u < bw) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q = 0; q < GB; ++q) acc = fma(Wb[pr_rows[u] * GPB + q], pv[q], acc);
-          M[(size_t)pr_rows[u] * w2 + cb] = acc;
+            if (live[u]) M[(size_t)(i0 + u * nw) * w2 + cb] = acc[u];
         }
       }
     }
-    __syncthreads();
-    GJT(3)
   }
-#ifdef DENSE_DBG
-  if (threadIdx.x == 0) printf("gj phases: stage %lld panel %lld upd_a %lld upd_b %lld\n", tp[0], tp[1], tp[2], tp[3]);
-#endif
-  return true;
+  sync();
+  for (int cb = c_begin + tl; cb < c_end; cb += nt) {
+    double pv[GB];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) pv[q] = q < bw ? M[(size_t)pr_rows[q] * w2 + cb] : 0.0;
+#pragma unroll
+    for (int u = 0; u < GB; ++u) {
+      if (u < bw) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < GB; ++q) acc = fma(Wc[pr_rows[u] * GPB + q], pv[q], acc);
+        M[(size_t)pr_rows[u] * w2 + cb] = acc;
+      }
+    }
+  }
 }
 
-// dispatcher: the blocked solve for n <= MM_MAXR (pan / Wb live in the matrix-product staging
+// Panels with look-ahead: while warps 1..15 apply panel p's rank-8 update to the columns right
+// of panel p+1, warp 0 already factors panel p+1 (whose columns were updated first, by all
+// warps); the transforms alternate between two buffers.  The step costs the longer of the two
+// instead of their sum.
+__device__ __noinline__ bool gj_solve_blocked(double* M, int n, double* W0, double* W1, int* used,
+                                              int* rowof, double* red) {
+  const int w2 = 2 * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < n; i += DT) used[i] = 0;
+  if (threadIdx.x == 0) red[0] = 1.0;              // cleared by the panel warp on a zero pivot
+  __syncthreads();
+  double* Wbuf[2] = {W0, W1};
+  if (warp == 0) gj_panel_warp(M, w2, n, 0, min(GB, n), used, rowof, Wbuf[0], red, lane);
+  __syncthreads();
+  int cur = 0;
+  for (int k = 0; k < n; k += GB) {
+    if (red[0] == 0.0) return false;
+    const int bw = min(GB, n - k);
+    const int kn = k + bw;                          // first column of the next panel
+    const int bwn = kn < n ? min(GB, n - kn) : 0;
+    int pr_rows[GB];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) pr_rows[q] = q < bw ? rowof[k + q] : -1;
+    const double* Wc = Wbuf[cur];
+    // (1) the next panel's columns first, by everybody
+    gj_update(M, w2, n, kn, kn + bwn, pr_rows, bw, Wc, 0, DT, 0);
+    __syncthreads();
+    // (2) warp 0 factors the next panel while the other warps update the rest
+    if (warp == 0) {
+      if (bwn > 0) gj_panel_warp(M, w2, n, kn, bwn, used, rowof, Wbuf[cur ^ 1], red, lane);
+    } else {
+      gj_update(M, w2, n, kn + bwn, w2, pr_rows, bw, Wc, 32, DT - 32, 1);
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  return red[0] != 0.0;
+}
+
+// dispatcher: the blocked solve for n <= MM_MAXR (its two transform buffers live in the matrix-product staging
 // buffers sA / sB, free during the solve; used / rowof in the factor area), else the unblocked
 // one.  *rowof: row of M holding solution row j (null: natural order)
 __device__ bool gj_solve_any(double* M, int n, double* red, int* ired, double* fac, double* prow,
