@@ -112,12 +112,14 @@ int emhd_status_clear_errors(emhd_ctx* ctx);
 typedef struct emhd_stencil_path {
   int kernel;        /* EMHD_STENCIL_* */
   int rows_per_cta;  /* marching: rows per CTA; 0 = one wave of resident CTAs (>= min_rows) */
-  int strip;         /* marching: 32 / 64 / 128 columns per CTA; 0 = by ny */
+  int strip;         /* marching: 32 / 64 / 128 columns per CTA; 0 = by ny and raw_rows (64 with two
+                      * staged rows, 4 CTAs/SM; 128 with one) */
   int bulk;          /* marching: interior strips stage rows with bulk async copies (TMA engine)
                         when 16-byte aligned; 0 = per-thread cp.async everywhere */
   int min_rows;      /* >= 1 */
   int tile_rows;
-  int raw_rows;      /* marching normalised Jv: input rows staged ahead, 1 or 2 (0 = 2) */
+  int raw_rows;      /* marching: input rows staged ahead, 1 or 2 (0 = auto: 2 with the halo warp for
+                      * Jv / normalised Jv, 1 for the RHS) */
 } emhd_stencil_path;
 int emhd_set_stencil_path(emhd_ctx* ctx, const emhd_stencil_path* sel);
 int emhd_get_stencil_path(emhd_ctx* ctx, emhd_stencil_path* out);

@@ -21,6 +21,13 @@
 #include "emhd_common.cuh"
 #include "stencil.cuh"
 
+#ifndef EMHD_QP_REG
+#define EMHD_QP_REG 1
+#endif
+#ifndef EMHD_GX_SMEM
+#define EMHD_GX_SMEM 0
+#endif
+
 namespace emhd {
 
 // primitives differentiated across rows/columns: shared by the CTA in the primitive ring
@@ -177,6 +184,12 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, unsign
       : "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+  unsigned p;
+  asm volatile("{\n .reg .pred q;\n elect.sync _|q, 0xffffffff;\n selp.u32 %0, 1, 0, q;\n}\n" : "=r"(p));
+  return p != 0;
+}
+
 // one raw row of an interior strip (columns j0-2 .. j0+TY+1, all inside the grid): 8 or 16
 // contiguous row segments, issued by one thread; completion lands on the slot's mbarrier
 template <int MODE, int QW>
@@ -245,7 +258,8 @@ __device__ __forceinline__ void consume_raw(const double* slot, int c, RawCell<M
 
 // pressure / admissibility / primitives (mhd.py:106-131, 176-181, 217-221)
 __device__ __forceinline__ void cell_prims(const StencilParams& P, const double u[NF],
-                                           double* q, double* cq, int qs, int& flag) {
+                                           double* q, double* cq, int qs, int& flag,
+                                           double* qreg = nullptr) {
   const double rho = u[0], mx = u[1], my = u[2], mz = u[3];
   const double b0 = u[4], b1 = u[5], b2 = u[6], en = u[7];
   if (P.check && rho <= 0.0) flag |= ST_RHO;
@@ -263,11 +277,19 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
   q[Q_B0 * qs] = b0;
   q[Q_B1 * qs] = b1;
   q[Q_B2 * qs] = b2;
-  q[Q_V0 * qs] = div_const(mx, rho, rr);      // == mx / rho bit for bit
-  q[Q_V1 * qs] = div_const(my, rho, rr);
-  q[Q_V2 * qs] = div_const(mz, rho, rr);
-  q[Q_T * qs] = div_const(p, rho, rr);
+  const double v0 = div_const(mx, rho, rr);   // == mx / rho bit for bit
+  const double v1 = div_const(my, rho, rr);
+  const double v2 = div_const(mz, rho, rr);
+  const double tt = div_const(p, rho, rr);
+  q[Q_V0 * qs] = v0;
+  q[Q_V1 * qs] = v1;
+  q[Q_V2 * qs] = v2;
+  q[Q_T * qs] = tt;
   cq[C_PT * qs] = __dadd_rn(p, __dmul_rn(0.5, bb));
+  if (qreg) {
+    qreg[Q_V0] = v0; qreg[Q_V1] = v1; qreg[Q_V2] = v2;
+    qreg[Q_B0] = b0; qreg[Q_B1] = b1; qreg[Q_B2] = b2; qreg[Q_T] = tt;
+  }
 }
 
 // x- and y-flux G = F_hyp - F_diff at one cell (mhd.py:174-197, 209-266, 275-276).
@@ -276,15 +298,17 @@ template <int FXY>
 __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* qm,
                                           const double* q0, const double* qp, const double* c0,
                                           int c, int qs,
-                                          bool need_x, bool need_y, double gx[NF], double gy[NF]) {
+                                          bool need_x, bool need_y, double gx[NF], double gy[NF],
+                                          const double* qpreg = nullptr) {
 #define QV(row, k, col) row[(k) * qs + (col)]
+#define QP(k) (qpreg ? qpreg[k] : QV(qp, k, c))
   const double thx = P.two_hx, rhx = P.r_two_hx, thy = P.two_hy, rhy = P.r_two_hy;
   // centred derivatives of v, B, T at the cell (mhd.py:224-227, 261, 264)
-  const double dvx0 = div_c<FXY>(__dsub_rn(QV(qp, Q_V0, c), QV(qm, Q_V0, c)), thx, rhx);
-  const double dvx1 = div_c<FXY>(__dsub_rn(QV(qp, Q_V1, c), QV(qm, Q_V1, c)), thx, rhx);
+  const double dvx0 = div_c<FXY>(__dsub_rn(QP(Q_V0), QV(qm, Q_V0, c)), thx, rhx);
+  const double dvx1 = div_c<FXY>(__dsub_rn(QP(Q_V1), QV(qm, Q_V1, c)), thx, rhx);
   const double dvy0 = div_c<FXY>(__dsub_rn(QV(q0, Q_V0, c + 1), QV(q0, Q_V0, c - 1)), thy, rhy);
   const double dvy1 = div_c<FXY>(__dsub_rn(QV(q0, Q_V1, c + 1), QV(q0, Q_V1, c - 1)), thy, rhy);
-  const double dBx1 = div_c<FXY>(__dsub_rn(QV(qp, Q_B1, c), QV(qm, Q_B1, c)), thx, rhx);
+  const double dBx1 = div_c<FXY>(__dsub_rn(QP(Q_B1), QV(qm, Q_B1, c)), thx, rhx);
   const double dBy0 = div_c<FXY>(__dsub_rn(QV(q0, Q_B0, c + 1), QV(q0, Q_B0, c - 1)), thy, rhy);
 
   const double rho = QV(c0, C_RHO, c), en = QV(c0, C_EN, c), pt = QV(c0, C_PT, c);
@@ -301,9 +325,9 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
   const double r0 = __dmul_rn(rho, v0), r1 = __dmul_rn(rho, v1), r2 = __dmul_rn(rho, v2);
 
   if (need_x) {
-    const double dvx2 = div_c<FXY>(__dsub_rn(QV(qp, Q_V2, c), QV(qm, Q_V2, c)), thx, rhx);
-    const double dBx2 = div_c<FXY>(__dsub_rn(QV(qp, Q_B2, c), QV(qm, Q_B2, c)), thx, rhx);
-    const double dTx = div_c<FXY>(__dsub_rn(QV(qp, Q_T, c), QV(qm, Q_T, c)), thx, rhx);
+    const double dvx2 = div_c<FXY>(__dsub_rn(QP(Q_V2), QV(qm, Q_V2, c)), thx, rhx);
+    const double dBx2 = div_c<FXY>(__dsub_rn(QP(Q_B2), QV(qm, Q_B2, c)), thx, rhx);
+    const double dTx = div_c<FXY>(__dsub_rn(QP(Q_T), QV(qm, Q_T, c)), thx, rhx);
     const double tau_xx = __dsub_rn(__dmul_rn(2.0, dvx0), c23d);
     // diffusive x-flux (mhd.py:244-262)
     const double fmx = __dmul_rn(mu, tau_xx);
@@ -349,24 +373,31 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
     gy[6] = __dsub_rn(__dsub_rn(__dmul_rn(v1, b2), __dmul_rn(b1, v2)), fbz);
     gy[7] = __dsub_rn(__dsub_rn(__dmul_rn(ept, v1), __dmul_rn(b1, bv)), fen);
   }
+#undef QP
 #undef QV
 }
 
-// raw input rows in flight per CTA (NR): row r+NR is requested while row r is consumed.  The
-// Arnoldi-loop stencil (MODE_JVN) takes two (2 CTAs/SM, one more row of prefetch, plus the
-// halo warp): 1024^2 78.9 us vs 87.5 with one row at 3 CTAs/SM, 2048^2 301.5 vs 312.9,
-// 4096^2 1224 vs 1218 (three rows: 1024^2 93.6 us).  RHS / Jv keep one (Jv 1024^2 69 us vs 72).
+// raw input rows in flight per CTA (NR): row r+NR is requested while row r is consumed.  NR = 2
+// comes with the halo warp (HW below) and, on grids wider than 64 columns, 64-column strips at
+// 4 CTAs/SM (12 warps: 8 column warps + 4 halo warps, the register file exactly full at 168
+// registers): four independent per-row barrier groups of three warps instead of two groups of
+// five.  Back-to-back launches (tools/bench_jvn.py), two rows + halo warp, strip 64 / 128 (one row,
+// no halo warp, 128 columns in brackets): normalised Jv 1024^2 64.6 / 72.1 us (87.5), 2048^2
+// 236 / 267 us (313), 4096^2 938 / 1037 us (1218); Jv 1024^2 59.2 / 59.7 us (67.7), 2048^2
+// 215 / 219 us (242); RHS 1024^2 47.1 / 44.9 us (43.5), 2048^2 172 / 164 us (151): the RHS keeps
+// one row at 3 CTAs/SM; 32-column strips (6 CTAs/SM) and 96-column strips (3 CTAs/SM) lose
+// everywhere.  sel.raw_rows forces 1 or 2 for every mode.
 static bool two_raw_rows(int mode, const StencilParams& P, const StencilPath& sel) {
   (void)P;
-  if (mode != MODE_JVN) return false;
-  return sel.raw_rows != 1;
+  if (sel.raw_rows == 0) return mode != MODE_RHS;
+  return sel.raw_rows == 2;
 }
 
 // HW (with two staged rows, 2 CTAs/SM): one extra warp per CTA does the strip's halo work (the
 // four halo columns' primitives and the two halo y-fluxes) beside the TY column threads, so no
 // column warp carries extra work into the per-row barrier
 template <int TY, int MODE, bool AUG, int FXY, int NR>
-__global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY)
+__global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 4 : 2) : 384 / TY)
     stencil_kernel(const StencilParams P) {
   constexpr bool HW = NR == 2;
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
@@ -382,10 +413,21 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
   constexpr int NRAW = NR;
   double* rawring = cring + 2 * NC * QW;            // [NRAW][NARR*NF][QW] raw rows in flight
-  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NRAW * NARR * NF * QW);
+  // GXS: the x-flux history (rows r-3, r-2) in a thread-private shared-memory ring [2][NF][TY]
+  // instead of a rotated register ring (16 register moves less per row, 147 instead of 167
+  // registers).  Measured slower (normalised Jv 1024^2 64.9 -> 75.0 us, Jv 56.9 -> 61.2 us): the
+  // row step is bound by shared-memory instructions, not by the moves.  Off.
+  constexpr bool GXS = HW && EMHD_GX_SMEM;
+  // measured (tools/bench_jvn.py): RHS 1024^2 42.3 -> 41.5 us, 2048^2 145.8 -> 142.9 us; the Jv
+  // variants are at their 168-register cap (4 CTAs/SM) and spill with it (normalised Jv 64.7 ->
+  // 85.9 us), so only the RHS takes it
+  constexpr bool QPR = EMHD_QP_REG != 0 && MODE == MODE_RHS;
+  double* gxring = rawring + NRAW * NARR * NF * QW;
+  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(gxring + (GXS ? 2 * NF * TY : 0));
 
   pdl_sync();
   const int tid = threadIdx.x;
+  const int warp_u = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp index, known warp-uniform
   const int t = HW ? tid - 32 : tid;               // column thread index (< 0: the halo warp)
   const int j0 = blockIdx.x * TY;
   // output rows [i0, i1) of this CTA: a chunk of [row_lo, row_hi) (rows_mode 0/1), or the
@@ -514,12 +556,16 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
     double gxA[NF], gxB[NF], gxC[NF];        // x-fluxes of rows r-3, r-2, r-1 (own column)
 #pragma unroll
     for (int f = 0; f < NF; ++f) { gxA[f] = 0.0; gxB[f] = 0.0; gxC[f] = 0.0; }
+    if (GXS && t >= 0) {
+#pragma unroll
+      for (int f = 0; f < NF; ++f) { gxring[f * TY + t] = 0.0; gxring[(NF + f) * TY + t] = 0.0; }
+    }
     // interior strips (no y-ghost columns) stream whole row segments with bulk async copies
     // issued by thread 0 (tracked by one mbarrier); edge strips keep per-thread cp.async
     const bool bulk = P.tma && j0 >= 2 && j0 + TY + 2 <= P.ny;
     constexpr int SLOT = NARR * NF * QW;     // doubles per raw row slot
     if (bulk) {
-      if (tid == 0) {
+      if (warp_u == 0 && elect_one()) {
         for (int k = 0; k < NRAW; ++k) mbar_init(rbar + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         for (int k = 0; k < NRAW && i0 + k <= i1 + 1; ++k)
@@ -542,7 +588,9 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
       double* sraw = rawring + (rk % NRAW) * SLOT;
       if (bulk) mbar_wait(rbar + rk % NRAW, (unsigned)((rk / NRAW) & 1));
       else cp_wait<NRAW - 1>();              // row r has landed (later rows may be in flight)
-      // ---- primitives of row r
+      // ---- primitives of row r (QPR: the own column's shared primitives also stay in registers
+      // for this step's fluxes of row r-1, whose x-derivatives read row r: 6 shared loads less)
+      double qown[NQ];
       {
         const RowRef Rr = row_ref(P, r);
         double* q = qring + ((r + 4) % 4) * NQ * QW;
@@ -554,7 +602,7 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
           double vj[MODE == MODE_JVN ? NF : 1];
           combine_cell<MODE>(xm, Rr.flip ? 0x80000000u : 0u, ymm, sigma, hnext, rh, fh, u,
                              MODE == MODE_JVN ? vj : nullptr);
-          cell_prims(P, u, q + cmain, cq + cmain, QW, flag);
+          cell_prims(P, u, q + cmain, cq + cmain, QW, flag, QPR ? qown : nullptr);
           if (MODE == MODE_JVN && r >= i0 && r < i1 && t < ncols_out) {
             // v_j = w / h_next of an owned cell (krylov.py:167), computed once for the stencil
             // input above (the ghost flips apply to u only, never to the stored basis entry)
@@ -587,10 +635,14 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
       // row r-3 (last read by the outputs of row r-3, previous step); centre quantities
       // are private to their thread.
       __syncthreads();
-      if (bulk && tid == 0 && r + NRAW <= i1 + 1) {
+      if (bulk && warp_u == 0 && r + NRAW <= i1 + 1) {
+        // warp-uniform branch, one elected lane issues: the row's source addresses stay in
+        // uniform registers (no per-copy vector-to-uniform hand-over).
         // generic-proxy reads of the row (before the barrier) precede the async-proxy refill
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        fetch_row_bulk<MODE, QW>(P, row_ref(P, r + NRAW), j0 - 2, sraw, rbar + rk % NRAW);
+        if (elect_one()) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          fetch_row_bulk<MODE, QW>(P, row_ref(P, r + NRAW), j0 - 2, sraw, rbar + rk % NRAW);
+        }
       }
       // ---- fluxes of row rf = r - 1
       const int rf = r - 1;
@@ -603,7 +655,7 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
         const bool out_row = (rf >= i0 && rf < i1);
         double gy[NF];
         if (t >= 0 && t < ncols_out) {
-          flux_cell<FXY>(P, qm, q0, qp, c0, cmain, QW, true, out_row, gxC, gy);
+          flux_cell<FXY>(P, qm, q0, qp, c0, cmain, QW, true, out_row, gxC, gy, QPR ? qown : nullptr);
           if (out_row) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) gyr[f * GYW + t + 1] = gy[f];
@@ -632,6 +684,12 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
       // ---- output row ro = r - 2: x-fluxes of rows ro+1 (gxC) and ro-1 (gxA) are this
       // thread's own registers; y-fluxes of row ro come from the ring (previous step)
       const int ro = r - 2;
+      // x-flux of row r-3 from this thread's ring slot, which then takes row r-1
+      double* gxs = gxring + ((r + 1) & 1) * NF * TY + (t >= 0 ? t : 0);
+      if (GXS && ro >= i0 && t >= 0 && t < ncols_out) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) gxA[f] = gxs[f * TY];
+      }
       if (ro >= i0 && t >= 0 && t < ncols_out) {
         const double* gyr = gyring + ((ro + 2) % 2) * NF * GYW;
         const unsigned o = (unsigned)ro * P.ny + j0 + t;
@@ -665,8 +723,15 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? 2 : 384 / TY
           for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + (o2 + f * plane));
         }
       }
+      if (GXS) {
+        if (rf >= i0 - 1 && t >= 0 && t < ncols_out) {
 #pragma unroll
-      for (int f = 0; f < NF; ++f) { gxA[f] = gxB[f]; gxB[f] = gxC[f]; }
+          for (int f = 0; f < NF; ++f) gxs[f * TY] = gxC[f];
+        }
+      } else {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) { gxA[f] = gxB[f]; gxB[f] = gxC[f]; }
+      }
     }
   }
 
@@ -1048,7 +1113,8 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
                             StencilPath* used) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NRAW * NARR * NF * QW) +
+  const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NRAW * NARR * NF * QW +
+                                     ((NRAW == 2 && EMHD_GX_SMEM) ? 2 * NF * TY : 0)) +
                     NRAW * sizeof(unsigned long long);
   auto k = stencil_kernel<TY, MODE, AUG, FXY, NRAW>;
   if ((long long)NF * P.nx * P.ny >= (1LL << 32)) return cudaErrorInvalidValue;   // 32-bit offsets
@@ -1101,11 +1167,18 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
 template <int TY, int FXY>
 static cudaError_t launch_f(const StencilParams& P, int mode, bool aug, int ns, cudaStream_t s,
                             const StencilPath& sel, StencilPath* used) {
-  if (mode == MODE_RHS) return launch_t<TY, MODE_RHS, false, FXY>(P, ns, s, sel, used);
-  if (mode == MODE_JV)
+  const bool two = two_raw_rows(mode, P, sel);
+  if (mode == MODE_RHS)
+    return two ? launch_t<TY, MODE_RHS, false, FXY, 2>(P, ns, s, sel, used)
+               : launch_t<TY, MODE_RHS, false, FXY>(P, ns, s, sel, used);
+  if (mode == MODE_JV) {
+    if (two)
+      return aug ? launch_t<TY, MODE_JV, true, FXY, 2>(P, ns, s, sel, used)
+                 : launch_t<TY, MODE_JV, false, FXY, 2>(P, ns, s, sel, used);
     return aug ? launch_t<TY, MODE_JV, true, FXY>(P, ns, s, sel, used)
                : launch_t<TY, MODE_JV, false, FXY>(P, ns, s, sel, used);
-  if (two_raw_rows(mode, P, sel))
+  }
+  if (two)
     return aug ? launch_t<TY, MODE_JVN, true, FXY, 2>(P, ns, s, sel, used)
                : launch_t<TY, MODE_JVN, false, FXY, 2>(P, ns, s, sel, used);
   return aug ? launch_t<TY, MODE_JVN, true, FXY>(P, ns, s, sel, used)
@@ -1125,9 +1198,9 @@ static cudaError_t launch_ty(const StencilParams& P, int mode, bool aug, int ns,
              : launch_f<TY, DIV_GENERAL>(P, mode, aug, ns, s, sel, used);
 }
 
-int stencil_tile_width(int ny, int forced) {
+int stencil_tile_width(int ny, int forced, bool two_rows) {
   if (forced == 32 || forced == 64 || forced == 128) return forced;
-  return ny <= 32 ? 32 : (ny <= 64 ? 64 : 128);
+  return ny <= 32 ? 32 : ((ny <= 64 || two_rows) ? 64 : 128);
 }
 
 static int env_int(const char* name, int dflt) {
@@ -1149,7 +1222,7 @@ StencilPath stencil_path_defaults() {
 
 cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s,
                            const StencilPath& sel, StencilPath* used) {
-  const int ty = stencil_tile_width(P.ny, sel.strip);
+  const int ty = stencil_tile_width(P.ny, sel.strip, two_raw_rows(mode, P, sel));
   if (ty == 32) return launch_ty<32>(P, mode, aug, num_sms, s, sel, used);
   if (ty == 64) return launch_ty<64>(P, mode, aug, num_sms, s, sel, used);
   return launch_ty<128>(P, mode, aug, num_sms, s, sel, used);

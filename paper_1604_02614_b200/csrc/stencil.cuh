@@ -50,13 +50,13 @@ struct StencilPath {
   int bulk;          // marching: interior strips stage raw rows with bulk async copies (when aligned)
   int min_rows;      // auto: floor of rows per CTA
   int tile_rows;     // auto: 2D tiles when a marching CTA would get fewer rows than this
-  int raw_rows;      // marching MODE_JVN: raw rows staged ahead (0 auto = 2, 1, 2)
+  int raw_rows;      // marching: raw rows staged ahead (0 auto: 2 for Jv / normalised Jv, 1 for RHS)
 };
 
 StencilPath stencil_path_defaults();   // EMHD_STENCIL_TY / _TMA / _TILE_ROWS, EMHD_MIN_ROWS
 cudaError_t launch_stencil(StencilParams P, int mode, bool aug, int num_sms, cudaStream_t s,
                            const StencilPath& sel, StencilPath* used = nullptr);
-int stencil_tile_width(int ny, int forced);
+int stencil_tile_width(int ny, int forced, bool two_rows);
 cudaError_t launch_diag(StencilParams P, int which, double* out, unsigned long long* dmax, cudaStream_t s);
 cudaError_t launch_admissibility(StencilParams P, int mode, unsigned long long* keys, cudaStream_t s);
 

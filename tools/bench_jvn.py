@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Micro-benchmark of the Arnoldi-loop stencil (fused normalise + Jv, MODE_JVN) per kernel
-variant: python tools/bench_jvn.py 1024,2048 [raw_rows,...] [strip,...]   (raw rows staged ahead: 1 or
-2; strip width 0 = default, 32 / 64 / 128 / 256)
+variant: python tools/bench_jvn.py 1024,2048 [raw_rows,...] [strip,...] [mode]   (raw rows staged ahead:
+1 or 2; strip width 0 = default, 32 / 64 / 96 / 128; mode jvn (default) / jv / rhs: the plain Jv
+(4W) and RHS (2W) launches of the same marching kernel)
 CUDA-event timed, back-to-back launches on inputs larger than L2 only from 2048^2 up; at 1024^2
 the a / w / F(a) / out set (320 MB) already exceeds the 126 MB L2."""
 import json
@@ -22,6 +23,8 @@ def main():
     sizes = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["1024"])]
     variants = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "2"])]
     strips = [int(x) for x in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["0"])]
+    mode = sys.argv[4] if len(sys.argv) > 4 else "jvn"
+    nw = {"jvn": 5, "jv": 4, "rhs": 2}[mode]
     res = []
     for n in sizes:
         g = fourier_grid(n)
@@ -40,7 +43,16 @@ def main():
         for rr, strip in [(r, st) for r in variants for st in strips]:
             f.ctx.stencil_path(kernel=1, raw_rows=rr, strip=strip)
 
+            vn = scal[1:2] / scal[0:1]
+
             def go():
+                if mode == "rhs":
+                    f.launch(a, out)
+                    return
+                if mode == "jv":
+                    N.check(L.emhd_jv(f.ctx.sync_stream(), a.data_ptr(), None, fa.data_ptr(), w.data_ptr(),
+                                      None, vn.data_ptr(), out.data_ptr()), "jv")
+                    return
                 N.check(L.emhd_jv_normalized(f.ctx.sync_stream(), a.data_ptr(), None, fa.data_ptr(),
                                              w.data_ptr(), None, scal.data_ptr(), vout.data_ptr(), 0, 1.0, 0,
                                              N.ptr_array([]), N.int_array([]), out.data_ptr()), "jvn")
@@ -62,8 +74,8 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 best = min(best, e0.elapsed_time(e1) * 1e3 / reps)
-            byts = 5 * a.numel() * 8
-            res.append({"n": n, "raw_rows": rr, "us": round(best, 2), "GBps": round(byts / best / 1e3, 1),
+            byts = nw * a.numel() * 8
+            res.append({"mode": mode, "n": n, "raw_rows": rr, "us": round(best, 2), "GBps": round(byts / best / 1e3, 1),
                         "ran": f.ctx.last_stencil(), "same_as_first": same})
     for r in res:
         print(json.dumps(r))
