@@ -24,9 +24,6 @@
 #ifndef EMHD_QP_REG
 #define EMHD_QP_REG 1
 #endif
-#ifndef EMHD_GX_SMEM
-#define EMHD_GX_SMEM 0
-#endif
 
 namespace emhd {
 
@@ -256,9 +253,16 @@ __device__ __forceinline__ void consume_raw(const double* slot, int c, RawCell<M
   }
 }
 
+// Shared-memory layout of a cell's primitives: 16-byte pairs, [pair][column] of double2, so the
+// flux stage reads two quantities per LDS.128 (the row step is bound by shared-memory
+// instructions).  Ring pairs (read by neighbours): (v0, v1) (v2, T) (B0, B1) (B2, p_tot);
+// centre pairs (read by the cell's own thread only): (rho, E) (mx, my).
+enum : int { PQ_V01 = 0, PQ_V2T, PQ_B01, PQ_B2P, NQP };
+enum : int { PC_RE = 0, PC_M, NCP };
+
 // pressure / admissibility / primitives (mhd.py:106-131, 176-181, 217-221)
 __device__ __forceinline__ void cell_prims(const StencilParams& P, const double u[NF],
-                                           double* q, double* cq, int qs, int& flag,
+                                           double2* q, double2* cq, int qs, int& flag,
                                            double* qreg = nullptr) {
   const double rho = u[0], mx = u[1], my = u[2], mz = u[3];
   const double b0 = u[4], b1 = u[5], b2 = u[6], en = u[7];
@@ -270,22 +274,17 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
   const double mag = __dmul_rn(P.bfac, bb);
   const double p = __dmul_rn(P.gm1, __dsub_rn(__dsub_rn(en, kin), mag));
   if (P.check && p <= 0.0) flag |= ST_PRESSURE;
-  cq[C_RHO * qs] = rho;
-  cq[C_MX * qs] = mx;
-  cq[C_MY * qs] = my;
-  cq[C_EN * qs] = en;
-  q[Q_B0 * qs] = b0;
-  q[Q_B1 * qs] = b1;
-  q[Q_B2 * qs] = b2;
   const double v0 = div_const(mx, rho, rr);   // == mx / rho bit for bit
   const double v1 = div_const(my, rho, rr);
   const double v2 = div_const(mz, rho, rr);
   const double tt = div_const(p, rho, rr);
-  q[Q_V0 * qs] = v0;
-  q[Q_V1 * qs] = v1;
-  q[Q_V2 * qs] = v2;
-  q[Q_T * qs] = tt;
-  cq[C_PT * qs] = __dadd_rn(p, __dmul_rn(0.5, bb));
+  const double pt = __dadd_rn(p, __dmul_rn(0.5, bb));
+  cq[PC_RE * qs] = make_double2(rho, en);
+  cq[PC_M * qs] = make_double2(mx, my);
+  q[PQ_B01 * qs] = make_double2(b0, b1);
+  q[PQ_V01 * qs] = make_double2(v0, v1);
+  q[PQ_V2T * qs] = make_double2(v2, tt);
+  q[PQ_B2P * qs] = make_double2(b2, pt);
   if (qreg) {
     qreg[Q_V0] = v0; qreg[Q_V1] = v1; qreg[Q_V2] = v2;
     qreg[Q_B0] = b0; qreg[Q_B1] = b1; qreg[Q_B2] = b2; qreg[Q_T] = tt;
@@ -295,25 +294,32 @@ __device__ __forceinline__ void cell_prims(const StencilParams& P, const double 
 // x- and y-flux G = F_hyp - F_diff at one cell (mhd.py:174-197, 209-266, 275-276).
 // c: prim column slot of the cell; qm/q0/qp: prim rows i-1, i, i+1; c0: centre row i.
 template <int FXY>
-__device__ __forceinline__ void flux_cell(const StencilParams& P, const double* qm,
-                                          const double* q0, const double* qp, const double* c0,
+__device__ __forceinline__ void flux_cell(const StencilParams& P, const double2* qm,
+                                          const double2* q0, const double2* qp, const double2* c0,
                                           int c, int qs,
                                           bool need_x, bool need_y, double gx[NF], double gy[NF],
                                           const double* qpreg = nullptr) {
-#define QV(row, k, col) row[(k) * qs + (col)]
-#define QP(k) (qpreg ? qpreg[k] : QV(qp, k, c))
   const double thx = P.two_hx, rhx = P.r_two_hx, thy = P.two_hy, rhy = P.r_two_hy;
+  // row i+1 of the own column: from registers when the caller kept them (QPR)
+  const double2 pV = qpreg ? make_double2(qpreg[Q_V0], qpreg[Q_V1]) : qp[PQ_V01 * qs + c];
+  const double2 pB = qpreg ? make_double2(qpreg[Q_B0], qpreg[Q_B1]) : qp[PQ_B01 * qs + c];
+  const double2 mV = qm[PQ_V01 * qs + c], mB = qm[PQ_B01 * qs + c];
+  const double2 rV = q0[PQ_V01 * qs + c + 1], lV = q0[PQ_V01 * qs + c - 1];
+  const double2 rB = q0[PQ_B01 * qs + c + 1], lB = q0[PQ_B01 * qs + c - 1];
   // centred derivatives of v, B, T at the cell (mhd.py:224-227, 261, 264)
-  const double dvx0 = div_c<FXY>(__dsub_rn(QP(Q_V0), QV(qm, Q_V0, c)), thx, rhx);
-  const double dvx1 = div_c<FXY>(__dsub_rn(QP(Q_V1), QV(qm, Q_V1, c)), thx, rhx);
-  const double dvy0 = div_c<FXY>(__dsub_rn(QV(q0, Q_V0, c + 1), QV(q0, Q_V0, c - 1)), thy, rhy);
-  const double dvy1 = div_c<FXY>(__dsub_rn(QV(q0, Q_V1, c + 1), QV(q0, Q_V1, c - 1)), thy, rhy);
-  const double dBx1 = div_c<FXY>(__dsub_rn(QP(Q_B1), QV(qm, Q_B1, c)), thx, rhx);
-  const double dBy0 = div_c<FXY>(__dsub_rn(QV(q0, Q_B0, c + 1), QV(q0, Q_B0, c - 1)), thy, rhy);
+  const double dvx0 = div_c<FXY>(__dsub_rn(pV.x, mV.x), thx, rhx);
+  const double dvx1 = div_c<FXY>(__dsub_rn(pV.y, mV.y), thx, rhx);
+  const double dvy0 = div_c<FXY>(__dsub_rn(rV.x, lV.x), thy, rhy);
+  const double dvy1 = div_c<FXY>(__dsub_rn(rV.y, lV.y), thy, rhy);
+  const double dBx1 = div_c<FXY>(__dsub_rn(pB.y, mB.y), thx, rhx);
+  const double dBy0 = div_c<FXY>(__dsub_rn(rB.x, lB.x), thy, rhy);
 
-  const double rho = QV(c0, C_RHO, c), en = QV(c0, C_EN, c), pt = QV(c0, C_PT, c);
-  const double v0 = QV(q0, Q_V0, c), v1 = QV(q0, Q_V1, c), v2 = QV(q0, Q_V2, c);
-  const double b0 = QV(q0, Q_B0, c), b1 = QV(q0, Q_B1, c), b2 = QV(q0, Q_B2, c);
+  const double2 cRE = c0[PC_RE * qs + c], cM = c0[PC_M * qs + c];
+  const double2 cV = q0[PQ_V01 * qs + c], cV2 = q0[PQ_V2T * qs + c];
+  const double2 cB = q0[PQ_B01 * qs + c], cB2 = q0[PQ_B2P * qs + c];
+  const double rho = cRE.x, en = cRE.y, pt = cB2.y;
+  const double v0 = cV.x, v1 = cV.y, v2 = cV2.x;
+  const double b0 = cB.x, b1 = cB.y, b2 = cB2.x;
   const double mu = P.mu, eta = P.eta, heat = P.heat;
 
   const double divv = __dadd_rn(dvx0, dvy1);
@@ -325,9 +331,12 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
   const double r0 = __dmul_rn(rho, v0), r1 = __dmul_rn(rho, v1), r2 = __dmul_rn(rho, v2);
 
   if (need_x) {
-    const double dvx2 = div_c<FXY>(__dsub_rn(QP(Q_V2), QV(qm, Q_V2, c)), thx, rhx);
-    const double dBx2 = div_c<FXY>(__dsub_rn(QP(Q_B2), QV(qm, Q_B2, c)), thx, rhx);
-    const double dTx = div_c<FXY>(__dsub_rn(QP(Q_T), QV(qm, Q_T, c)), thx, rhx);
+    const double2 pV2 = qpreg ? make_double2(qpreg[Q_V2], qpreg[Q_T]) : qp[PQ_V2T * qs + c];
+    const double pB2 = qpreg ? qpreg[Q_B2] : qp[PQ_B2P * qs + c].x;
+    const double2 mV2 = qm[PQ_V2T * qs + c];
+    const double dvx2 = div_c<FXY>(__dsub_rn(pV2.x, mV2.x), thx, rhx);
+    const double dBx2 = div_c<FXY>(__dsub_rn(pB2, qm[PQ_B2P * qs + c].x), thx, rhx);
+    const double dTx = div_c<FXY>(__dsub_rn(pV2.y, mV2.y), thx, rhx);
     const double tau_xx = __dsub_rn(__dmul_rn(2.0, dvx0), c23d);
     // diffusive x-flux (mhd.py:244-262)
     const double fmx = __dmul_rn(mu, tau_xx);
@@ -340,7 +349,7 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
     const double res = __dmul_rn(eta, __dadd_rn(__dmul_rn(b1, curl), __dmul_rn(b2, dBx2)));
     const double fen = __dadd_rn(__dadd_rn(visc, __dmul_rn(heat, dTx)), res);
     // hyperbolic x-flux (mhd.py:185-196) minus diffusive
-    gx[0] = QV(c0, C_MX, c);
+    gx[0] = cM.x;
     gx[1] = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(r0, v0), __dmul_rn(b0, b0)), pt), fmx);
     gx[2] = __dsub_rn(__dsub_rn(__dmul_rn(r1, v0), __dmul_rn(b1, b0)), fmy);
     gx[3] = __dsub_rn(__dsub_rn(__dmul_rn(r2, v0), __dmul_rn(b2, b0)), fmz);
@@ -350,9 +359,10 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
     gx[7] = __dsub_rn(__dsub_rn(__dmul_rn(ept, v0), __dmul_rn(b0, bv)), fen);
   }
   if (need_y) {
-    const double dvy2 = div_c<FXY>(__dsub_rn(QV(q0, Q_V2, c + 1), QV(q0, Q_V2, c - 1)), thy, rhy);
-    const double dBy2 = div_c<FXY>(__dsub_rn(QV(q0, Q_B2, c + 1), QV(q0, Q_B2, c - 1)), thy, rhy);
-    const double dTy = div_c<FXY>(__dsub_rn(QV(q0, Q_T, c + 1), QV(q0, Q_T, c - 1)), thy, rhy);
+    const double2 rV2 = q0[PQ_V2T * qs + c + 1], lV2 = q0[PQ_V2T * qs + c - 1];
+    const double dvy2 = div_c<FXY>(__dsub_rn(rV2.x, lV2.x), thy, rhy);
+    const double dBy2 = div_c<FXY>(__dsub_rn(q0[PQ_B2P * qs + c + 1].x, q0[PQ_B2P * qs + c - 1].x), thy, rhy);
+    const double dTy = div_c<FXY>(__dsub_rn(rV2.y, lV2.y), thy, rhy);
     const double tau_yy = __dsub_rn(__dmul_rn(2.0, dvy1), c23d);
     // diffusive y-flux (mhd.py:245-265)
     const double fmx = __dmul_rn(mu, tau_xy);
@@ -364,7 +374,7 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
                                                 __dmul_rn(dvy2, v2)));
     const double res = __dmul_rn(eta, __dadd_rn(__dmul_rn(b0, __dsub_rn(dBy0, dBx1)), __dmul_rn(b2, dBy2)));
     const double fen = __dadd_rn(__dadd_rn(visc, __dmul_rn(heat, dTy)), res);
-    gy[0] = QV(c0, C_MY, c);
+    gy[0] = cM.y;
     gy[1] = __dsub_rn(__dsub_rn(__dmul_rn(r0, v1), __dmul_rn(b0, b1)), fmx);
     gy[2] = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(r1, v1), __dmul_rn(b1, b1)), pt), fmy);
     gy[3] = __dsub_rn(__dsub_rn(__dmul_rn(r2, v1), __dmul_rn(b2, b1)), fmz);
@@ -373,8 +383,6 @@ __device__ __forceinline__ void flux_cell(const StencilParams& P, const double* 
     gy[6] = __dsub_rn(__dsub_rn(__dmul_rn(v1, b2), __dmul_rn(b1, v2)), fbz);
     gy[7] = __dsub_rn(__dsub_rn(__dmul_rn(ept, v1), __dmul_rn(b1, bv)), fen);
   }
-#undef QP
-#undef QV
 }
 
 // raw input rows in flight per CTA (NR): row r+NR is requested while row r is consumed.  NR = 2
@@ -402,28 +410,23 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
   constexpr bool HW = NR == 2;
   constexpr int QW = TY + 4;         // prim columns (2-cell halo each side)
   constexpr int GYW = TY + 2;        // y-flux columns (1-cell halo each side)
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   // rings sized so ONE barrier per row step suffices (see the loop): primitives 4 rows,
   // y-fluxes 2 rows, thread-private centre quantities 2 rows, NRAW raw rows in flight;
-  // x-fluxes live in registers of the column's own thread.  ~72 KB at TY=128 with one raw
-  // row (3 CTAs/SM), ~90 KB with two (2 CTAs/SM)
-  double* qring = smem;                             // [4][NQ][QW]
-  double* gyring = qring + 4 * NQ * QW;             // [2][NF][GYW]
-  double* cring = gyring + 2 * NF * GYW;            // [2][NC][QW]
+  // x-fluxes live in registers of the column's own thread.  ~76 KB at TY=128 with one raw
+  // row (2-3 CTAs/SM), ~49 KB at TY=64 with two (4 CTAs/SM)
+  double2* qring = reinterpret_cast<double2*>(smem);              // [4][NQP][QW] pairs
+  double2* gyring = qring + 4 * NQP * QW;                         // [2][NF/2][GYW] pairs (f, f+1)
+  double2* cring = gyring + 2 * (NF / 2) * GYW;                   // [2][NCP][QW] pairs
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
   constexpr int NRAW = NR;
-  double* rawring = cring + 2 * NC * QW;            // [NRAW][NARR*NF][QW] raw rows in flight
-  // GXS: the x-flux history (rows r-3, r-2) in a thread-private shared-memory ring [2][NF][TY]
-  // instead of a rotated register ring (16 register moves less per row, 147 instead of 167
-  // registers).  Measured slower (normalised Jv 1024^2 64.9 -> 75.0 us, Jv 56.9 -> 61.2 us): the
-  // row step is bound by shared-memory instructions, not by the moves.  Off.
-  constexpr bool GXS = HW && EMHD_GX_SMEM;
-  // measured (tools/bench_jvn.py): RHS 1024^2 42.3 -> 41.5 us, 2048^2 145.8 -> 142.9 us; the Jv
+  double* rawring = reinterpret_cast<double*>(cring + 2 * NCP * QW);   // [NRAW][NARR*NF][QW] raw rows in flight
+  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(rawring + NRAW * NARR * NF * QW);
+  // QPR: the own column's next-row primitives stay in registers from the primitive stage to the
+  // flux stage; measured (tools/bench_jvn.py): RHS 1024^2 42.3 -> 41.5 us, 2048^2 145.8 -> 142.9 us; the Jv
   // variants are at their 168-register cap (4 CTAs/SM) and spill with it (normalised Jv 64.7 ->
   // 85.9 us), so only the RHS takes it
   constexpr bool QPR = EMHD_QP_REG != 0 && MODE == MODE_RHS;
-  double* gxring = rawring + NRAW * NARR * NF * QW;
-  unsigned long long* rbar = reinterpret_cast<unsigned long long*>(gxring + (GXS ? 2 * NF * TY : 0));
 
   pdl_sync();
   const int tid = threadIdx.x;
@@ -533,8 +536,8 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
     // prologue: primitives of rows i0-2 and i0-1
     for (int r = i0 - 2; r < i0; ++r) {
       const RowRef R = row_ref(P, r);
-      double* q = qring + ((r + 4) % 4) * NQ * QW;
-      double* cq = cring + ((r + 2) % 2) * NC * QW;
+      double2* q = qring + ((r + 4) % 4) * NQP * QW;
+      double2* cq = cring + ((r + 2) % 2) * NCP * QW;
       double u[NF];
       if (okm) {
         load_cell<MODE>(P, R, jm, fm, sigma, hnext, rh, u);
@@ -556,10 +559,6 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
     double gxA[NF], gxB[NF], gxC[NF];        // x-fluxes of rows r-3, r-2, r-1 (own column)
 #pragma unroll
     for (int f = 0; f < NF; ++f) { gxA[f] = 0.0; gxB[f] = 0.0; gxC[f] = 0.0; }
-    if (GXS && t >= 0) {
-#pragma unroll
-      for (int f = 0; f < NF; ++f) { gxring[f * TY + t] = 0.0; gxring[(NF + f) * TY + t] = 0.0; }
-    }
     // interior strips (no y-ghost columns) stream whole row segments with bulk async copies
     // issued by thread 0 (tracked by one mbarrier); edge strips keep per-thread cp.async
     const bool bulk = P.tma && j0 >= 2 && j0 + TY + 2 <= P.ny;
@@ -593,8 +592,8 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
       double qown[NQ];
       {
         const RowRef Rr = row_ref(P, r);
-        double* q = qring + ((r + 4) % 4) * NQ * QW;
-        double* cq = cring + ((r + 2) % 2) * NC * QW;
+        double2* q = qring + ((r + 4) % 4) * NQP * QW;
+        double2* cq = cring + ((r + 2) % 2) * NCP * QW;
         double u[NF];
         if (okm) {
           RawCell<MODE> xm;
@@ -647,18 +646,18 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
       // ---- fluxes of row rf = r - 1
       const int rf = r - 1;
       if (rf >= i0 - 1) {
-        const double* qm = qring + ((rf + 3) % 4) * NQ * QW;
-        const double* q0 = qring + ((rf + 4) % 4) * NQ * QW;
-        const double* qp = qring + ((rf + 5) % 4) * NQ * QW;
-        const double* c0 = cring + ((rf + 2) % 2) * NC * QW;
-        double* gyr = gyring + ((rf + 2) % 2) * NF * GYW;
+        const double2* qm = qring + ((rf + 3) % 4) * NQP * QW;
+        const double2* q0 = qring + ((rf + 4) % 4) * NQP * QW;
+        const double2* qp = qring + ((rf + 5) % 4) * NQP * QW;
+        const double2* c0 = cring + ((rf + 2) % 2) * NCP * QW;
+        double2* gyr = gyring + ((rf + 2) % 2) * (NF / 2) * GYW;
         const bool out_row = (rf >= i0 && rf < i1);
         double gy[NF];
         if (t >= 0 && t < ncols_out) {
           flux_cell<FXY>(P, qm, q0, qp, c0, cmain, QW, true, out_row, gxC, gy, QPR ? qown : nullptr);
           if (out_row) {
 #pragma unroll
-            for (int f = 0; f < NF; ++f) gyr[f * GYW + t + 1] = gy[f];
+            for (int f = 0; f < NF; f += 2) gyr[(f / 2) * GYW + t + 1] = make_double2(gy[f], gy[f + 1]);
           }
         }
         if (out_row) {
@@ -677,27 +676,27 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
             double gdummy[NF];
             flux_cell<FXY>(P, qm, q0, qp, c0, cs, QW, false, true, gdummy, gy);
 #pragma unroll
-            for (int f = 0; f < NF; ++f) gyr[f * GYW + gslot] = gy[f];
+            for (int f = 0; f < NF; f += 2) gyr[(f / 2) * GYW + gslot] = make_double2(gy[f], gy[f + 1]);
           }
         }
       }
       // ---- output row ro = r - 2: x-fluxes of rows ro+1 (gxC) and ro-1 (gxA) are this
       // thread's own registers; y-fluxes of row ro come from the ring (previous step)
       const int ro = r - 2;
-      // x-flux of row r-3 from this thread's ring slot, which then takes row r-1
-      double* gxs = gxring + ((r + 1) & 1) * NF * TY + (t >= 0 ? t : 0);
-      if (GXS && ro >= i0 && t >= 0 && t < ncols_out) {
-#pragma unroll
-        for (int f = 0; f < NF; ++f) gxA[f] = gxs[f * TY];
-      }
       if (ro >= i0 && t >= 0 && t < ncols_out) {
-        const double* gyr = gyring + ((ro + 2) % 2) * NF * GYW;
+        const double2* gyr = gyring + ((ro + 2) % 2) * (NF / 2) * GYW;
+        double gyp[NF], gym[NF];             // y-fluxes at columns j+1, j-1 (two fields per load)
+#pragma unroll
+        for (int f = 0; f < NF; f += 2) {
+          const double2 a = gyr[(f / 2) * GYW + t + 2], b = gyr[(f / 2) * GYW + t];
+          gyp[f] = a.x; gyp[f + 1] = a.y; gym[f] = b.x; gym[f + 1] = b.y;
+        }
         const unsigned o = (unsigned)ro * P.ny + j0 + t;
         unsigned nfmask = 0;                 // bit f: F of field f is inf / nan
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
           const double ddx = div_c<FXY>(__dsub_rn(gxC[f], gxA[f]), P.two_hx, P.r_two_hx);
-          const double ddy = div_c<FXY>(__dsub_rn(gyr[f * GYW + t + 2], gyr[f * GYW + t]), P.two_hy, P.r_two_hy);
+          const double ddy = div_c<FXY>(__dsub_rn(gyp[f], gym[f]), P.two_hy, P.r_two_hy);
           double F = __dsub_rn(-ddx, ddy);                    // -ddx(gx) - ddy(gy) (mhd.py:277)
           const unsigned idx = o + f * plane;
           if (MODE == MODE_RHS) {
@@ -723,15 +722,8 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
           for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + (o2 + f * plane));
         }
       }
-      if (GXS) {
-        if (rf >= i0 - 1 && t >= 0 && t < ncols_out) {
 #pragma unroll
-          for (int f = 0; f < NF; ++f) gxs[f * TY] = gxC[f];
-        }
-      } else {
-#pragma unroll
-        for (int f = 0; f < NF; ++f) { gxA[f] = gxB[f]; gxB[f] = gxC[f]; }
-      }
+      for (int f = 0; f < NF; ++f) { gxA[f] = gxB[f]; gxB[f] = gxC[f]; }
     }
   }
 
@@ -783,16 +775,16 @@ constexpr int TT_R = 8, TT_C = 32, TT_THREADS = TT_R * TT_C;
 constexpr int TT_QR = TT_R + 4, TT_QC = TT_C + 4, TT_QN = TT_QR * TT_QC;   // primitive region
 
 size_t tile_stencil_smem() {
-  return sizeof(double) * ((size_t)(NQ + NC) * TT_QN + (size_t)NF * (TT_R + 2) * TT_C +
+  return sizeof(double) * ((size_t)2 * (NQP + NCP) * TT_QN + (size_t)NF * (TT_R + 2) * TT_C +
                            (size_t)NF * TT_R * (TT_C + 2));
 }
 
 template <int MODE, bool AUG, int FXY>
 __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const StencilParams P) {
-  extern __shared__ double smem[];
-  double* q = smem;                                   // [NQ][TT_QR][TT_QC]
-  double* cq = q + NQ * TT_QN;                        // [NC][TT_QR][TT_QC]
-  double* gxs = cq + NC * TT_QN;                      // [NF][TT_R + 2][TT_C]   rows -1 .. TR
+  extern __shared__ __align__(16) double smem[];
+  double2* q = reinterpret_cast<double2*>(smem);      // [NQP][TT_QR][TT_QC] pairs
+  double2* cq = q + NQP * TT_QN;                      // [NCP][TT_QR][TT_QC] pairs
+  double* gxs = reinterpret_cast<double*>(cq + NCP * TT_QN);   // [NF][TT_R + 2][TT_C]   rows -1 .. TR
   double* gys = gxs + NF * (TT_R + 2) * TT_C;         // [NF][TT_R][TT_C + 2]   cols -1 .. TC
   pdl_sync();
   const int t = threadIdx.x;
@@ -1113,8 +1105,7 @@ static cudaError_t launch_t(StencilParams P, int num_sms, cudaStream_t s, const 
                             StencilPath* used) {
   constexpr int QW = TY + 4, GYW = TY + 2;
   constexpr int NARR = MODE == MODE_RHS ? 1 : 2;
-  const size_t sm = sizeof(double) * (4 * NQ * QW + 2 * NF * GYW + 2 * NC * QW + NRAW * NARR * NF * QW +
-                                     ((NRAW == 2 && EMHD_GX_SMEM) ? 2 * NF * TY : 0)) +
+  const size_t sm = sizeof(double) * (4 * 2 * NQP * QW + 2 * NF * GYW + 2 * 2 * NCP * QW + NRAW * NARR * NF * QW) +
                     NRAW * sizeof(unsigned long long);
   auto k = stencil_kernel<TY, MODE, AUG, FXY, NRAW>;
   if ((long long)NF * P.nx * P.ny >= (1LL << 32)) return cudaErrorInvalidValue;   // 32-bit offsets
