@@ -266,11 +266,17 @@ def test_config2_jv_and_normalised_jv_bitwise_1024(P):
     assert np.array_equal(case.jv(v), case.jo(v))
     r = case.ran()
     assert r["kernel"] == 1 and r["bulk"] == 1, r
+    # the default launch shape of the Jv variants: 64-column strips (4 CTAs/SM), one wave
+    assert r["strip"] == 64, r
     w = case.jo(v)
     h = float(np.linalg.norm(w))
     out, vout = case.jv_normalized(w, h)
+    assert case.ran()["strip"] == 64
     assert np.array_equal(vout, w / h)
     assert np.array_equal(out, case.jo(w / h))
+    # the RHS keeps 128-column strips with one staged row
+    assert np.array_equal(case.rhs(), case.fo(case.a))
+    assert case.ran()["strip"] == 128, case.ran()
     # through the public operator as well
     op = P.FdJacobianOperator(case.f, case.a_d)
     assert np.array_equal(op(v), case.jo(v))
@@ -315,8 +321,14 @@ def test_harris_2048_jv_bitwise(P):
     U = P.reconnection_ic(g, params=prm)
     case = Case(P, g, prm, P.default_bc("reconnection"), U)
     v = np.random.default_rng(2048).standard_normal(U.size)
-    assert np.array_equal(case.jv(v), case.jo(v))
-    assert case.ran()["kernel"] == 1
+    ref = case.jo(v)
+    assert np.array_equal(case.jv(v), ref)
+    assert case.ran()["kernel"] == 1 and case.ran()["strip"] == 64
+    # the Arnoldi-loop launch on the same grid: v_j = w / h written and J v_j
+    h = float(np.linalg.norm(ref))
+    out, vout = case.jv_normalized(ref, h)
+    assert np.array_equal(vout, ref / h)
+    assert np.array_equal(out, case.jo(ref / h))
 
 
 @pytest.mark.slow
