@@ -380,6 +380,10 @@ def run_ours(args):
     out["roofline"] = {"bound": "hbm", "achieved": top["alg_GBps"], "peak": hbm, "unit": "GB/s",
                        "frac": top["alg_GBps"] / hbm, "traffic": traffic,
                        "kernel": top["kernel"], "peak_source": hbm_src,
+                       "traffic_of": "ncu --set full capture of ONE launch of this kernel (profiles/*_ncu_full.json "
+                                     "via profiles/summarize.py): compare it with that launch's own algorithmic "
+                                     "bytes, (nvec+2)*L*8 with nvec = round(traffic / (L*8)) - 2; `achieved` "
+                                     "averages the launches j = 0..m-1 of the timed steps",
                        "alg_bytes_rule": "multidot (nvec+1)*L*8, update (nvec+2)*L*8, "
                                          "jv_normalized 5W, jv 4W, rhs 2W (SURVEY 8d)"}
     out["kernels"] = kern
