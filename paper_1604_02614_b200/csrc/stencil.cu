@@ -692,7 +692,9 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
           gyp[f] = a.x; gyp[f + 1] = a.y; gym[f] = b.x; gym[f + 1] = b.y;
         }
         const unsigned o = (unsigned)ro * P.ny + j0 + t;
-        unsigned nfmask = 0;                 // bit f: F of field f is inf / nan
+        // |F| high words: F of field f is inf / nan <=> fhi[f] >= 0x7ff00000 (one AND per field
+        // and a running maximum; which field only matters on the rare path below)
+        unsigned fhi[NF], fhmax = 0;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
           const double ddx = div_c<FXY>(__dsub_rn(gxC[f], gxA[f]), P.two_hx, P.r_two_hx);
@@ -702,17 +704,20 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
           if (MODE == MODE_RHS) {
             P.out[idx] = F;
           } else {
-            // exponent all ones <=> bit 31 of (hi & 0x7ff00000) + 2^20
-            nfmask |= (((unsigned)__double2hiint(F) & 0x7ff00000u) + 0x00100000u) >> (31 - f) & (1u << f);
+            fhi[f] = (unsigned)__double2hiint(F) & 0x7fffffffu;
+            fhmax = max(fhmax, fhi[f]);
             const double df = __dsub_rn(F, fa_pre[f]);
             double jv = fsig ? div_const1(df, sigma, rsig) : div_const(df, sigma, rsig);   // fdjac.py:49
             if (AUG) jv = aug_add(P, qb, idx, __dmul_rn(P.ch, jv));
             P.out[idx] = jv;
           }
         }
-        if (MODE != MODE_RHS && nfmask) {
+        if (MODE != MODE_RHS && fhmax >= 0x7ff00000u) {
           // rare path: flat index (global (8, nxg, ny) order) of the first bad field
-          const unsigned long long gidx = (unsigned long long)(__ffs(nfmask) - 1) * P.nxg * P.ny +
+          int fb = NF - 1;
+#pragma unroll
+          for (int f = NF - 2; f >= 0; --f) fb = fhi[f] >= 0x7ff00000u ? f : fb;
+          const unsigned long long gidx = (unsigned long long)fb * P.nxg * P.ny +
               (unsigned long long)(P.x_off + ro) * P.ny + j0 + t;
           bad = gidx < bad ? gidx : bad;
         }
@@ -904,7 +909,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
     __syncthreads();
     // phase 3: outputs (as the marching kernel's output stage)
     if (own) {
-      unsigned nfmask = 0;
+      unsigned fhi[NF], fhmax = 0;
 #pragma unroll
       for (int f = 0; f < NF; ++f) {
         const double* gxf = gxs + f * (TT_R + 2) * TT_C;
@@ -916,15 +921,19 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tile_stencil_kernel(const Stenc
         if (MODE == MODE_RHS) {
           P.out[idx] = F;
         } else {
-          nfmask |= (((unsigned)__double2hiint(F) & 0x7ff00000u) + 0x00100000u) >> (31 - f) & (1u << f);
+          fhi[f] = (unsigned)__double2hiint(F) & 0x7fffffffu;
+          fhmax = max(fhmax, fhi[f]);
           const double df = __dsub_rn(F, __ldg(P.fa + idx));
           double jv = fsig ? div_const1(df, sigma, rsig) : div_const(df, sigma, rsig);
           if (AUG) jv = aug_add(P, qb, idx, __dmul_rn(P.ch, jv));
           P.out[idx] = jv;
         }
       }
-      if (MODE != MODE_RHS && nfmask) {
-        const unsigned long long gidx = (unsigned long long)(__ffs(nfmask) - 1) * P.nxg * P.ny +
+      if (MODE != MODE_RHS && fhmax >= 0x7ff00000u) {
+        int fb = NF - 1;
+#pragma unroll
+        for (int f = NF - 2; f >= 0; --f) fb = fhi[f] >= 0x7ff00000u ? f : fb;
+        const unsigned long long gidx = (unsigned long long)fb * P.nxg * P.ny +
             (unsigned long long)(P.x_off + i0 + ro) * P.ny + j0 + co;
         bad = gidx < bad ? gidx : bad;
       }

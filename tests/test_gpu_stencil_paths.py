@@ -342,3 +342,37 @@ def test_harris_4096_jv_bitwise(P):
     got = case.jv(v)
     assert case.ran()["kernel"] == 1
     assert np.array_equal(got, case.jo(v))
+
+
+@pytest.mark.parametrize("kernel,strip", [(1, 32), (1, 64), (2, 0)])
+def test_nonfinite_component_named_by_every_kernel(P, kernel, strip):
+    """The first non-finite Jv component (fdjac.py:47-48) is named identically by the marching
+    kernel (either strip width) and the 2D-tile kernel: several fields and cells go non-finite,
+    the reference reports the smallest flat index."""
+    from oracle import jvp, stencil
+    g = P.Grid2D(12, 70, 0.0, 1.0, 0.0, 1.0)
+    prm = P.MhdParams()
+    bc = P.BoundaryPolicy("periodic", "periodic")
+    U = np.zeros((8, 12, 70))
+    U[0] = 1.0
+    U[7] = 2.0
+    U[1, 5, 40] = 1e200          # momentum^2 overflows in the perturbed state
+    U[7, 5, 40] = 1e308
+    U[2, 9, 3] = 1e200
+    U[7, 9, 3] = 1e308
+    v = np.zeros(U.size)
+    v[5] = 1.0
+    fa = np.zeros(U.size)
+    ref = jvp.FdJv(stencil.rhs_closure(prm, g, bc, check=False), U.reshape(-1), fa)
+    with pytest.raises(FloatingPointError) as want:
+        ref(v)
+    f = P.make_rhs(prm, g, bc, check=False)
+    if kernel == 1:
+        f.ctx.stencil_path(kernel=1, strip=strip, rows_per_cta=5)
+    else:
+        f.ctx.stencil_path(kernel=2)
+    op = P.FdJacobianOperator(f, U.reshape(-1), fa)
+    with pytest.raises(FloatingPointError) as got:
+        op(v)
+    assert f.ctx.last_stencil()["kernel"] == kernel
+    assert str(got.value) == str(want.value)
