@@ -301,6 +301,37 @@ def run_ours(args):
                  "us_per_jv": jv_ms * 1e3 / args.jv, "alg_GBps_per_gpu": jv_gbs / world,
                  "frac_of_hbm": jv_gbs / world / hbm}
 
+    # ---- the Arnoldi loop's stencil (fused normalise + Jv, 5W) launched back to back: the same
+    # kernel as the `emhd_jv_normalized` entry of `kernels` below, without the loop's power-capped
+    # clocks and without the per-launch event bracketing of the profile run (single rank only)
+    if world == 1:
+        from paper_1604_02614_b200 import _native as N
+        L = f.ctx.lib
+        wv = jout.clone()
+        sc = torch.tensor([float(wv.norm()), float(wv.abs().max()), 0.0, 0.0], dtype=torch.float64,
+                          device="cuda")
+        vout = torch.empty_like(a)
+        nout = torch.empty_like(a)
+
+        def jvn():
+            N.check(L.emhd_jv_normalized(f.ctx.sync_stream(), a.data_ptr(), None, op.f_a.data_ptr(),
+                                         wv.data_ptr(), None, sc.data_ptr(), vout.data_ptr(), 0, 1.0, 0,
+                                         N.ptr_array([]), N.int_array([]), nout.data_ptr()), "jv_normalized")
+        for _ in range(3):
+            jvn()
+        torch.cuda.synchronize()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record()
+        for _ in range(args.jv):
+            jvn()
+        n1.record()
+        torch.cuda.synchronize()
+        jvn_us = n0.elapsed_time(n1) * 1e3 / args.jv
+        jvn_gbs = 5.0 * 8.0 * n_local / (jvn_us * 1e-6) / 1e9
+        out["jv_normalized_back_to_back"] = {"launches": args.jv, "us": jvn_us, "alg_GBps": jvn_gbs,
+                                             "frac_of_hbm": jvn_gbs / hbm, "ran": f.ctx.last_stencil()}
+        del wv, vout, nout
+
     # ---- the same K steps with the second Gram-Schmidt pass in every iteration (the
     # reference's order of work: selective re-orthogonalisation off, EMHD_REORTH_ETA=0)
     if not args.no_two_pass:
