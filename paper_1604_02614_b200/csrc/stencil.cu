@@ -21,6 +21,9 @@
 #include "emhd_common.cuh"
 #include "stencil.cuh"
 
+#ifndef EMHD_PFB
+#define EMHD_PFB 1
+#endif
 #ifndef EMHD_QP_REG
 #define EMHD_QP_REG 1
 #endif
@@ -725,6 +728,20 @@ __global__ void __launch_bounds__(NR == 2 ? TY + 32 : TY, NR == 2 ? (TY == 64 ? 
           const unsigned o2 = o + P.ny;
 #pragma unroll
           for (int f = 0; f < NF; ++f) fa_pre[f] = __ldg(P.fa + (o2 + f * plane));
+        }
+        if (AUG && EMHD_PFB > 0 && ro + EMHD_PFB < i1 && (t & 3) == 0) {
+          // the B columns of the augmented epilogue are read just in time (no registers to
+          // stage them): ask L2 for the next output row's values, one request per 32-byte sector
+          // (augmented normalised Jv 1024^2 126.5 -> 117.9 us, 2048^2 479 -> 428 us; two rows
+          // ahead, an L1 hint, bulk L2 prefetches and the same for F(a): no further gain)
+          const unsigned o3 = o + EMHD_PFB * P.ny;
+#pragma unroll
+          for (int k = 0; k < 5; ++k)
+            if (k < P.nb) {
+#pragma unroll
+              for (int f = 0; f < NF; ++f)
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(P.bcol[k] + (o3 + f * plane)));
+            }
         }
       }
 #pragma unroll
