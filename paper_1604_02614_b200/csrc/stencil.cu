@@ -404,7 +404,7 @@ static bool two_raw_rows(int mode, const StencilParams& P, const StencilPath& se
   return sel.raw_rows == 2;
 }
 
-// HW (with two staged rows, 2 CTAs/SM): one extra warp per CTA does the strip's halo work (the
+// HW (with two staged rows; 4 CTAs/SM at 64 columns, 2 at 128): one extra warp per CTA does the strip's halo work (the
 // four halo columns' primitives and the two halo y-fluxes) beside the TY column threads, so no
 // column warp carries extra work into the per-row barrier
 template <int TY, int MODE, bool AUG, int FXY, int NR>
