@@ -105,8 +105,10 @@ def main():
             api = C_API.get(base_name(c["kernel"]))
             if base_name(c["kernel"]) == "update_kernel" and "<1" in c["kernel"]:
                 api = "emhd_update_finish"      # mode 1 (+ fused column bookkeeping)
-            if api and api not in traffic and "dram_read_bytes" in c:
-                traffic[api] = c["dram_read_bytes"] + c["dram_write_bytes"]
+            # a kernel profiled more than once (a real launch and a device-gated no-op of the
+            # second pass): keep the launch that moved the most bytes
+            if api and "dram_read_bytes" in c:
+                traffic[api] = max(traffic.get(api, 0.0), c["dram_read_bytes"] + c["dram_write_bytes"])
         with open(os.path.join(HERE, "traffic.json"), "w") as fh:
             json.dump(traffic, fh, indent=1)
         for c in caps:
